@@ -1,0 +1,234 @@
+"""Independent exact references that pin the split Bregman oracle — TEST INFRASTRUCTURE.
+
+None of these run the paper's iteration; each is a *plain definition* of the
+same quantity, so a dropped term, a wrong sign, a transposed operand or an index
+slip in ``hopf_oracle.c`` makes one of them disagree.
+
+Hopf formula (1.2)/(3.3), P:135-142 / P:815-818:
+    phi(x,t) = max_v { <x,v> - J*(v) - t H(v) },  grad phi = the unique maximiser.
+Hopf-Lax formula, P:640-646 and P:749-752 (H = support function of C):
+    phi(x,t) = min { J(z) : (x - z)/t in C },      grad phi = grad J(z*).
+C is the box prod_i [-w_i, w_i] for H = sum_i w_i |p_i|, the unit ball for H = ||p||_2.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+
+# --------------------------------------------------------------------------- diag, l1
+def diag_wl1_closed(x, t, D, c=None, gamma=0.0, w=None):
+    """Separable closed form for J = 1/2<x-c,D^{-1}(x-c)> + gamma, H = sum w_i|p_i|.
+
+    The ellipsoid/l1 computation of P:209-263 (a_i^2 = D_i; alpha_i = t w_i):
+    the Hopf objective decouples into 1-D problems 1/2 D_i v_i^2 + t w_i |v_i| - xt_i v_i
+    whose minimiser is shrink_1(xt_i, t w_i)/D_i, giving
+        grad_i = sign(xt_i) max(|xt_i| - t w_i, 0) / D_i
+        phi    = gamma + sum_i 1/2 max(|xt_i| - t w_i, 0)^2 / D_i.
+    """
+    x = np.asarray(x, np.float64)
+    D = np.asarray(D, np.float64)
+    xt = x - (0.0 if c is None else np.asarray(c, np.float64))
+    w = np.ones_like(D) if w is None else np.asarray(w, np.float64)
+    t = np.asarray(t, np.float64)[..., None]
+    s = np.maximum(np.abs(xt) - t * w, 0.0)
+    grad = np.sign(xt) * s / D
+    phi = gamma + 0.5 * np.sum(s * s / D, axis=-1)
+    return phi, grad
+
+
+# --------------------------------------------------------------------------- diag, l2
+def diag_l2_secular(x, t, D, c=None, gamma=0.0, iters=200):
+    """Exact phi, grad for J = 1/2<x-c,D^{-1}(x-c)> + gamma, H = ||.||_2.
+
+    Optimality of the Hopf objective (3.3): D v + t v/||v|| = xt for v != 0, i.e.
+    v_i = xt_i/(D_i + mu) with mu = t/||v|| > 0 the root of
+        g(mu) = mu^2 sum_i xt_i^2/(D_i+mu)^2 - t^2      (strictly increasing, 0 -> ||xt||^2 - t^2).
+    v = 0 iff ||xt|| <= t.  phi = <xt,v> - 1/2<v,Dv> - t||v|| + gamma
+                                = gamma + 1/2 sum_i D_i xt_i^2/(D_i+mu)^2.
+    D = I reduces to the sphere formula of P:306-310 (mu = t/(||x||-t)).
+    Solved by fp64 bisection on the bracket [t Dmin/(|xt|-t), t Dmax/(|xt|-t)].
+    """
+    x = np.atleast_2d(np.asarray(x, np.float64))
+    D = np.asarray(D, np.float64)
+    xt = x - (0.0 if c is None else np.asarray(c, np.float64))
+    t = np.broadcast_to(np.asarray(t, np.float64), (x.shape[0],))
+    r = np.linalg.norm(xt, axis=1)
+    phi = np.full(x.shape[0], float(gamma))
+    grad = np.zeros_like(xt)
+    for p in range(x.shape[0]):
+        if not r[p] > t[p]:
+            continue
+        lo = t[p] * D.min() / (r[p] - t[p])
+        hi = t[p] * D.max() / (r[p] - t[p])
+        xp = xt[p]
+        for _ in range(iters):
+            mid = 0.5 * (lo + hi)
+            g = mid * mid * np.sum(xp * xp / (D + mid) ** 2) - t[p] ** 2
+            if g > 0:
+                hi = mid
+            else:
+                lo = mid
+        mu = 0.5 * (lo + hi)
+        grad[p] = xp / (D + mu)
+        phi[p] = gamma + 0.5 * np.sum(D * xp * xp / (D + mu) ** 2)
+    return phi, grad
+
+
+# --------------------------------------------------------------------------- dense
+def box_qp_hopf_lax(x, t, A, w=None, gamma=0.0, sweeps=20000, tol=1e-15):
+    """phi = min { 1/2<z,Az> + gamma : |x_i - z_i| <= t w_i } by projected Gauss-Seidel.
+
+    Hopf-Lax for H = sum w_i |p_i| (C = box, P:465-496 with P:640-646).
+    grad phi = A z* (grad phi = grad H*(...) in dJ(z*)).  Independent of
+    split Bregman: exact coordinate minimisation of a strongly convex quadratic over a box.
+    """
+    x = np.asarray(x, np.float64)
+    A = np.asarray(A, np.float64)
+    n = x.size
+    w = np.ones(n) if w is None else np.asarray(w, np.float64)
+    lo, hi = x - t * w, x + t * w
+    z = np.clip(np.zeros(n), lo, hi)
+    g = A @ z
+    diag = np.diag(A).copy()
+    for _ in range(sweeps):
+        zmax = 0.0
+        for i in range(n):
+            zi = min(max(z[i] - g[i] / diag[i], lo[i]), hi[i])
+            dz = zi - z[i]
+            if dz != 0.0:
+                g += A[:, i] * dz
+                z[i] = zi
+                zmax = max(zmax, abs(dz))
+        if zmax <= tol:
+            break
+    g = A @ z
+    return 0.5 * z @ g + gamma, g, z
+
+
+def dual_lower_bound(x, t, v, Ainv, w=None, gamma=0.0, h="l1"):
+    """L(v) = <x,v> - J*(v) - t H(v) <= phi(x,t) for every v (weak duality of (3.3))."""
+    x, v = np.asarray(x, np.float64), np.asarray(v, np.float64)
+    Hv = np.linalg.norm(v) if h == "l2" else np.sum((1.0 if w is None else w) * np.abs(v))
+    return x @ v - 0.5 * v @ (Ainv @ v) + gamma - t * Hv
+
+
+def primal_upper_bound(x, t, v, A, Ainv, w=None, gamma=0.0):
+    """U(z) = J(z) >= phi(x,t) for the Hopf-Lax-feasible z = x - clip(x - A^{-1}v, -tw, tw)."""
+    x, v = np.asarray(x, np.float64), np.asarray(v, np.float64)
+    ww = np.ones_like(x) if w is None else np.asarray(w, np.float64)
+    z = x - np.clip(x - Ainv @ v, -t * ww, t * ww)
+    return 0.5 * z @ (A @ z) + gamma
+
+
+def box_qp_bruteforce(x, t, A, w=None, gamma=0.0):
+    """Exhaustive KKT active-set enumeration (3^n sets) of the box QP, n <= 8.
+
+    For every assignment of each coordinate to {lower bound, upper bound, free}
+    solve the equality-constrained QP and keep the feasible point with the
+    smallest J.  Brute force: no iteration, no tolerance.
+    """
+    x = np.asarray(x, np.float64)
+    A = np.asarray(A, np.float64)
+    n = x.size
+    w = np.ones(n) if w is None else np.asarray(w, np.float64)
+    lo, hi = x - t * w, x + t * w
+    best, bestz = np.inf, None
+    for pattern in itertools.product((0, 1, 2), repeat=n):
+        pat = np.array(pattern)
+        z = np.where(pat == 0, lo, np.where(pat == 1, hi, 0.0))
+        free = pat == 2
+        if free.any():
+            fixed = ~free
+            rhs = -A[np.ix_(free, fixed)] @ z[fixed]
+            z[free] = np.linalg.solve(A[np.ix_(free, free)], rhs)
+            if np.any(z[free] < lo[free] - 1e-12) or np.any(z[free] > hi[free] + 1e-12):
+                continue
+        val = 0.5 * z @ (A @ z)
+        if val < best:
+            best, bestz = val, z
+    return best + gamma, A @ bestz, bestz
+
+
+# --------------------------------------------------------------------------- brute force n <= 2
+def hopf_lax_grid_2d(x, t, J, h="l2", w=None, m=801):
+    """phi(x,t) = min_{p in C} J(x - t p) on a fine grid over C (n = 2), plus a local refine.
+
+    C = unit disc (H = l2) or the box [-w1,w1]x[-w2,w2] (H = weighted l1), P:465-496,
+    P:640-646.  J is any callable on an (k,2) array (e.g. a union min_k J_k).
+    """
+    x = np.asarray(x, np.float64)
+    w = np.ones(2) if w is None else np.asarray(w, np.float64)
+
+    def cands(c0, half, mm):
+        g = np.linspace(-1.0, 1.0, mm)
+        P = np.stack(np.meshgrid(c0[0] + half[0] * g, c0[1] + half[1] * g), -1).reshape(-1, 2)
+        if h == "l2":
+            nr = np.linalg.norm(P, axis=1)
+            P = np.where(nr[:, None] > 1.0, P / np.maximum(nr, 1e-300)[:, None], P)
+        else:
+            P = np.clip(P, -w, w)
+        return P
+
+    P = cands(np.zeros(2), w if h != "l2" else np.ones(2), m)
+    vals = J(x[None, :] - t * P)
+    best = np.argmin(vals)
+    p0, v0 = P[best], vals[best]
+    half = (w if h != "l2" else np.ones(2)) * (4.0 / (m - 1))
+    for _ in range(6):
+        P = cands(p0, half, 81)
+        vals = J(x[None, :] - t * P)
+        k = np.argmin(vals)
+        if vals[k] <= v0:
+            p0, v0 = P[k], vals[k]
+        half = half / 10.0
+    return float(v0), x - t * p0
+
+
+def hopf_dual_grid_2d(x, t, Jstar, Hfun, radius, m=801):
+    """phi = -min_v {J*(v) + t H(v) - <x,v>} on a grid |v_i| <= radius (n = 2), refined.
+
+    The Hopf formula (3.3) itself, minimised by exhaustive search.  Returns (phi, argmin v).
+    """
+    x = np.asarray(x, np.float64)
+
+    def obj(V):
+        return Jstar(V) + t * Hfun(V) - V @ x
+
+    c0 = np.zeros(2)
+    half = radius
+    best_v, best = None, np.inf
+    mm = m
+    for _ in range(7):
+        g = np.linspace(-1.0, 1.0, mm)
+        V = np.stack(np.meshgrid(c0[0] + half * g, c0[1] + half * g), -1).reshape(-1, 2)
+        vals = obj(V)
+        k = np.argmin(vals)
+        if vals[k] <= best:
+            best, best_v = vals[k], V[k]
+        c0 = best_v
+        half = half * 8.0 / (mm - 1)
+        mm = 81
+    return float(-best), best_v
+
+
+# --------------------------------------------------------------------------- union
+def union_exact(x, t, Dk, Ck, gammak, h="l2", w=None):
+    """phi = min_k phi_k with each phi_k from the exact single-set form
+    (translation: J_k(x) = J_0(x - c_k) => phi_k(x,t) = phi_0(x - c_k, t)).
+    Returns phi, grad of the lowest-index minimiser, kstar, phi_k."""
+    x = np.atleast_2d(np.asarray(x, np.float64))
+    K = len(gammak)
+    phik = np.empty((x.shape[0], K))
+    grads = []
+    for k in range(K):
+        if h == "l2":
+            p, g = diag_l2_secular(x, t, Dk[k], Ck[k], gammak[k])
+        else:
+            p, g = diag_wl1_closed(x, t, Dk[k], Ck[k], gammak[k], w)
+        phik[:, k] = p
+        grads.append(g)
+    kstar = np.argmin(phik, axis=1)
+    grad = np.stack([grads[k][i] for i, k in enumerate(kstar)])
+    return phik[np.arange(x.shape[0]), kstar], grad, kstar, phik

@@ -1,0 +1,347 @@
+/*
+ * hopf_oracle.c — TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct fp64 CPU implementation of the split Bregman
+ * evaluation of the Hopf formula (Darbon & Osher, arXiv 1605.01799).
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load this library.  It shares no code, header, table or
+ * constant generator with the CUDA product path (paper_1605_01799_b200/csrc).
+ *
+ * Citations are PAPER.md line numbers ("P:n") with the equation label.
+ *
+ *   Hopf formula (1.2)/(3.3), P:135-142, P:815-818:
+ *       phi(x,t) = -min_v { J*(v) + t H(v) - <x,v> }
+ *   Split Bregman (3.4a)-(3.4c), lambda, v0=d0=x, b0=0 at P:842-844:
+ *       v^{k+1} = argmin_v J*(v) - <x,v> + lambda/2 ||d^k - v - b^k||^2
+ *       d^{k+1} = argmin_d t H(d) + lambda/2 ||d - v^{k+1} - b^k||^2
+ *       b^{k+1} = b^k + v^{k+1} - d^{k+1}
+ *   Stopping rule, P:1595-1601 (squared l2 norms, all three, every iteration):
+ *       ||v^k-v^{k-1}||^2 <= tol  and ||d^k-d^{k-1}||^2 <= tol and ||d^k-v^k||^2 <= tol
+ *   shrink_1 (soft threshold), P:239-247 (sign(0)=+1 at P:1322);
+ *   shrink_2.
+ *   Quadratic prox.
+ *   Min over initial data (union).
+ *   Closest point y = x - t grad/||grad||.
+ *
+ * Readings of the paper: R1 grad := d at stop,
+ * R2 phi := Hopf objective at d, R3 tol on squared norms, R5 shifted problems
+ * solved centred at x - c with v0 = d0 = x - c, R6 t == 0 answered by J(x),
+ * R8 shrink at the threshold -> 0, R18 y := c_k* when grad == 0, R19 lowest k
+ * wins ties.
+ *
+ * Initial data handled:
+ *   diag : J(x) = 1/2 <x-c, D^{-1}(x-c)> + gamma,  J*(v) = 1/2<v,Dv> + <c,v> - gamma
+ *   dense: J(x) = 1/2 <x, A x> + gamma,            J*(v) = 1/2<v,A^{-1}v> - gamma
+ * Hamiltonians: H_L1 (sum |p_i|), H_WL1 (sum w_i |p_i|), H_L2 (||p||_2).
+ *
+ * Per-point status in iters[i] (same convention as the product ABI):
+ *   k >= 1 converged at iteration k; 0: t == 0; -max_iter: not converged;
+ *   INT32_MIN: invalid point (t < 0 or non-finite input), phi/grad = NaN.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_H_L1 0
+#define ORACLE_H_WL1 1
+#define ORACLE_H_L2 2
+
+/* ---------------- prox of t/lambda * H (3.4b) ---------------------------- */
+
+/* shrink_1 with per-coordinate threshold alpha_i. */
+static void shrink1(int n, const double *u, const double *alpha, double *out) {
+  for (int i = 0; i < n; i++) {
+    double a = fabs(u[i]) - alpha[i];
+    double s = (u[i] >= 0.0) ? 1.0 : -1.0; /* sign(0) = +1 */
+    out[i] = (a > 0.0) ? s * a : 0.0;      /* |u_i| <= alpha -> 0 */
+  }
+}
+
+/* shrink_2: u/||u|| * max(||u|| - alpha, 0); 0 if u == 0. */
+static void shrink2(int n, const double *u, double alpha, double *out) {
+  double r2 = 0.0;
+  for (int i = 0; i < n; i++) r2 += u[i] * u[i];
+  double r = sqrt(r2);
+  if (r == 0.0 || r - alpha <= 0.0) {
+    for (int i = 0; i < n; i++) out[i] = 0.0;
+    return;
+  }
+  double f = (r - alpha) / r;
+  for (int i = 0; i < n; i++) out[i] = u[i] * f;
+}
+
+static void prox_tH(int n, int h, const double *u, double t, const double *w,
+                    double lambda, double *alpha_buf, double *out) {
+  if (h == ORACLE_H_L2) {
+    shrink2(n, u, t / lambda, out);
+  } else {
+    for (int i = 0; i < n; i++)
+      alpha_buf[i] = t * (h == ORACLE_H_WL1 ? w[i] : 1.0) / lambda;
+    shrink1(n, u, alpha_buf, out);
+  }
+}
+
+static double H_of(int n, int h, const double *p, const double *w) {
+  double s = 0.0;
+  if (h == ORACLE_H_L2) {
+    for (int i = 0; i < n; i++) s += p[i] * p[i];
+    return sqrt(s);
+  }
+  for (int i = 0; i < n; i++) s += (h == ORACLE_H_WL1 ? w[i] : 1.0) * fabs(p[i]);
+  return s;
+}
+
+static double sqdist(int n, const double *a, const double *b) {
+  double s = 0.0;
+  for (int i = 0; i < n; i++) {
+    double e = a[i] - b[i];
+    s += e * e;
+  }
+  return s;
+}
+
+static int point_invalid(int n, const double *x, double t) {
+  if (!isfinite(t) || t < 0.0) return 1;
+  for (int i = 0; i < n; i++)
+    if (!isfinite(x[i])) return 1;
+  return 0;
+}
+
+/* ---------------- one point, diagonal J ---------------------------------- */
+/* Solves the problem centred at xt = x - c (reading R5), returns iters.
+ * v-update (3.4a) with J*(v) = 1/2<v,Dv> + <c,v> - gamma: setting the gradient
+ * D v + c - x - lambda (d - b - v) to zero gives
+ *     v = (D + lambda I)^{-1} (x - c + lambda (d - b)). */
+static int solve_diag_point(int n, const double *x, double t, const double *D,
+                            const double *c, double gamma, int h, const double *w,
+                            double lambda, int max_iter, double tol, double *phi,
+                            double *grad, double *ws) {
+  double *xt = ws, *v = ws + n, *d = ws + 2 * n, *b = ws + 3 * n;
+  double *vp = ws + 4 * n, *dp = ws + 5 * n, *u = ws + 6 * n, *al = ws + 7 * n;
+  if (point_invalid(n, x, t)) {
+    *phi = NAN;
+    for (int i = 0; i < n; i++) grad[i] = NAN;
+    return INT32_MIN;
+  }
+  for (int i = 0; i < n; i++) xt[i] = x[i] - (c ? c[i] : 0.0);
+  if (t == 0.0) { /* reading R6: phi(x,0) = J(x), grad = grad J(x) (1.1b) */
+    double J = gamma;
+    for (int i = 0; i < n; i++) {
+      J += 0.5 * xt[i] * xt[i] / D[i];
+      grad[i] = xt[i] / D[i];
+    }
+    *phi = J;
+    return 0;
+  }
+  /* v^0 = d^0 = x, b^0 = 0, in centred coordinates (R5). */
+  for (int i = 0; i < n; i++) {
+    v[i] = xt[i];
+    d[i] = xt[i];
+    b[i] = 0.0;
+  }
+  int iters = -max_iter;
+  for (int k = 1; k <= max_iter; k++) {
+    memcpy(vp, v, sizeof(double) * n);
+    memcpy(dp, d, sizeof(double) * n);
+    /* (3.4a) */
+    for (int i = 0; i < n; i++) v[i] = (xt[i] + lambda * (d[i] - b[i])) / (D[i] + lambda);
+    /* (3.4b): d = prox_{(t/lambda) H}(v + b) */
+    for (int i = 0; i < n; i++) u[i] = v[i] + b[i];
+    prox_tH(n, h, u, t, w, lambda, al, d);
+    /* (3.4c) */
+    for (int i = 0; i < n; i++) b[i] = b[i] + v[i] - d[i];
+    /* stopping rule P:1597-1601 */
+    if (sqdist(n, v, vp) <= tol && sqdist(n, d, dp) <= tol && sqdist(n, d, v) <= tol) {
+      iters = k;
+      break;
+    }
+  }
+  /* grad := d (R1); phi := -(J*(d) + t H(d) - <x,d>) (R2, (3.3)) */
+  double xd = 0.0, dDd = 0.0;
+  for (int i = 0; i < n; i++) {
+    xd += xt[i] * d[i];
+    dDd += d[i] * D[i] * d[i];
+    grad[i] = d[i];
+  }
+  *phi = xd - 0.5 * dDd - t * H_of(n, h, d, w) + gamma;
+  return iters;
+}
+
+static int nthreads_or_default(int nthreads) {
+#ifdef _OPENMP
+  return nthreads > 0 ? nthreads : omp_get_max_threads();
+#else
+  (void)nthreads;
+  return 1;
+#endif
+}
+
+int oracle_threads(int nthreads) { return nthreads_or_default(nthreads); }
+
+/* Batched diagonal-J evaluation. X: [M*n] row-major, t: [M]. */
+int oracle_diag(int64_t M, int n, const double *X, const double *t, const double *D,
+                const double *c, double gamma, int h, const double *w, double lambda,
+                int max_iter, double tol, double *phi, double *grad, int32_t *iters,
+                int nthreads) {
+  if (M < 0 || n < 1 || !D || lambda <= 0.0 || max_iter < 1 || tol < 0.0) return -1;
+  if (h == ORACLE_H_WL1 && !w) return -1;
+  int nt = nthreads_or_default(nthreads);
+#pragma omp parallel num_threads(nt)
+  {
+    double *ws = (double *)malloc(sizeof(double) * 8 * (size_t)n);
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t p = 0; p < M; p++)
+      iters[p] = solve_diag_point(n, X + p * n, t[p], D, c, gamma, h, w, lambda, max_iter,
+                                  tol, phi + p, grad + p * n, ws);
+    free(ws);
+  }
+  return 0;
+}
+
+/* ---------------- one point, dense SPD J --------------------------------- */
+/* v-update (3.4a) with J*(v) = 1/2<v,A^{-1}v> - gamma:
+ *     (A^{-1} + lambda I) v = x + lambda (d - b)  =>  v = M_lambda (x + lambda(d-b)),
+ * M_lambda = (A^{-1} + lambda I)^{-1} = P (I + ...)^{-1} P^T form of P:1336-1347,
+ * supplied precomputed in fp64 by the caller (oracle/__init__.py). */
+static int solve_dense_point(int n, const double *x, double t, const double *Ml,
+                             const double *A, const double *Ainv, double gamma, int h,
+                             const double *w, double lambda, int max_iter, double tol,
+                             double *phi, double *grad, double *ws) {
+  double *v = ws, *d = ws + n, *b = ws + 2 * n, *vp = ws + 3 * n, *dp = ws + 4 * n;
+  double *u = ws + 5 * n, *al = ws + 6 * n, *r = ws + 7 * n;
+  if (point_invalid(n, x, t)) {
+    *phi = NAN;
+    for (int i = 0; i < n; i++) grad[i] = NAN;
+    return INT32_MIN;
+  }
+  if (t == 0.0) { /* R6: J(x) = 1/2<x,Ax> + gamma, grad J = A x */
+    double J = gamma;
+    for (int i = 0; i < n; i++) {
+      double s = 0.0;
+      for (int j = 0; j < n; j++) s += A[(size_t)i * n + j] * x[j];
+      grad[i] = s;
+      J += 0.5 * x[i] * s;
+    }
+    *phi = J;
+    return 0;
+  }
+  for (int i = 0; i < n; i++) {
+    v[i] = x[i];
+    d[i] = x[i];
+    b[i] = 0.0;
+  }
+  int iters = -max_iter;
+  for (int k = 1; k <= max_iter; k++) {
+    memcpy(vp, v, sizeof(double) * n);
+    memcpy(dp, d, sizeof(double) * n);
+    for (int j = 0; j < n; j++) r[j] = x[j] + lambda * (d[j] - b[j]);
+    for (int i = 0; i < n; i++) { /* (3.4a) */
+      double s = 0.0;
+      for (int j = 0; j < n; j++) s += Ml[(size_t)i * n + j] * r[j];
+      v[i] = s;
+    }
+    for (int i = 0; i < n; i++) u[i] = v[i] + b[i];
+    prox_tH(n, h, u, t, w, lambda, al, d);                   /* (3.4b) */
+    for (int i = 0; i < n; i++) b[i] = b[i] + v[i] - d[i]; /* (3.4c) */
+    if (sqdist(n, v, vp) <= tol && sqdist(n, d, dp) <= tol && sqdist(n, d, v) <= tol) {
+      iters = k;
+      break;
+    }
+  }
+  double xd = 0.0, dAd = 0.0;
+  for (int i = 0; i < n; i++) {
+    double s = 0.0;
+    for (int j = 0; j < n; j++) s += Ainv[(size_t)i * n + j] * d[j];
+    xd += x[i] * d[i];
+    dAd += d[i] * s;
+    grad[i] = d[i];
+  }
+  *phi = xd - 0.5 * dAd - t * H_of(n, h, d, w) + gamma;
+  return iters;
+}
+
+int oracle_dense(int64_t M, int n, const double *X, const double *t, const double *Ml,
+                 const double *A, const double *Ainv, double gamma, int h, const double *w,
+                 double lambda, int max_iter, double tol, double *phi, double *grad,
+                 int32_t *iters, int nthreads) {
+  if (M < 0 || n < 1 || !Ml || !A || !Ainv || lambda <= 0.0 || max_iter < 1 || tol < 0.0)
+    return -1;
+  if (h == ORACLE_H_WL1 && !w) return -1;
+  int nt = nthreads_or_default(nthreads);
+#pragma omp parallel num_threads(nt)
+  {
+    double *ws = (double *)malloc(sizeof(double) * 8 * (size_t)n);
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t p = 0; p < M; p++)
+      iters[p] = solve_dense_point(n, X + p * n, t[p], Ml, A, Ainv, gamma, h, w, lambda,
+                                   max_iter, tol, phi + p, grad + p * n, ws);
+    free(ws);
+  }
+  return 0;
+}
+
+/* ---------------- union of K diagonal initial data ----------- */
+/* phi = min_k phi_k (lowest k on ties, R19); grad = grad of the winner;
+ * y = x - t grad/||grad|| (P:757-761 for H = l2), c_k* if grad = 0 (R18).
+ * Y is only defined for H = l2 (returns -1 otherwise when Y is requested). */
+int oracle_union(int64_t M, int n, int K, const double *X, const double *t, const double *Dk,
+                 const double *Ck, const double *gammak, int h, const double *w,
+                 double lambda, int max_iter, double tol, double *phi, double *grad,
+                 int32_t *iters, double *Y, int32_t *kstar, double *phik, int nthreads) {
+  if (M < 0 || n < 1 || K < 1 || !Dk || !Ck || !gammak || lambda <= 0.0 || max_iter < 1 ||
+      tol < 0.0)
+    return -1;
+  if (h == ORACLE_H_WL1 && !w) return -1;
+  if (Y && h != ORACLE_H_L2) return -1;
+  int nt = nthreads_or_default(nthreads);
+#pragma omp parallel num_threads(nt)
+  {
+    double *ws = (double *)malloc(sizeof(double) * 8 * (size_t)n);
+    double *g = (double *)malloc(sizeof(double) * (size_t)n);
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t p = 0; p < M; p++) {
+      const double *x = X + p * n;
+      double best = INFINITY;
+      int bestk = -1, bestit = 0;
+      double *gout = grad + p * n;
+      for (int k = 0; k < K; k++) {
+        double ph;
+        int it = solve_diag_point(n, x, t[p], Dk + (size_t)k * n, Ck + (size_t)k * n,
+                                  gammak[k], h, w, lambda, max_iter, tol, &ph, g, ws);
+        if (phik) phik[p * K + k] = ph;
+        if (it == INT32_MIN) { bestk = -1; bestit = INT32_MIN; break; }
+        if (ph < best) { /* strict: lowest k wins ties (R19) */
+          best = ph;
+          bestk = k;
+          bestit = it;
+          memcpy(gout, g, sizeof(double) * n);
+        }
+      }
+      if (bestk < 0) {
+        phi[p] = NAN;
+        for (int i = 0; i < n; i++) gout[i] = NAN;
+        iters[p] = INT32_MIN;
+        if (kstar) kstar[p] = -1;
+        if (Y) for (int i = 0; i < n; i++) Y[p * n + i] = NAN;
+        continue;
+      }
+      phi[p] = best;
+      iters[p] = bestit;
+      if (kstar) kstar[p] = bestk;
+      if (Y) {
+        double gn = 0.0;
+        for (int i = 0; i < n; i++) gn += gout[i] * gout[i];
+        gn = sqrt(gn);
+        for (int i = 0; i < n; i++)
+          Y[p * n + i] = (gn > 0.0) ? x[i] - t[p] * gout[i] / gn : Ck[(size_t)bestk * n + i];
+      }
+    }
+    free(g);
+    free(ws);
+  }
+  return 0;
+}

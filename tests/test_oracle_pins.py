@@ -1,0 +1,281 @@
+"""Pins of the fp64 oracle (oracle/hopf_oracle.c) to things other than itself.
+
+Each test compares the split Bregman oracle with a plain definition of the same
+quantity from the paper (closed forms, the secular equation, Hopf-Lax box QP,
+weak-duality certificates, exhaustive search, PDE invariants).  A dropped term,
+a wrong sign, a wrong index or a transposed operand in the oracle fails at least
+one of them.  "tight" runs use tol = 1e-26 on the squared norms so the iterate
+is at the fixed point to fp64 precision; "paper" runs use tol = 1e-8.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import exact
+from paper_1605_01799_b200 import inputs
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")
+TIGHT = dict(tol=1e-26, max_iter=200000)
+
+
+def _diag_case(case):
+    n = case["n"]
+    D = np.broadcast_to(np.asarray(case["D"], float), (n,)).copy()
+    return n, D
+
+
+@pytest.mark.parametrize("case", json.load(open(GOLD))["cases"], ids=lambda c: c["name"])
+def test_golden_paper_examples(case):
+    n, D = _diag_case(case)
+    X = np.asarray(case["x"], float)[None, :]
+    t = np.asarray([case["t"]])
+    for kw in (TIGHT, dict(tol=1e-8, max_iter=1000)):
+        phi, g, it = oracle.eval_diag(X, t, D, None, case["gamma"], case["h"], **kw)
+        assert it[0] >= 1
+        assert abs(phi[0] - case["phi"]) <= 1e-9, (phi, case)
+        np.testing.assert_allclose(g[0], case["grad"], atol=1e-9 if kw is TIGHT else 2e-4)
+
+
+def test_c1_closed_form_and_three_iterations():
+    """C1: J = 1/2||x||^2, H = l1: phi = 1/2 sum max(|x_i|-t,0)^2, grad = shrink_1(x,t)
+    (P:248-263 with a_i = 1, constant dropped).  With lambda = 1 the iteration is exact
+    after two steps and the paper's test fires at k = 3 (v1 = x, d1 = d2 = shrink, v2 = v3 = d1)."""
+    wl = inputs.config("c1")
+    X, t = inputs.points(wl)
+    phi, g, it = oracle.eval_diag(X, t, wl.D, None, wl.gamma, "l1")
+    pe, ge = exact.diag_wl1_closed(X, t, wl.D)
+    assert np.all(it == 3)
+    np.testing.assert_allclose(phi, pe, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(g, ge, rtol=0, atol=1e-12)
+    # same for H = l2 (shrink_2): exact after two steps as well
+    phi2, g2, it2 = oracle.eval_diag(X, t, wl.D, None, 0.0, "l2")
+    pe2, ge2 = exact.diag_l2_secular(X, t, wl.D)
+    assert np.all(it2 == 3)
+    np.testing.assert_allclose(phi2, pe2, atol=1e-12)
+    np.testing.assert_allclose(g2, ge2, atol=1e-12)
+
+
+def test_c2_weighted_l1_ellipsoid_closed_form():
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 400)
+    pe, ge = exact.diag_wl1_closed(X, t, wl.D, None, wl.gamma, wl.w)
+    phi, g, it = oracle.eval_diag(X, t, wl.D, None, wl.gamma, "wl1", wl.w, **TIGHT)
+    np.testing.assert_allclose(phi, pe, atol=1e-11)
+    np.testing.assert_allclose(g, ge, atol=1e-10)
+    # the paper's tolerance: within the north_star parity budget of the exact answer
+    phi, g, it = oracle.eval_diag(X, t, wl.D, None, wl.gamma, "wl1", wl.w)
+    assert np.all(it > 0)
+    assert np.max(np.abs(phi - pe) / np.maximum(1, np.abs(pe))) < 1e-6
+    assert np.max(np.abs(g - ge)) < 1e-3
+
+
+def test_c3_l2_secular_equation():
+    wl = inputs.config("c3")
+    X, t = inputs.points(wl, 0, 40)
+    pe, ge = exact.diag_l2_secular(X, t, wl.D, None, wl.gamma)
+    phi, g, it = oracle.eval_diag(X, t, wl.D, None, wl.gamma, "l2", **TIGHT)
+    np.testing.assert_allclose(phi, pe, atol=1e-11)
+    np.testing.assert_allclose(g, ge, atol=1e-10)
+    phi, g, it = oracle.eval_diag(X, t, wl.D, None, wl.gamma, "l2")
+    assert np.all(it > 0)
+    assert np.max(np.abs(g - ge)) < 1e-3
+
+
+@pytest.mark.parametrize("lam", [0.5, 2.0])
+@pytest.mark.parametrize("h", ["wl1", "l2"])
+def test_lambda_does_not_move_the_fixed_point(lam, h):
+    """Any lambda > 0 converges to the same minimiser."""
+    rng = np.random.default_rng(7)
+    n, M = 12, 30
+    D = rng.uniform(0.3, 3.0, n)
+    c = rng.normal(size=n)
+    w = rng.uniform(0.5, 1.5, n)
+    X = rng.normal(scale=2.0, size=(M, n))
+    t = rng.uniform(0.0, 2.0, M)
+    phi, g, it = oracle.eval_diag(X, t, D, c, 0.3, h, w, lam=lam, **TIGHT)
+    if h == "l2":
+        pe, ge = exact.diag_l2_secular(X, t, D, c, 0.3)
+    else:
+        pe, ge = exact.diag_wl1_closed(X, t, D, c, 0.3, w)
+    np.testing.assert_allclose(phi, pe, atol=1e-10)
+    np.testing.assert_allclose(g, ge, atol=1e-9)
+
+
+def test_dense_identity_rotation_reduces_to_separable():
+    """Q = I: A = diag(Lam) => grad_i = Lam_i shrink_1(x,t)_i, phi = 1/2 sum Lam_i max(|x_i|-t,0)^2."""
+    rng = np.random.default_rng(3)
+    n, M = 16, 50
+    Lam = np.exp(rng.uniform(np.log(0.1), np.log(10), n))
+    X = rng.normal(size=(M, n))
+    t = rng.uniform(0.1, 1.0, M)
+    phi, g, it = oracle.eval_dense(X, t, np.eye(n), Lam, **TIGHT)
+    pe, ge = exact.diag_wl1_closed(X, t, 1.0 / Lam)
+    np.testing.assert_allclose(phi, pe, atol=1e-10)
+    np.testing.assert_allclose(g, ge, atol=1e-9)
+
+
+def test_dense_against_box_qp_bruteforce():
+    """Random rotation, n = 5: exhaustive 3^n active-set enumeration of the Hopf-Lax box QP."""
+    rng = np.random.default_rng(11)
+    n = 5
+    Q = inputs.haar_orthogonal(rng, n)
+    Lam = np.exp(rng.uniform(np.log(0.1), np.log(10), n))
+    A = (Q * Lam) @ Q.T
+    X = rng.normal(size=(12, n))
+    t = rng.uniform(0.1, 1.0, 12)
+    w = rng.uniform(0.5, 1.5, n)
+    for h, ww in (("l1", None), ("wl1", w)):
+        phi, g, it = oracle.eval_dense(X, t, Q, Lam, 0.25, h, ww, **TIGHT)
+        for p in range(X.shape[0]):
+            pb, gb, _ = exact.box_qp_bruteforce(X[p], t[p], A, ww, 0.25)
+            assert abs(phi[p] - pb) < 1e-10
+            np.testing.assert_allclose(g[p], gb, atol=1e-8)
+
+
+def test_dense_c4_duality_certificate():
+    """C4 law at n = 256: L(v) <= phi <= U(z) with a certified gap, and the box-QP
+    coordinate-descent Hopf-Lax solve agrees."""
+    wl = inputs.config("c4")
+    X, t = inputs.points(wl, 0, 6)
+    A, Ainv, Ml = oracle.dense_matrices(wl.Q, wl.Lam)
+    phi, g, it = oracle.eval_dense(X, t, wl.Q, wl.Lam, **TIGHT)
+    lmax = wl.Lam.max()
+    for p in range(X.shape[0]):
+        L = exact.dual_lower_bound(X[p], t[p], g[p], Ainv)
+        U = exact.primal_upper_bound(X[p], t[p], g[p], A, Ainv)
+        assert L - 1e-9 <= phi[p] <= U + 1e-9
+        assert U - L < 1e-9
+        # ||v - v*||^2 <= 2 lambda_max(A) (U - L) (strong convexity of J*)
+    pq, gq, _ = exact.box_qp_hopf_lax(X[0], t[0], A, sweeps=4000, tol=1e-14)
+    assert abs(pq - phi[0]) < 1e-8
+    np.testing.assert_allclose(gq, g[0], atol=1e-6)
+    # paper tolerance: within budget
+    phi8, g8, it8 = oracle.eval_dense(X, t, wl.Q, wl.Lam)
+    assert np.all(it8 > 0)
+    assert np.max(np.abs(g8 - g)) < 1e-3
+    assert np.max(np.abs(phi8 - phi) / np.maximum(1, np.abs(phi))) < 1e-6
+
+
+def test_union_c5_secular_and_closest_point():
+    wl = inputs.config("c5")
+    X, t = inputs.points(wl, 0, 30)
+    Dk, Ck, gk = wl.Dk.astype(float), wl.Ck.astype(float), wl.gammak.astype(float)
+    pe, ge, kse, pke = exact.union_exact(X, t, Dk, Ck, gk, "l2")
+    phi, g, it, Y, ks, pk = oracle.eval_union(X, t, Dk, Ck, gk, "l2", **TIGHT)
+    np.testing.assert_allclose(pk, pke, atol=1e-10)
+    np.testing.assert_allclose(phi, pe, atol=1e-10)
+    assert np.array_equal(ks, kse)
+    np.testing.assert_allclose(g, ge, atol=1e-9)
+    # closest / Hopf-Lax point: ||x - y|| = t and J_k*(y) = phi when grad != 0
+    for p in range(X.shape[0]):
+        k = ks[p]
+        Jy = 0.5 * np.sum((Y[p] - Ck[k]) ** 2 / Dk[k]) + gk[k]
+        if np.linalg.norm(g[p]) > 0:
+            assert abs(np.linalg.norm(X[p] - Y[p]) - t[p]) < 1e-9
+            assert abs(Jy - phi[p]) < 1e-8
+        else:
+            np.testing.assert_allclose(Y[p], Ck[k])
+
+
+def test_union_fig4_fixture():
+    """Fig. 4: J = min(1/2||x||^2 - <b,x>, 1/2||x||^2 + <b,x>), b = 1^8, H = l1.
+    Branch k is D = 1, c = +-b, gamma = -1/2||b||^2; closed form per branch; iters = 3."""
+    n = 8
+    b = np.ones(n)
+    Dk = np.ones((2, n))
+    Ck = np.stack([b, -b])
+    gk = np.full(2, -0.5 * b @ b)
+    rng = np.random.default_rng(5)
+    X = rng.uniform(-20, 20, (200, n))
+    t = rng.uniform(0, 15, 200)
+    phi, g, it, Y, ks, pk = oracle.eval_union(X, t, Dk, Ck, gk, "l1", want_y=False)
+    for k in range(2):
+        pe, _ = exact.diag_wl1_closed(X, t, Dk[k], Ck[k], gk[k])
+        np.testing.assert_allclose(pk[:, k], pe, atol=1e-10)
+    np.testing.assert_allclose(phi, pk.min(axis=1), atol=0)
+    assert np.all((it == 3) | (it == 0))
+
+
+@pytest.mark.parametrize("h", ["l1", "wl1", "l2"])
+def test_bruteforce_n2_hopf_and_hopf_lax(h):
+    """n = 2: the oracle matches (i) the Hopf formula (3.3) minimised by exhaustive grid search
+    over v and (ii) the Hopf-Lax formula min_{z in x - tC} J(z) by grid search (north_star)."""
+    rng = np.random.default_rng(19)
+    D = np.array([0.7, 1.8])
+    c = np.array([0.3, -0.4])
+    w = np.array([0.6, 1.4]) if h == "wl1" else np.ones(2)
+    gamma = -0.5
+    for _ in range(6):
+        x = rng.normal(scale=2.0, size=2)
+        t = rng.uniform(0.2, 1.5)
+        phi, g, it = oracle.eval_diag(x[None], np.array([t]), D, c, gamma, h, w, **TIGHT)
+        Jstar = lambda V: 0.5 * np.sum(D * V * V, axis=1) + V @ c - gamma
+        Hf = (lambda V: np.linalg.norm(V, axis=1)) if h == "l2" else (lambda V: np.abs(V) @ w)
+        pd, vd = exact.hopf_dual_grid_2d(x, t, Jstar, Hf, radius=10.0)
+        J = lambda Z: 0.5 * np.sum((Z - c) ** 2 / D, axis=1) + gamma
+        pl, _ = exact.hopf_lax_grid_2d(x, t, J, "l2" if h == "l2" else "box", w)
+        assert abs(phi[0] - pd) < 1e-7, (phi, pd)
+        assert abs(phi[0] - pl) < 1e-7, (phi, pl)
+        np.testing.assert_allclose(g[0], vd, atol=1e-4)
+
+
+def test_bruteforce_n2_union_hopf_lax():
+    """Union of two ellipses in n = 2: min_k phi_k equals Hopf-Lax with J = min_k J_k."""
+    rng = np.random.default_rng(23)
+    Dk = np.array([[0.5, 2.0], [1.5, 0.7]])
+    Ck = np.array([[2.0, 0.0], [-1.0, 1.5]])
+    gk = np.array([-0.5, -0.5])
+    J = lambda Z: np.min(np.stack([0.5 * np.sum((Z - Ck[k]) ** 2 / Dk[k], axis=1) + gk[k]
+                                   for k in range(2)]), axis=0)
+    for _ in range(6):
+        x = rng.normal(scale=3.0, size=2)
+        t = rng.uniform(0.2, 1.5)
+        phi, g, it, Y, ks, pk = oracle.eval_union(x[None], np.array([t]), Dk, Ck, gk, "l2", **TIGHT)
+        pl, yl = exact.hopf_lax_grid_2d(x, t, J, "l2")
+        assert abs(phi[0] - pl) < 1e-7
+        if np.linalg.norm(g[0]) > 0:
+            np.testing.assert_allclose(Y[0], yl, atol=1e-4)
+
+
+def test_invariants_initial_value_monotone_fd_gradient_pde():
+    """phi(x,0+) = J(x); t -> phi nonincreasing (dphi/dt = -H(grad) <= 0);
+    grad = central differences of phi in x; PDE residual dphi/dt + H(grad phi) = 0."""
+    rng = np.random.default_rng(29)
+    n = 6
+    D = rng.uniform(0.5, 2.0, n)
+    w = rng.uniform(0.5, 1.5, n)
+    gamma = -0.5
+    for h in ("wl1", "l2"):
+        Hf = (lambda p: np.linalg.norm(p)) if h == "l2" else (lambda p: np.abs(p) @ w)
+        for _ in range(5):
+            x = rng.normal(scale=2.0, size=n)
+            J = 0.5 * np.sum(x * x / D) + gamma
+            ev = lambda X, T: oracle.eval_diag(np.atleast_2d(X), np.atleast_1d(T), D, None,
+                                               gamma, h, w, **TIGHT)
+            assert abs(ev(x, 1e-9)[0][0] - J) < 1e-7
+            assert ev(x, 0.0)[2][0] == 0 and abs(ev(x, 0.0)[0][0] - J) < 1e-12
+            ts = np.linspace(0.05, 3.0, 12)
+            ph = ev(np.repeat(x[None], 12, 0), ts)[0]
+            assert np.all(np.diff(ph) <= 1e-12)
+            t = 0.7
+            phi, g, _ = ev(x, t)
+            hs = 1e-5
+            E = np.eye(n) * hs
+            fd = (ev(x[None] + E, np.full(n, t))[0] - ev(x[None] - E, np.full(n, t))[0]) / (2 * hs)
+            np.testing.assert_allclose(fd, g[0], atol=1e-6)
+            dt = (ev(x, t + hs)[0][0] - ev(x, t - hs)[0][0]) / (2 * hs)
+            assert abs(dt + Hf(g[0])) < 1e-6
+
+
+def test_status_codes_nonconvergence_and_invalid():
+    X = np.array([[3.0, -1.0], [1.0, 2.0], [np.nan, 0.0], [1.0, 1.0]])
+    t = np.array([0.5, -1.0, 0.5, 0.0])
+    D = np.array([1.3, 0.6])
+    phi, g, it = oracle.eval_diag(X, t, D, None, 0.0, "l2", max_iter=2)
+    assert it[0] == -2 and np.isfinite(phi[0])           # not converged in 2 iterations
+    assert it[1] == oracle.INVALID and np.isnan(phi[1])  # t < 0
+    assert it[2] == oracle.INVALID and np.all(np.isnan(g[2]))
+    assert it[3] == 0 and abs(phi[3] - 0.5 * np.sum(X[3] ** 2 / D)) < 1e-15
