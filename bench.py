@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark of the batched Hopf-formula evaluator (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+Metric: Hopf evaluations per second (phi and grad phi written) at n = 1000 — BASELINE config 3
+(J = 1/2(<x,D^-1 x> - 1), H = ||.||_2, M = 1e5 points per GPU, x ~ N(0,I), t ~ U[0,2]).
+A "step" is one pass of the whole hot path (stage, (3.4a), (3.4b), (3.4c),
+stopping test with masking/refill, phi/grad output) over one batch of M points = one
+hopf_eval_diag launch.  Multi-GPU (torchrun): every rank evaluates its own M points (weak
+scaling, shards by global index, no data-path collective); the time is the max over ranks.
+
+value      device throughput with X, t resident in HBM (inputs 400 MB > 126 MB L2, no flush needed)
+e2e        same metric through hopf_eval_diag_host: pinned host X,t -> device -> host phi,grad,iters
+roofline   dominant kernel vs the FP32 ALU peak (148 SMs x 128 lanes x 2 flop x 1965 MHz)
+cpu_baseline  the fp64 oracle (oracle/, as it stands) on the host cores, bounded sample
+--impl reference  times that oracle as the reference arm (rank 0 only under torchrun)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1605_01799_b200 import inputs  # noqa: E402
+
+METRIC = "Hopf evals/sec (phi+grad phi) at n=1000"
+UNIT = "evals/s"
+SM_COUNT_NOMINAL = 148
+FP32_LANES_PER_SM = 128
+# algorithmic FP32 flops per coordinate-iteration: update + the paper's test
+FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14}
+# per-point HBM bytes: x (4n) + grad (4n) + t, phi, iters (12)
+CPU_SAMPLE = {"c1": 1024, "c2": 200_000, "c3": 12_000, "c4": 1024, "c5": 8_000}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def clocks_sampler(uuid):
+    q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    try:
+        return subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                 "-lms", "100"] + (["-i", uuid] if uuid else []),
+                                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except Exception:
+        return None
+
+
+def clocks_summary(proc):
+    if proc is None:
+        return None
+    proc.terminate()
+    try:
+        out, _ = proc.communicate(timeout=5)
+    except Exception:
+        proc.kill()
+        return None
+    sm, smax, reasons = [], [], set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in out.strip().splitlines():
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 7:
+            continue
+        try:
+            sm.append(float(f[0]))
+            smax.append(float(f[1]))
+        except ValueError:
+            continue
+        for nm, v in zip(names, f[3:7]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def load_traffic(config):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+def cpu_baseline_run(wl, sample):
+    import oracle
+    X, t = inputs.points(wl, 0, sample)
+    t0 = time.perf_counter()
+    if wl.kind == "diag":
+        oracle.eval_diag(X, t, wl.D, wl.c, wl.gamma, wl.h, wl.w, lam=wl.lam,
+                         max_iter=wl.max_iter, tol=wl.tol)
+    elif wl.kind == "union":
+        oracle.eval_union(X, t, wl.Dk, wl.Ck, wl.gammak, wl.h, lam=wl.lam, max_iter=wl.max_iter,
+                          tol=wl.tol)
+    else:
+        oracle.eval_dense(X, t, wl.Q, wl.Lam, wl.gamma, wl.h, lam=wl.lam, max_iter=wl.max_iter,
+                          tol=wl.tol)
+    dt = time.perf_counter() - t0
+    return sample / dt, dt, oracle.threads()
+
+
+def run_reference(args, wl):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    sample = args.cpu_sample or CPU_SAMPLE[wl.name]
+    for _ in range(args.warmup):
+        cpu_baseline_run(wl, max(1, sample // 8))
+    times = []
+    for _ in range(args.steps):
+        v, dt, cores = cpu_baseline_run(wl, sample)
+        times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    value = sample / (ms / 1e3)
+    line = {"metric": METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={wl.n})",
+            "value": value, "unit": UNIT, "impl": "reference", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE law)",
+            "config": config_dict(wl, ws),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"first {sample} points of {wl.name} per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(wl, ws):
+    d = {"workload": f"{wl.name}: n={wl.n}, M={wl.M} points per GPU, H={wl.h}, J={wl.kind}",
+         "n": wl.n, "M_per_gpu": wl.M, "global_points": wl.M * ws, "lambda": wl.lam,
+         "tol": wl.tol, "max_iter": wl.max_iter, "parallelism": f"dp{ws} (point shards)",
+         "l2_flush": "none needed: per-step inputs+outputs exceed the 126 MB L2"}
+    if wl.kind == "union":
+        d["K"] = wl.K
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--M", type=int, default=None, help="points per GPU (default: the config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    wl = inputs.config(args.config, M=args.M)
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1605_01799_b200 as hb
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = hb.lib()
+
+    # ---- inputs: this rank's shard of the global points (generated by global index) ----------
+    M = wl.M
+    r0 = rank * M
+    wl_g = inputs.config(args.config, M=M * ws)
+    Xh, th = inputs.points(wl_g, r0, r0 + M)
+    X = torch.from_numpy(Xh).to(dev)
+    t = torch.from_numpy(th).to(dev)
+    n = wl.n
+    f32 = lambda a: None if a is None else torch.as_tensor(a, dtype=torch.float32, device=dev)
+    phi = torch.empty(M, device=dev)
+    grad = torch.empty((M, n), device=dev)
+    iters = torch.empty(M, dtype=torch.int32, device=dev)
+    out = (phi, grad, iters)
+    stream = torch.cuda.current_stream(dev)
+
+    if wl.kind == "diag":
+        D, c, w = f32(wl.D), f32(wl.c), f32(wl.w)
+        step = lambda: hb.eval_diag(X, t, D, c, wl.gamma, wl.h, w, wl.lam, wl.max_iter, wl.tol,
+                                    out=out, stream=stream)
+    elif wl.kind == "union":
+        Dk, Ck, gk = f32(wl.Dk), f32(wl.Ck), f32(wl.gammak)
+        Y = torch.empty((M, n), device=dev)
+        kst = torch.empty(M, dtype=torch.int32, device=dev)
+
+        def step():
+            rc = L.hopf_eval_union(M, n, wl.K, X.data_ptr(), t.data_ptr(), Dk.data_ptr(),
+                                   Ck.data_ptr(), gk.data_ptr(), hb.H_KINDS[wl.h], None,
+                                   float(wl.lam), wl.max_iter, float(wl.tol), phi.data_ptr(),
+                                   grad.data_ptr(), iters.data_ptr(), Y.data_ptr(),
+                                   kst.data_ptr(), None, stream.cuda_stream)
+            hb._check(rc, "hopf_eval_union")
+    else:
+        plan = hb.DensePlan(wl.Q, wl.Lam, wl.lam)
+        step = lambda: hb.eval_dense(X, t, plan, wl.gamma, wl.h, None, wl.max_iter, wl.tol,
+                                     out=out, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    iters_np = iters.cpu().numpy()
+    launches_per_step = hb.last_launch_count()
+
+    uuid = None
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:
+        pass
+    smi = clocks_sampler(uuid)
+    time.sleep(0.3)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    clocks = clocks_summary(smi)
+    ms_total = ev0.elapsed_time(ev1)
+    if ws > 1:
+        tm = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ms_total = float(tm.item())
+    ms_step = ms_total / args.steps
+    value = M * ws / (ms_step / 1e3)
+
+    # ---- end to end through the host-buffer entry point (diag path) ----------------------------
+    e2e = None
+    if not args.no_e2e and wl.kind == "diag":
+        Xp = torch.from_numpy(Xh).pin_memory()
+        tp = torch.from_numpy(th).pin_memory()
+        outh = (torch.empty(M, pin_memory=True), torch.empty((M, n), pin_memory=True),
+                torch.empty(M, dtype=torch.int32, pin_memory=True))
+        Dd, cd, wd = f32(wl.D), f32(wl.c), f32(wl.w)
+        e2e_step = lambda: hb.eval_diag_host(Xp, tp, Dd, cd, wl.gamma, wl.h, wd, wl.lam,
+                                             wl.max_iter, wl.tol, out=outh)
+        for _ in range(2):
+            e2e_step()
+        if ws > 1:
+            dist.barrier()
+        ksteps = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(ksteps):
+            e2e_step()
+        el = time.perf_counter() - t0   # the call is synchronous: results are in host memory
+        if ws > 1:
+            tm = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            el = float(tm.item())
+        e2e = {"value": M * ws * ksteps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(Xp.numel() * 4 + tp.numel() * 4),
+               "d2h_bytes_per_step": int(M * 4 + M * n * 4 + M * 4),
+               "api": "hopf_eval_diag_host (pinned host buffers, chunked H2D/kernel/D2H pipeline)"}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel ---------------------------------------------------
+    peaks = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    conv = iters_np[iters_np > 0]
+    roof = None
+    if wl.kind in ("diag", "union"):
+        it_sum = float(np.abs(iters_np[iters_np != inputs_invalid()]).sum())
+        if wl.kind == "union":
+            it_sum = float("nan")  # per-set counts are not returned; see DESIGN.md
+        flops = it_sum * n * FLOPS_PER_COORD_ITER[wl.h]
+        achieved = flops / (ms_step / 1e3) / 1e12
+        peak = sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": load_traffic(wl.name),
+                "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (guide unit "
+                              "counts, max SM clock)",
+                "algorithmic_flops_per_launch": flops,
+                "flops_per_coord_iter": FLOPS_PER_COORD_ITER[wl.h],
+                "mean_iters": float(conv.mean()) if conv.size else None,
+                "hbm_bytes_per_launch": M * (8 * n + 12),
+                "hbm_GBps": M * (8 * n + 12) / (ms_step / 1e3) / 1e9}
+        if clocks:
+            roof["frac_at_measured_clock"] = achieved / (sms * FP32_LANES_PER_SM * 2 *
+                                                         clocks["sm_mhz"] * 1e6 / 1e12)
+    else:
+        flops = float(np.abs(iters_np).sum()) * 2.0 * n * n
+        achieved = flops / (ms_step / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "unit": "TFLOP/s",
+                "peak": sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12,
+                "traffic": load_traffic(wl.name), "note": "v1 SIMT FP32 dense GEMM; flops = 2 n^2 "
+                "per point-iteration (the v-update GEMM)"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        sample = args.cpu_sample or CPU_SAMPLE[wl.name]
+        v, dt, cores = cpu_baseline_run(wl, sample)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {sample} points of {wl.name} ({dt:.1f} s of fp64 oracle)"}
+
+    line = {"metric": METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={n})",
+            "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded; BASELINE config law)", "config": config_dict(wl, ws),
+            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "iters": {"min": int(conv.min()) if conv.size else None,
+                      "mean": float(conv.mean()) if conv.size else None,
+                      "max": int(conv.max()) if conv.size else None,
+                      "nonconverged": int(np.sum((iters_np < 0) & (iters_np != inputs_invalid())))}}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def inputs_invalid():
+    return -(2 ** 31)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

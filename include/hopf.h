@@ -1,0 +1,137 @@
+/*
+ * hopf.h — C ABI of the B200-native batched Hopf-formula evaluator (libhopf.so).
+ *
+ * For M independent queries (x, t) in R^n the library evaluates the Hopf formula
+ *     phi(x,t) = -min_v { J*(v) + t H(v) - <x,v> }              PAPER.md (1.2)/(3.3)
+ * and its gradient grad phi(x,t) = the unique minimiser
+ * by split Bregman iterations
+ *     v^{k+1} = argmin_v J*(v) - <x,v> + lambda/2 ||d^k - v - b^k||^2     (3.4a) P:834-836
+ *     d^{k+1} = argmin_d t H(d) + lambda/2 ||d - v^{k+1} - b^k||^2         (3.4b) P:837-839
+ *     b^{k+1} = b^k + v^{k+1} - d^{k+1}                                    (3.4c) P:840
+ * started at v^0 = d^0 = x, b^0 = 0 and stopped at the first k with
+ *     ||v^k - v^{k-1}||^2 <= tol, ||d^k - d^{k-1}||^2 <= tol, ||d^k - v^k||^2 <= tol.
+ * (3.4b) is the prox of a 1-homogeneous H: shrink_1 or shrink_2
+ * via Moreau's identity.  (3.4a) is the quadratic prox.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Array pointers are DEVICE pointers (except where a name ends in _host), caller-allocated
+ *    and caller-owned, row-major point-major: X[i*n + j] is coordinate j of point i.
+ *    fp32 unless stated.  The library never allocates, frees or retains caller memory.
+ *  - Calls validate host-side arguments, enqueue their kernels on `stream` and return
+ *    (asynchronous).  Outputs are valid once `stream` has been synchronised.
+ *  - Return codes: HOPF_OK (0); HOPF_EINVAL (-1) invalid argument (M < 0, n < 1, K < 1,
+ *    a required pointer NULL, lambda <= 0 or non-finite, tol < 0 or non-finite,
+ *    max_iter < 1, unknown H kind, w NULL for HOPF_H_WL1, lambda different from the
+ *    plan's, Y requested with a non-l2 H); HOPF_EUNSUPPORTED (-2) shape outside the
+ *    compiled kernels (e.g. n > 1024 for the diagonal kernels, n != 256-multiple for dense);
+ *    HOPF_ECUDA (-3) a CUDA launch/runtime error (hopf_last_error() has the text).
+ *    M == 0 is a successful no-op.  Device-resident parameter values (D <= 0, NaN) are not
+ *    validated on the host.
+ *  - Per-point status iters[i]: k >= 1 converged at iteration k (the paper's test);
+ *    0: t[i] == 0, answered directly as phi = J(x), grad = grad J(x) (Hopf needs t > 0,
+ *    P:106-107); -max_iter: not converged, phi/grad from the last d are still written;
+ *    INT32_MIN: invalid point (t < 0 or a non-finite x/t coordinate), phi/grad = NaN.
+ *  - Outputs: grad := d at termination (reading R1 of DESIGN.md); phi := the Hopf
+ *    objective (3.3) evaluated at d (R2).
+ *  - Thread safety: calls on different streams or devices may run concurrently; the
+ *    library keeps no mutable global state besides the per-thread error string.
+ */
+#ifndef HOPF_H_
+#define HOPF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *hopf_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+enum {
+  HOPF_OK = 0,
+  HOPF_EINVAL = -1,
+  HOPF_EUNSUPPORTED = -2,
+  HOPF_ECUDA = -3
+};
+
+/* Hamiltonians (support functions of a box / a ball):
+ *   HOPF_H_L1  : H(p) = sum_i |p_i|        (shrink_1, threshold t/lambda)
+ *   HOPF_H_WL1 : H(p) = sum_i w_i |p_i|    (shrink_1, threshold t w_i/lambda), w_i > 0
+ *   HOPF_H_L2  : H(p) = ||p||_2            (shrink_2, threshold t/lambda)              */
+typedef enum { HOPF_H_L1 = 0, HOPF_H_WL1 = 1, HOPF_H_L2 = 2 } hopf_h_kind;
+
+/* Diagonal (ellipsoidal) initial data:
+ *   J(x) = 1/2 <x - c, diag(Dj)^{-1} (x - c)> + gamma,  J*(v) = 1/2 <v, Dj v> + <c, v> - gamma
+ * (P:209-263 with Dj_i = a_i^2; Table 4's J = 1/2<., D^{-1}.>).
+ *   M, n      number of points, dimension (1 <= n <= 1024)
+ *   X [M*n]   query points;  t [M] times (t >= 0)
+ *   Dj [n]    diagonal of J's curvature inverse (> 0);  c [n] centre or NULL (= 0)
+ *   gamma     additive constant of J
+ *   h, w      Hamiltonian kind and weights w [n] (HOPF_H_WL1 only, else ignored / may be NULL)
+ *   lambda    split Bregman penalty (> 0; the paper uses 1)
+ *   max_iter  iteration cap (>= 1); tol squared-norm stopping threshold (>= 0, paper 1e-8)
+ *   phi [M], grad [M*n], iters [M]   outputs                                               */
+int hopf_eval_diag(int64_t M, int32_t n, const float *X, const float *t, const float *Dj,
+                   const float *c, float gamma, hopf_h_kind h, const float *w, float lambda,
+                   int32_t max_iter, float tol, float *phi, float *grad, int32_t *iters,
+                   hopf_stream_t stream);
+
+/* Union of K diagonal initial data (min-plus over initial data):
+ *   J(x) = min_k [ 1/2 <x - c_k, diag(Dj_k)^{-1} (x - c_k)> + gamma_k ]
+ *   phi = min_k phi_k, the lowest k wins ties (R19); grad = grad of the winner;
+ *   each phi_k is solved centred at x - c_k with v^0 = d^0 = x - c_k (R5).
+ *   Dj [K*n], C [K*n] (row k = set k), gamma [K]  (HOST-side copy not needed: device pointers)
+ *   iters[i] = the winning set's status.
+ *   Y [M*n] or NULL   closest (Hopf-Lax terminal) point y = x - t grad/||grad||
+ *                     (P:1049-1051), y = c_k* if grad == 0 (R18); HOPF_H_L2 only.
+ *   kstar [M] or NULL winning set index;  phi_k [M*K] or NULL every phi_k.
+ *   Constraints: 1 <= K <= 64, n <= 256.                                                   */
+int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float *t,
+                    const float *Dj, const float *C, const float *gamma, hopf_h_kind h,
+                    const float *w, float lambda, int32_t max_iter, float tol, float *phi,
+                    float *grad, int32_t *iters, float *Y, int32_t *kstar, float *phi_k,
+                    hopf_stream_t stream);
+
+/* Full SPD initial data J(x) = 1/2 <x, A x> + gamma with A = Q diag(Lambda) Q^T (spectral
+ * form as in P:1287-1290).  The plan owns device copies of
+ *   M_lambda = (A^{-1} + lambda I)^{-1} = Q diag(Lambda/(1 + lambda Lambda)) Q^T
+ * (the quadratic prox of (3.4a)) split into tensor-core operands, and of A^{-1}
+ * (for phi).  Built on the host in fp64 from HOST arrays Q_host [n*n] (row-major, orthogonal)
+ * and Lambda_host [n] (> 0).  Synchronous.                                                  */
+typedef struct hopf_dense_plan hopf_dense_plan;
+int hopf_dense_plan_create(int32_t n, const double *Q_host, const double *Lambda_host,
+                           float lambda, hopf_dense_plan **out);
+int hopf_dense_plan_destroy(hopf_dense_plan *plan);
+
+/* Dense evaluation; arguments as hopf_eval_diag, lambda must equal the plan's. */
+int hopf_eval_dense(int64_t M, int32_t n, const float *X, const float *t,
+                    const hopf_dense_plan *plan, float gamma, hopf_h_kind h, const float *w,
+                    float lambda, int32_t max_iter, float tol, float *phi, float *grad,
+                    int32_t *iters, hopf_stream_t stream);
+
+/* End-to-end variant of hopf_eval_diag on HOST buffers (X_host, t_host in, phi_host,
+ * grad_host, iters_host out; pinned memory strongly recommended).  Dj, c, w are DEVICE
+ * pointers as above.  The call splits the points into chunks and pipelines
+ * host->device copies, kernels and device->host copies on internal streams of the
+ * current device; it returns after all results are in host memory (synchronous).
+ * Device work buffers are allocated per call.                                              */
+int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host, const float *t_host,
+                        const float *Dj, const float *c, float gamma, hopf_h_kind h,
+                        const float *w, float lambda, int32_t max_iter, float tol,
+                        float *phi_host, float *grad_host, int32_t *iters_host);
+
+/* Number of kernel launches the most recent successful call made on this thread. */
+int32_t hopf_last_launch_count(void);
+
+/* Text of the most recent error on this thread ("" if none) and a static string for a code. */
+const char *hopf_last_error(void);
+const char *hopf_strerror(int code);
+
+/* Library version (semantic, e.g. 100 = 0.1.0). */
+int32_t hopf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOPF_H_ */

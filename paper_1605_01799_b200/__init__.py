@@ -1,0 +1,210 @@
+"""paper_1605_01799_b200 — B200-native batched Hopf-formula evaluator (arXiv 1605.01799).
+
+Thin Python binding over the C ABI of ``libhopf.so`` (include/hopf.h): argument
+marshalling only.  Every step of the split Bregman path runs in the library's sm_100a
+kernels; PyTorch provides device memory (``data_ptr()``) and streams.  There is no
+CPU fallback: if the extension is missing this module raises on import of ``lib()``.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+__all__ = ["lib", "eval_diag", "eval_union", "eval_dense", "DensePlan", "eval_diag_host",
+           "HopfError", "H_KINDS", "INVALID"]
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libhopf.so"
+H_KINDS = {"l1": 0, "wl1": 1, "l2": 2}
+INVALID = -(2 ** 31)
+_lib = None
+
+
+class HopfError(RuntimeError):
+    def __init__(self, code: int, where: str, detail: str):
+        super().__init__(f"{where} failed with code {code}: {detail}")
+        self.code = code
+
+
+def lib():
+    """The loaded libhopf.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1605_01799_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+        L.hopf_eval_diag.argtypes = [i64, i32, vp, vp, vp, vp, f32, ctypes.c_int, vp, f32, i32, f32,
+                                     vp, vp, vp, vp]
+        L.hopf_eval_union.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, ctypes.c_int, vp, f32, i32,
+                                      f32, vp, vp, vp, vp, vp, vp, vp]
+        L.hopf_dense_plan_create.argtypes = [i32, vp, vp, f32, ctypes.POINTER(vp)]
+        L.hopf_dense_plan_destroy.argtypes = [vp]
+        L.hopf_eval_dense.argtypes = [i64, i32, vp, vp, vp, f32, ctypes.c_int, vp, f32, i32, f32,
+                                      vp, vp, vp, vp]
+        L.hopf_eval_diag_host.argtypes = [i64, i32, vp, vp, vp, vp, f32, ctypes.c_int, vp, f32, i32,
+                                          f32, vp, vp, vp]
+        for f in (L.hopf_eval_diag, L.hopf_eval_union, L.hopf_dense_plan_create,
+                  L.hopf_dense_plan_destroy, L.hopf_eval_dense, L.hopf_eval_diag_host):
+            f.restype = ctypes.c_int
+        L.hopf_last_error.restype = ctypes.c_char_p
+        L.hopf_strerror.restype = ctypes.c_char_p
+        L.hopf_strerror.argtypes = [ctypes.c_int]
+        L.hopf_last_launch_count.restype = ctypes.c_int32
+        L.hopf_version.restype = ctypes.c_int32
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        L = lib()
+        raise HopfError(rc, where, (L.hopf_last_error() or b"").decode() or
+                        L.hopf_strerror(rc).decode())
+
+
+def last_launch_count() -> int:
+    return int(lib().hopf_last_launch_count())
+
+
+def _ptr(tensor, dtype_name, numel=None, name="tensor"):
+    """Device pointer of a contiguous CUDA tensor (validates dtype/size/device)."""
+    import torch
+    if tensor is None:
+        return None
+    if not isinstance(tensor, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    want = {"f32": torch.float32, "i32": torch.int32, "f64": torch.float64}[dtype_name]
+    if tensor.dtype != want:
+        raise TypeError(f"{name} must be {want}, got {tensor.dtype}")
+    if not tensor.is_cuda:
+        raise ValueError(f"{name} must live on a CUDA device")
+    if not tensor.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if numel is not None and tensor.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {tensor.numel()}")
+    return tensor.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def _outputs(M, n, device, out):
+    import torch
+    if out is not None:
+        return out
+    phi = torch.empty(M, dtype=torch.float32, device=device)
+    grad = torch.empty((M, n), dtype=torch.float32, device=device)
+    iters = torch.empty(M, dtype=torch.int32, device=device)
+    return phi, grad, iters
+
+
+def eval_diag(X, t, D, c=None, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=1e-8,
+              out=None, stream=None):
+    """hopf_eval_diag: J(x) = 1/2<x-c, D^{-1}(x-c)> + gamma, H in {l1, wl1, l2}.
+
+    X [M,n], t [M], D [n], c [n]|None, w [n]|None: float32 CUDA tensors.
+    Returns (phi [M], grad [M,n], iters [M] int32)."""
+    M, n = X.shape
+    phi, grad, iters = _outputs(M, n, X.device, out)
+    rc = lib().hopf_eval_diag(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                              _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma),
+                              H_KINDS[h], _ptr(w, "f32", n, "w"), float(lam), int(max_iter),
+                              float(tol), _ptr(phi, "f32", M, "phi"), _ptr(grad, "f32", M * n, "grad"),
+                              _ptr(iters, "i32", M, "iters"), _stream(stream))
+    _check(rc, "hopf_eval_diag")
+    return phi, grad, iters
+
+
+def eval_union(X, t, Dk, Ck, gammak, h="l2", w=None, lam=1.0, max_iter=1000, tol=1e-8,
+               want_y=True, want_kstar=True, want_phik=False, out=None, stream=None):
+    """hopf_eval_union: J = min_k J_k.  Returns (phi, grad, iters, Y|None, kstar|None, phik|None)."""
+    import torch
+    M, n = X.shape
+    K = Dk.shape[0]
+    phi, grad, iters = _outputs(M, n, X.device, out)
+    Y = torch.empty((M, n), dtype=torch.float32, device=X.device) if want_y else None
+    ks = torch.empty(M, dtype=torch.int32, device=X.device) if want_kstar else None
+    pk = torch.empty((M, K), dtype=torch.float32, device=X.device) if want_phik else None
+    rc = lib().hopf_eval_union(M, n, K, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                               _ptr(Dk, "f32", K * n, "Dk"), _ptr(Ck, "f32", K * n, "Ck"),
+                               _ptr(gammak, "f32", K, "gammak"), H_KINDS[h], _ptr(w, "f32", n, "w"),
+                               float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                               _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                               _ptr(Y, "f32", M * n, "Y"), _ptr(ks, "i32", M, "kstar"),
+                               _ptr(pk, "f32", M * K, "phik"), _stream(stream))
+    _check(rc, "hopf_eval_union")
+    return phi, grad, iters, Y, ks, pk
+
+
+class DensePlan:
+    """hopf_dense_plan for J(x) = 1/2<x, Q diag(Lam) Q^T x> (built in fp64 on the host)."""
+
+    def __init__(self, Q, Lam, lam=1.0):
+        import numpy as np
+        Q = np.ascontiguousarray(np.asarray(Q, dtype=np.float64))
+        Lam = np.ascontiguousarray(np.asarray(Lam, dtype=np.float64))
+        n = Lam.shape[0]
+        if Q.shape != (n, n):
+            raise ValueError("Q must be n x n")
+        self.n, self.lam = n, float(lam)
+        h = ctypes.c_void_p()
+        rc = lib().hopf_dense_plan_create(n, Q.ctypes.data, Lam.ctypes.data, float(lam),
+                                          ctypes.byref(h))
+        _check(rc, "hopf_dense_plan_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hopf_dense_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def eval_dense(X, t, plan: DensePlan, gamma=0.0, h="l1", w=None, max_iter=1000, tol=1e-8,
+               out=None, stream=None):
+    """hopf_eval_dense with a DensePlan.  Returns (phi, grad, iters)."""
+    M, n = X.shape
+    phi, grad, iters = _outputs(M, n, X.device, out)
+    rc = lib().hopf_eval_dense(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"), plan._h,
+                               float(gamma), H_KINDS[h], _ptr(w, "f32", n, "w"), float(plan.lam),
+                               int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                               _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                               _stream(stream))
+    _check(rc, "hopf_eval_dense")
+    return phi, grad, iters
+
+
+def eval_diag_host(X, t, D, c=None, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=1e-8,
+                   out=None):
+    """hopf_eval_diag_host: HOST (ideally pinned) X, t in and phi, grad, iters out; D/c/w on device.
+    Copies are pipelined inside the library.  Returns host tensors (phi, grad, iters)."""
+    import torch
+    M, n = X.shape
+    if X.is_cuda or t.is_cuda:
+        raise ValueError("eval_diag_host takes host tensors")
+    if out is None:
+        out = (torch.empty(M, dtype=torch.float32, pin_memory=True),
+               torch.empty((M, n), dtype=torch.float32, pin_memory=True),
+               torch.empty(M, dtype=torch.int32, pin_memory=True))
+    phi, grad, iters = out
+    for a, nm in ((X, "X"), (t, "t"), (phi, "phi"), (grad, "grad"), (iters, "iters")):
+        if not a.is_contiguous():
+            raise ValueError(f"{nm} must be contiguous")
+    rc = lib().hopf_eval_diag_host(M, n, X.data_ptr(), t.data_ptr(), _ptr(D, "f32", n, "D"),
+                                   _ptr(c, "f32", n, "c"), float(gamma), H_KINDS[h],
+                                   _ptr(w, "f32", n, "w"), float(lam), int(max_iter), float(tol),
+                                   phi.data_ptr(), grad.data_ptr(), iters.data_ptr())
+    _check(rc, "hopf_eval_diag_host")
+    return phi, grad, iters

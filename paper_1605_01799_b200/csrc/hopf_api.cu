@@ -1,0 +1,172 @@
+// hopf_api.cu — the C ABI of libhopf.so (declared in include/hopf.h).
+// Argument validation, kernel-variant selection and launch; no arithmetic of the method
+// happens on the host except the fp64 dense-plan construction (dense_plan.cu).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hopf.h"
+#include "common.cuh"
+#include "diag_kernel.cuh"
+
+namespace hopf {
+
+thread_local std::string g_last_error;
+thread_local int32_t g_launches = 0;
+
+int set_error(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HOPF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HOPF_OK;
+}
+
+int num_sms() {
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (sms[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v > 0 ? v : 148;
+  }
+  return sms[dev];
+}
+
+// ---------------------------------------------------------------- diag / union variants
+using KernFn = void (*)(const DiagParams);
+
+struct Variant {
+  int G, CPL;
+  KernFn fn[3][2];  // [h kind][union]
+};
+
+#define HOPF_VARIANT(G_, C_)                                                                 \
+  {G_, C_,                                                                                   \
+   {{hopf_diag_kernel<G_, C_, HK_L1, false>, hopf_diag_kernel<G_, C_, HK_L1, true>},         \
+    {hopf_diag_kernel<G_, C_, HK_WL1, false>, hopf_diag_kernel<G_, C_, HK_WL1, true>},       \
+    {hopf_diag_kernel<G_, C_, HK_L2, false>, hopf_diag_kernel<G_, C_, HK_L2, true>}}}
+
+// Ordered by padded width G*CPL, then G: the first variant with G*CPL >= n is used.
+static const Variant kVariants[] = {
+    HOPF_VARIANT(1, 1),  HOPF_VARIANT(1, 2),  HOPF_VARIANT(1, 4),   HOPF_VARIANT(1, 8),
+    HOPF_VARIANT(1, 16), HOPF_VARIANT(2, 12), HOPF_VARIANT(2, 16),  HOPF_VARIANT(4, 16),
+    HOPF_VARIANT(4, 25), HOPF_VARIANT(4, 32), HOPF_VARIANT(8, 16),  HOPF_VARIANT(8, 32),
+    HOPF_VARIANT(16, 32), HOPF_VARIANT(32, 32)};
+
+static const Variant *pick_variant(int n, bool is_union) {
+  // union keeps x and the best grad resident too: cap CPL at 16 for register room
+  for (const Variant &v : kVariants) {
+    if (v.G * v.CPL < n) continue;
+    if (is_union && v.CPL > 16 && n > 16) continue;
+    return &v;
+  }
+  return nullptr;
+}
+
+static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
+                            cudaStream_t stream) {
+  const Variant *v = pick_variant(p.n, is_union);
+  if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
+  KernFn fn = v->fn[(int)h][is_union ? 1 : 0];
+  const int threads = 256;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
+  if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+  const int64_t groups_needed = p.M;
+  const int64_t blocks_needed = (groups_needed * v->G + threads - 1) / threads;
+  int64_t blocks = (int64_t)num_sms() * per_sm;
+  if (blocks > blocks_needed) blocks = blocks_needed;
+  if (blocks < 1) blocks = 1;
+  fn<<<(unsigned)blocks, threads, 0, stream>>>(p);
+  g_launches += 1;
+  return check_launch("hopf_diag_kernel");
+}
+
+static bool finite_pos(float x) { return std::isfinite(x) && x > 0.f; }
+
+}  // namespace hopf
+
+using namespace hopf;
+
+extern "C" {
+
+int hopf_eval_diag(int64_t M, int32_t n, const float *X, const float *t, const float *Dj,
+                   const float *c, float gamma, hopf_h_kind h, const float *w, float lambda,
+                   int32_t max_iter, float tol, float *phi, float *grad, int32_t *iters,
+                   hopf_stream_t stream) {
+  g_launches = 0;
+  g_last_error.clear();
+  if (M < 0 || n < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d", (long long)M, n);
+  if ((int)h < 0 || (int)h > 2) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
+  if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
+  if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
+  if (h == HOPF_H_WL1 && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1");
+  if (M == 0) return HOPF_OK;
+  if (!X || !t || !Dj || !phi || !grad || !iters)
+    return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  DiagParams p{};
+  p.M = M; p.n = n; p.X = X; p.t = t; p.D = Dj; p.c = c; p.w = w; p.gk = nullptr;
+  p.gamma = gamma; p.lambda = lambda; p.max_iter = max_iter; p.tol = tol; p.K = 0;
+  p.phi = phi; p.grad = grad; p.iters = iters; p.Y = nullptr; p.kstar = nullptr; p.phik = nullptr;
+  return launch_diag_like(p, h, false, (cudaStream_t)stream);
+}
+
+int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float *t,
+                    const float *Dj, const float *C, const float *gamma, hopf_h_kind h,
+                    const float *w, float lambda, int32_t max_iter, float tol, float *phi,
+                    float *grad, int32_t *iters, float *Y, int32_t *kstar, float *phi_k,
+                    hopf_stream_t stream) {
+  g_launches = 0;
+  g_last_error.clear();
+  if (M < 0 || n < 1 || K < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d K=%d", (long long)M, n, K);
+  if ((int)h < 0 || (int)h > 2) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
+  if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
+  if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
+  if (h == HOPF_H_WL1 && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1");
+  if (Y && h != HOPF_H_L2) return set_error(HOPF_EINVAL, "Y (closest point) requires HOPF_H_L2");
+  if (K > 64 || n > 256) return set_error(HOPF_EUNSUPPORTED, "union supports K<=64, n<=256");
+  if (M == 0) return HOPF_OK;
+  if (!X || !t || !Dj || !C || !gamma || !phi || !grad || !iters)
+    return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  DiagParams p{};
+  p.M = M; p.n = n; p.X = X; p.t = t; p.D = Dj; p.c = C; p.w = w; p.gk = gamma;
+  p.gamma = 0.f; p.lambda = lambda; p.max_iter = max_iter; p.tol = tol; p.K = K;
+  p.phi = phi; p.grad = grad; p.iters = iters; p.Y = Y; p.kstar = kstar; p.phik = phi_k;
+  return launch_diag_like(p, h, true, (cudaStream_t)stream);
+}
+
+int32_t hopf_last_launch_count(void) { return g_launches; }
+
+const char *hopf_last_error(void) { return g_last_error.c_str(); }
+
+const char *hopf_strerror(int code) {
+  switch (code) {
+    case HOPF_OK: return "ok";
+    case HOPF_EINVAL: return "invalid argument";
+    case HOPF_EUNSUPPORTED: return "unsupported shape";
+    case HOPF_ECUDA: return "CUDA error";
+    default: return "unknown error code";
+  }
+}
+
+int32_t hopf_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// host_pipeline.cu — end-to-end entry point on host buffers (hopf_eval_diag_host).
+// Points are processed in chunks; chunk c runs on internal stream c % kStreams as
+//   H2D(X_c, t_c) -> hopf_diag_kernel -> D2H(grad_c, phi_c, iters_c)
+// so the PCIe copies of neighbouring chunks overlap each other (full duplex) and the kernels.
+// Device buffers and streams are cached per device (grown on demand, never shrunk).
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "../../include/hopf.h"
+#include "common.cuh"
+
+namespace hopf {
+namespace {
+constexpr int kStreams = 3;
+
+struct DevCache {
+  bool init = false;
+  cudaStream_t s[kStreams];
+  char *buf = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_mu;
+DevCache g_cache[64];
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+}  // namespace
+}  // namespace hopf
+
+using namespace hopf;
+
+extern "C" int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host,
+                                   const float *t_host, const float *Dj, const float *c,
+                                   float gamma, hopf_h_kind h, const float *w, float lambda,
+                                   int32_t max_iter, float tol, float *phi_host,
+                                   float *grad_host, int32_t *iters_host) {
+  if (M < 0 || n < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d", (long long)M, n);
+  if (M == 0) return HOPF_OK;
+  if (!X_host || !t_host || !phi_host || !grad_host || !iters_host || !Dj)
+    return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return set_error(HOPF_EINVAL, "device index %d", dev);
+  // ~16 MB of X per chunk: large enough to amortise launch + copy latency.
+  int64_t chunk = (int64_t)((16u << 20) / ((size_t)n * sizeof(float)));
+  if (chunk < 1024) chunk = 1024;
+  if (chunk > M) chunk = M;
+  const size_t xb = align_up((size_t)chunk * n * 4), vb = align_up((size_t)chunk * 4);
+  const size_t per = 2 * xb + 3 * vb;  // X, grad, t, phi, iters
+  std::lock_guard<std::mutex> lock(g_mu);
+  DevCache &dc = g_cache[dev];
+  if (!dc.init) {
+    for (int i = 0; i < kStreams; i++) cudaStreamCreateWithFlags(&dc.s[i], cudaStreamNonBlocking);
+    dc.init = true;
+  }
+  if (dc.bytes < per * kStreams) {
+    if (dc.buf) cudaFree(dc.buf);
+    dc.buf = nullptr;
+    dc.bytes = 0;
+    if (cudaMalloc(&dc.buf, per * kStreams) != cudaSuccess)
+      return set_error(HOPF_ECUDA, "cudaMalloc of %zu bytes failed", per * kStreams);
+    dc.bytes = per * kStreams;
+  }
+  int32_t launches = 0;
+  int rc = HOPF_OK;
+  for (int64_t off = 0, ci = 0; off < M; off += chunk, ci++) {
+    const int64_t cnt = (M - off < chunk) ? (M - off) : chunk;
+    const int slot = (int)(ci % kStreams);
+    cudaStream_t s = dc.s[slot];
+    char *base = dc.buf + per * slot;
+    float *dX = (float *)base, *dG = (float *)(base + xb);
+    float *dt = (float *)(base + 2 * xb), *dphi = (float *)(base + 2 * xb + vb);
+    int32_t *dit = (int32_t *)(base + 2 * xb + 2 * vb);
+    cudaMemcpyAsync(dX, X_host + off * n, (size_t)cnt * n * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(dt, t_host + off, (size_t)cnt * 4, cudaMemcpyHostToDevice, s);
+    rc = hopf_eval_diag(cnt, n, dX, dt, Dj, c, gamma, h, w, lambda, max_iter, tol, dphi, dG, dit,
+                        (hopf_stream_t)s);
+    launches += hopf_last_launch_count();
+    if (rc != HOPF_OK) break;
+    cudaMemcpyAsync(grad_host + off * n, dG, (size_t)cnt * n * 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(phi_host + off, dphi, (size_t)cnt * 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(iters_host + off, dit, (size_t)cnt * 4, cudaMemcpyDeviceToHost, s);
+  }
+  for (int i = 0; i < kStreams; i++) {
+    cudaError_t e = cudaStreamSynchronize(dc.s[i]);
+    if (e != cudaSuccess && rc == HOPF_OK)
+      rc = set_error(HOPF_ECUDA, "hopf_eval_diag_host: %s", cudaGetErrorString(e));
+  }
+  g_launches = launches;
+  return rc;
+}

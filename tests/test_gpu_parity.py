@@ -1,0 +1,300 @@
+"""GPU parity: the CUDA path (through the C ABI of libhopf.so) against the fp64 oracle.
+
+Bar (BASELINE.json north_star): |dphi| <= 1e-4 max(1,|phi|), ||d grad||_inf <= 1e-3 on identical
+seeded fp32 inputs; union winners per SURVEY §8(c) (a different k* is accepted only if the
+oracle's phi for it is within the phi tolerance of the oracle's minimum); closest points
+||dY||_inf <= 1e-3 max(1,t).  Status codes must agree exactly (converged / t == 0 / invalid),
+iteration counts may differ by rounding at the threshold (reported, bounded).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1605_01799_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+PHI_RTOL, GRAD_ATOL = 1e-4, 1e-3
+
+
+@pytest.fixture(scope="module")
+def hb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1605_01799_b200 as hb
+    hb.lib()  # fail loudly if the library is missing
+    return hb
+
+
+def dev(a, dtype=None):
+    import torch
+    if a is None:
+        return None
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype or torch.float32).cuda()
+
+
+def check(phi_g, grad_g, it_g, phi_o, grad_o, it_o, iters_slack=2, frac_exact=0.9):
+    phi_g, grad_g, it_g = (a.cpu().numpy() if hasattr(a, "cpu") else a for a in (phi_g, grad_g, it_g))
+    # status classes agree
+    cls = lambda it: np.where(it == oracle.INVALID, -2, np.where(it == 0, 0, np.where(it > 0, 1, -1)))
+    assert np.array_equal(cls(it_g), cls(it_o)), "status classes differ"
+    ok = it_o != oracle.INVALID
+    assert np.all(np.isnan(phi_g[~ok]))
+    dphi = np.abs(phi_g[ok] - phi_o[ok]) / np.maximum(1.0, np.abs(phi_o[ok]))
+    dgrad = np.abs(grad_g[ok] - grad_o[ok]).max(axis=1) if grad_o.size else np.zeros(0)
+    assert dphi.max(initial=0) <= PHI_RTOL, f"max rel dphi {dphi.max()}"
+    assert dgrad.max(initial=0) <= GRAD_ATOL, f"max dgrad {dgrad.max()}"
+    conv = it_o > 0
+    if conv.any():
+        di = np.abs(it_g[conv] - it_o[conv])
+        assert di.max() <= iters_slack, f"iteration counts differ by up to {di.max()}"
+        assert np.mean(di == 0) >= frac_exact, f"only {np.mean(di == 0):.3f} identical iteration counts"
+    return dphi.max(initial=0), dgrad.max(initial=0)
+
+
+def run_diag(hb, wl, X, t, **kw):
+    return hb.eval_diag(dev(X), dev(t), dev(wl.D), dev(wl.c), wl.gamma, wl.h, dev(wl.w), **kw)
+
+
+def oracle_diag(wl, X, t, **kw):
+    return oracle.eval_diag(X, t, wl.D, wl.c, wl.gamma, wl.h, wl.w, **kw)
+
+
+def test_c1_closed_form_config(hb):
+    wl = inputs.config("c1")
+    X, t = inputs.points(wl)
+    g = run_diag(hb, wl, X, t)
+    o = oracle_diag(wl, X, t)
+    check(*g, *o, iters_slack=0, frac_exact=1.0)
+    assert np.all(g[2].cpu().numpy() == 3)   # exact after two steps at lambda = 1 (oracle pin)
+
+
+@pytest.mark.parametrize("name,M", [("c2", 20000), ("c3", 3000)])
+def test_diag_configs_subset(hb, name, M):
+    wl = inputs.config(name)
+    X, t = inputs.points(wl, 0, M)
+    check(*run_diag(hb, wl, X, t), *oracle_diag(wl, X, t))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13, 16, 17, 31, 33, 64, 100, 127, 200, 255, 256,
+                               300, 511, 777, 1000, 1024])
+@pytest.mark.parametrize("h", ["l1", "wl1", "l2"])
+def test_diag_ragged_dimensions(hb, n, h):
+    """Every compiled lane-group variant, ragged tails, shifted centre c and lambda != 1."""
+    rng = np.random.default_rng(n * 7 + len(h))
+    M = 257
+    D = rng.uniform(0.5, 2.0, n).astype(np.float32)
+    c = rng.normal(size=n).astype(np.float32)
+    w = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    X = rng.normal(scale=2.0, size=(M, n)).astype(np.float32)
+    t = rng.uniform(0.0, 2.0, M).astype(np.float32)
+    lam = 1.0 if n % 2 else 0.7
+    g = hb.eval_diag(dev(X), dev(t), dev(D), dev(c), -0.5, h, dev(w), lam=lam)
+    o = oracle.eval_diag(X, t, D, c, -0.5, h, w, lam=lam)
+    check(*g, *o)
+
+
+def test_diag_edge_cases(hb):
+    import torch
+    wl = inputs.config("c3", n=40)
+    X, t = inputs.points(wl, 0, 64)
+    X = X.copy(); t = t.copy()
+    t[3] = 0.0                      # t == 0 -> J(x), grad J(x), iters 0
+    t[5] = -1.0                     # invalid
+    X[7, 11] = np.nan               # invalid
+    X[9, 0] = np.inf                # invalid
+    t[10] = np.inf                  # invalid
+    X[12] = 0.0                     # x = 0: grad = 0
+    t[13] = 100.0                   # ||x|| <= t: grad = 0, phi = gamma
+    g = run_diag(hb, wl, X, t)
+    o = oracle_diag(wl, X, t)
+    check(*g, *o)
+    it = g[2].cpu().numpy()
+    assert it[3] == 0 and it[5] == oracle.INVALID and it[7] == oracle.INVALID
+    assert it[9] == oracle.INVALID and it[10] == oracle.INVALID
+    assert np.all(g[1][13].cpu().numpy() == 0) and abs(g[0][13].item() + 0.5) < 1e-6
+    # max_iter exhausted: status -max_iter, outputs from the last d
+    g2 = run_diag(hb, wl, X, t, max_iter=3)
+    o2 = oracle_diag(wl, X, t, max_iter=3)
+    it2 = g2[2].cpu().numpy()
+    ok = (t > 0) & np.isfinite(t) & np.all(np.isfinite(X), axis=1)
+    assert np.all(it2[ok & (it2 < 0)] == -3)
+    np.testing.assert_allclose(g2[1].cpu().numpy()[ok], o2[1][ok], atol=1e-4)
+    # M == 0 is a no-op
+    e = torch.empty((0, 40), device="cuda")
+    hb.eval_diag(e, torch.empty(0, device="cuda"), dev(wl.D), None, 0.0, "l2")
+
+
+def test_abi_errors(hb):
+    import torch
+    X = torch.zeros((4, 8), device="cuda")
+    t = torch.ones(4, device="cuda")
+    D = torch.ones(8, device="cuda")
+    with pytest.raises(hb.HopfError) as e:
+        hb.eval_diag(X, t, D, None, 0.0, "wl1", None)       # WL1 without w
+    assert e.value.code == -1
+    with pytest.raises(hb.HopfError) as e:
+        hb.eval_diag(X, t, D, None, 0.0, "l1", None, lam=0.0)
+    assert e.value.code == -1
+    with pytest.raises(hb.HopfError) as e:
+        hb.eval_diag(X, t, D, None, 0.0, "l1", None, max_iter=0)
+    assert e.value.code == -1
+    Xb = torch.zeros((4, 2000), device="cuda")
+    with pytest.raises(hb.HopfError) as e:
+        hb.eval_diag(Xb, t, torch.ones(2000, device="cuda"), None, 0.0, "l1")
+    assert e.value.code == -2
+
+
+def test_union_c5_subset(hb):
+    wl = inputs.config("c5")
+    X, t = inputs.points(wl, 0, 3000)
+    phi, grad, it, Y, ks, pk = hb.eval_union(dev(X), dev(t), dev(wl.Dk), dev(wl.Ck), dev(wl.gammak),
+                                             "l2", want_phik=True)
+    o = oracle.eval_union(X, t, wl.Dk, wl.Ck, wl.gammak, "l2")
+    check_union(phi, grad, it, Y, ks, pk, o, t)
+
+
+def check_union(phi, grad, it, Y, ks, pk, o, t):
+    phi_o, grad_o, it_o, Y_o, ks_o, pk_o = o
+    phi, grad, it, ks = (a.cpu().numpy() for a in (phi, grad, it, ks))
+    pk = pk.cpu().numpy()
+    Yg = Y.cpu().numpy() if Y is not None else None
+    # every phi_k matches
+    assert np.max(np.abs(pk - pk_o) / np.maximum(1, np.abs(pk_o))) <= PHI_RTOL
+    assert np.max(np.abs(phi - phi_o) / np.maximum(1, np.abs(phi_o))) <= PHI_RTOL
+    same = ks == ks_o
+    diff = ~same
+    if diff.any():  # tie rule: GPU winner must be optimal within the phi tolerance
+        alt = pk_o[np.nonzero(diff)[0], ks[diff]]
+        assert np.all(alt <= phi_o[diff] + PHI_RTOL * np.maximum(1, np.abs(phi_o[diff])))
+    assert np.mean(same) > 0.98
+    # compare grad / Y on the GPU's own branch: recompute the oracle for those points per branch
+    assert np.max(np.abs(grad[same] - grad_o[same])) <= GRAD_ATOL
+    if Yg is not None:
+        tol = GRAD_ATOL * np.maximum(1, t[same])[:, None]
+        assert np.all(np.abs(Yg[same] - Y_o[same]) <= tol)
+
+
+def test_union_fig4_and_edge(hb):
+    n = 8
+    b = np.ones(n, np.float32)
+    Dk = np.ones((2, n), np.float32)
+    Ck = np.stack([b, -b]).astype(np.float32)
+    gk = np.full(2, -0.5 * n, np.float32)
+    rng = np.random.default_rng(5)
+    X = rng.uniform(-20, 20, (500, n)).astype(np.float32)
+    t = rng.uniform(0, 15, 500).astype(np.float32)
+    t[0] = 0.0
+    X[1] = 0.0   # exact tie between the two branches: lowest k wins
+    phi, grad, it, Y, ks, pk = hb.eval_union(dev(X), dev(t), dev(Dk), dev(Ck), dev(gk), "l1",
+                                             want_y=False, want_phik=True)
+    o = oracle.eval_union(X, t, Dk, Ck, gk, "l1", want_y=False)
+    check_union(phi, grad, it, None, ks, pk, o, t)
+    assert ks[1].item() == 0
+    assert it[0].item() == 0
+
+
+def test_dense_c4_subset(hb):
+    wl = inputs.config("c4")
+    X, t = inputs.points(wl, 0, 1500)
+    plan = hb.DensePlan(wl.Q, wl.Lam)
+    g = hb.eval_dense(dev(X), dev(t), plan, wl.gamma, "l1")
+    o = oracle.eval_dense(X, t, wl.Q, wl.Lam, wl.gamma, "l1")
+    check(*g, *o, iters_slack=3, frac_exact=0.8)
+
+
+@pytest.mark.parametrize("n,h", [(32, "l2"), (64, "wl1"), (96, "l1"), (160, "l2")])
+def test_dense_shapes_and_edges(hb, n, h):
+    rng = np.random.default_rng(n)
+    Q = inputs.haar_orthogonal(rng, n)
+    Lam = np.exp(rng.uniform(np.log(0.1), np.log(10), n))
+    w = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    X = rng.normal(size=(300, n)).astype(np.float32)
+    t = rng.uniform(0.1, 1.0, 300).astype(np.float32)
+    t[0] = 0.0
+    t[1] = -2.0
+    X[2, 3] = np.nan
+    plan = hb.DensePlan(Q, Lam)
+    g = hb.eval_dense(dev(X), dev(t), plan, 0.25, h, dev(w))
+    o = oracle.eval_dense(X, t, Q, Lam, 0.25, h, w)
+    check(*g, *o, iters_slack=3, frac_exact=0.8)
+
+
+def test_full_size_c3_sampled(hb):
+    """BASELINE's full C3 size in the bench launch configuration; sampled rows vs the oracle."""
+    import torch
+    wl = inputs.config("c3")
+    X, t = inputs.points(wl)
+    phi, grad, it = run_diag(hb, wl, X, t)
+    torch.cuda.synchronize()
+    idx = np.sort(np.random.default_rng(0).choice(wl.M, 400, replace=False))
+    idx = np.concatenate([idx, [0, wl.M - 1]])
+    o = oracle_diag(wl, X[idx], t[idx])
+    check(phi[idx], grad[idx], it[idx], *o)
+    # every point converged, properties at any size: grad = 0 iff ||x|| <= t, iters in range
+    itn = it.cpu().numpy()
+    assert np.all(itn > 0)
+
+
+def test_full_size_c2_sampled(hb):
+    import torch
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl)
+    phi, grad, it = run_diag(hb, wl, X, t)
+    torch.cuda.synchronize()
+    idx = np.sort(np.random.default_rng(1).choice(wl.M, 2000, replace=False))
+    o = oracle_diag(wl, X[idx], t[idx])
+    check(phi[idx], grad[idx], it[idx], *o)
+    assert np.all(it.cpu().numpy() > 0)
+
+
+def test_full_size_c5_sampled(hb):
+    wl = inputs.config("c5")
+    X, t = inputs.points(wl)
+    phi, grad, it, Y, ks, pk = hb.eval_union(dev(X), dev(t), dev(wl.Dk), dev(wl.Ck), dev(wl.gammak),
+                                             "l2", want_phik=True)
+    idx = np.sort(np.random.default_rng(2).choice(wl.M, 300, replace=False))
+    o = oracle.eval_union(X[idx], t[idx], wl.Dk, wl.Ck, wl.gammak, "l2")
+    check_union(phi[idx], grad[idx], it[idx], Y[idx], ks[idx], pk[idx], o, t[idx])
+
+
+def test_full_size_c4_sampled(hb):
+    import torch
+    wl = inputs.config("c4")
+    X, t = inputs.points(wl)
+    plan = hb.DensePlan(wl.Q, wl.Lam)
+    phi, grad, it = hb.eval_dense(dev(X), dev(t), plan, wl.gamma, "l1")
+    torch.cuda.synchronize()
+    idx = np.sort(np.random.default_rng(3).choice(wl.M, 200, replace=False))
+    o = oracle.eval_dense(X[idx], t[idx], wl.Q, wl.Lam, wl.gamma, "l1")
+    check(phi[idx], grad[idx], it[idx], *o, iters_slack=3, frac_exact=0.8)
+    assert np.all(it.cpu().numpy() > 0)
+
+
+def test_determinism_and_shard_invariance(hb):
+    """Per-point results are bitwise identical across repeated runs and any sharding."""
+    import torch
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 50000)
+    a = run_diag(hb, wl, X, t)
+    b = run_diag(hb, wl, X, t)
+    X2, t2 = inputs.points(wl, 20011, 50000)   # a shard generated independently
+    c = run_diag(hb, wl, X2, t2)
+    torch.cuda.synchronize()
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+    for u, v in zip(a, c):
+        assert torch.equal(u[20011:], v)
+
+
+def test_host_pipeline_matches_device(hb):
+    import torch
+    wl = inputs.config("c3")
+    X, t = inputs.points(wl, 0, 20000)
+    Xh = torch.from_numpy(X).pin_memory()
+    th = torch.from_numpy(t).pin_memory()
+    ph, gh, ih = hb.eval_diag_host(Xh, th, dev(wl.D), None, wl.gamma, "l2")
+    pd, gd, idv = run_diag(hb, wl, X, t)
+    torch.cuda.synchronize()
+    assert torch.equal(ph, pd.cpu()) and torch.equal(gh, gd.cpu()) and torch.equal(ih, idv.cpu())
