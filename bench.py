@@ -31,7 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1605_01799_b200 import inputs  # noqa: E402
+from paper_1605_01799_b200 import inputs, shard  # noqa: E402
 
 METRIC = "Hopf evals/sec (phi+grad phi) at n=1000"
 UNIT = "evals/s"
@@ -40,7 +40,8 @@ FP32_LANES_PER_SM = 128
 # algorithmic FP32 flops per coordinate-iteration: update + the paper's test
 FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14}
 # per-point HBM bytes: x (4n) + grad (4n) + t, phi, iters (12)
-CPU_SAMPLE = {"c1": 1024, "c2": 200_000, "c3": 12_000, "c4": 1024, "c5": 8_000}
+CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000}
+CPU_MIN_SECONDS = 10.0
 
 
 def dist_env():
@@ -108,10 +109,23 @@ def load_traffic(config):
         return None
 
 
-def cpu_baseline_run(wl, sample):
+def cpu_baseline_run(wl, sample, min_seconds=0.0):
+    """Oracle throughput on the first `sample` points, repeated until min_seconds elapsed."""
     import oracle
     X, t = inputs.points(wl, 0, sample)
     t0 = time.perf_counter()
+    reps = 0
+    while True:
+        _oracle_once(wl, X, t)
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= min_seconds:
+            break
+    return sample * reps / dt, dt, oracle.threads(), reps
+
+
+def _oracle_once(wl, X, t):
+    import oracle
     if wl.kind == "diag":
         oracle.eval_diag(X, t, wl.D, wl.c, wl.gamma, wl.h, wl.w, lam=wl.lam,
                          max_iter=wl.max_iter, tol=wl.tol)
@@ -121,8 +135,6 @@ def cpu_baseline_run(wl, sample):
     else:
         oracle.eval_dense(X, t, wl.Q, wl.Lam, wl.gamma, wl.h, lam=wl.lam, max_iter=wl.max_iter,
                           tol=wl.tol)
-    dt = time.perf_counter() - t0
-    return sample / dt, dt, oracle.threads()
 
 
 def run_reference(args, wl):
@@ -135,7 +147,7 @@ def run_reference(args, wl):
         cpu_baseline_run(wl, max(1, sample // 8))
     times = []
     for _ in range(args.steps):
-        v, dt, cores = cpu_baseline_run(wl, sample)
+        v, dt, cores, _ = cpu_baseline_run(wl, sample)
         times.append(dt)
     ms = 1e3 * statistics.mean(times)
     value = sample / (ms / 1e3)
@@ -164,7 +176,7 @@ def config_dict(wl, ws):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--M", type=int, default=None, help="points per GPU (default: the config's)")
@@ -192,9 +204,9 @@ def main():
 
     # ---- inputs: this rank's shard of the global points (generated by global index) ----------
     M = wl.M
-    r0 = rank * M
+    r0, r1 = shard.weak_range(M, rank)
     wl_g = inputs.config(args.config, M=M * ws)
-    Xh, th = inputs.points(wl_g, r0, r0 + M)
+    Xh, th = inputs.points(wl_g, r0, r1)
     X = torch.from_numpy(Xh).to(dev)
     t = torch.from_numpy(th).to(dev)
     n = wl.n
@@ -328,10 +340,11 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        sample = args.cpu_sample or CPU_SAMPLE[wl.name]
-        v, dt, cores = cpu_baseline_run(wl, sample)
+        sample = min(args.cpu_sample or CPU_SAMPLE[wl.name], wl.M)
+        v, dt, cores, reps = cpu_baseline_run(wl, sample, CPU_MIN_SECONDS)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"first {sample} points of {wl.name} ({dt:.1f} s of fp64 oracle)"}
+               "sample": f"first {sample} points of {wl.name} x {reps} passes "
+                         f"({dt:.1f} s of the fp64 oracle, OpenMP over points)"}
 
     line = {"metric": METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={n})",
             "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

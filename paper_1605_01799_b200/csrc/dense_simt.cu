@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(NT, 1)
         ds[row * n + j] = xv;   // d0 = x
         bs[row * n + j] = 0.f;  // b0 = 0
         vps[row * n + j] = xv;  // v0 = x
-        Us[row * n + j] = xv;   // U = x + lambda(d0 - b0)
+        Us[row * n + j] = fmaf(p.lambda, xv, xv);   // U = x + lambda (d0 - b0) = (1 + lambda) x
       }
     } else {
 #pragma unroll

@@ -34,7 +34,7 @@ def dev(a, dtype=None):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype or torch.float32).cuda()
 
 
-def check(phi_g, grad_g, it_g, phi_o, grad_o, it_o, iters_slack=2, frac_exact=0.9):
+def check(phi_g, grad_g, it_g, phi_o, grad_o, it_o, iters_slack=2, frac_exact=0.9, iters_rel=0.0):
     phi_g, grad_g, it_g = (a.cpu().numpy() if hasattr(a, "cpu") else a for a in (phi_g, grad_g, it_g))
     # status classes agree
     cls = lambda it: np.where(it == oracle.INVALID, -2, np.where(it == 0, 0, np.where(it > 0, 1, -1)))
@@ -48,7 +48,8 @@ def check(phi_g, grad_g, it_g, phi_o, grad_o, it_o, iters_slack=2, frac_exact=0.
     conv = it_o > 0
     if conv.any():
         di = np.abs(it_g[conv] - it_o[conv])
-        assert di.max() <= iters_slack, f"iteration counts differ by up to {di.max()}"
+        allow = np.maximum(iters_slack, iters_rel * it_o[conv])
+        assert np.all(di <= allow), f"iteration counts differ by up to {di.max()}"
         assert np.mean(di == 0) >= frac_exact, f"only {np.mean(di == 0):.3f} identical iteration counts"
     return dphi.max(initial=0), dgrad.max(initial=0)
 
@@ -169,7 +170,7 @@ def check_union(phi, grad, it, Y, ks, pk, o, t):
         alt = pk_o[np.nonzero(diff)[0], ks[diff]]
         assert np.all(alt <= phi_o[diff] + PHI_RTOL * np.maximum(1, np.abs(phi_o[diff])))
     assert np.mean(same) > 0.98
-    # compare grad / Y on the GPU's own branch: recompute the oracle for those points per branch
+    # grad / Y compared where both sides chose the same branch
     assert np.max(np.abs(grad[same] - grad_o[same])) <= GRAD_ATOL
     if Yg is not None:
         tol = GRAD_ATOL * np.maximum(1, t[same])[:, None]
@@ -201,7 +202,7 @@ def test_dense_c4_subset(hb):
     plan = hb.DensePlan(wl.Q, wl.Lam)
     g = hb.eval_dense(dev(X), dev(t), plan, wl.gamma, "l1")
     o = oracle.eval_dense(X, t, wl.Q, wl.Lam, wl.gamma, "l1")
-    check(*g, *o, iters_slack=3, frac_exact=0.8)
+    check(*g, *o)
 
 
 @pytest.mark.parametrize("n,h", [(32, "l2"), (64, "wl1"), (96, "l1"), (160, "l2")])
@@ -218,7 +219,7 @@ def test_dense_shapes_and_edges(hb, n, h):
     plan = hb.DensePlan(Q, Lam)
     g = hb.eval_dense(dev(X), dev(t), plan, 0.25, h, dev(w))
     o = oracle.eval_dense(X, t, Q, Lam, 0.25, h, w)
-    check(*g, *o, iters_slack=3, frac_exact=0.8)
+    check(*g, *o)
 
 
 def test_full_size_c3_sampled(hb):
@@ -268,7 +269,7 @@ def test_full_size_c4_sampled(hb):
     torch.cuda.synchronize()
     idx = np.sort(np.random.default_rng(3).choice(wl.M, 200, replace=False))
     o = oracle.eval_dense(X[idx], t[idx], wl.Q, wl.Lam, wl.gamma, "l1")
-    check(phi[idx], grad[idx], it[idx], *o, iters_slack=3, frac_exact=0.8)
+    check(phi[idx], grad[idx], it[idx], *o)
     assert np.all(it.cpu().numpy() > 0)
 
 
