@@ -115,18 +115,25 @@ __device__ __forceinline__ void group_reduce4(float v0, float v1, float v2, floa
   }
 }
 
-// kappa_j of this lane from shared memory (non-union kernels).  ld.volatile keeps the load
-// inside the loop (no hoisting back into registers): kappa is the same for every point, so it
-// is held once per CTA instead of occupying CPL registers per thread.
-__device__ __forceinline__ float lds_volatile(const float *p) {
-  float v;
-  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
-  return v;
+// ---- packed fp32x2 helpers (sm_100 FADD2 / FFMA2: two lanes' worth of FP32 work per issue) --
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+// a - b as one FFMA2 with a broadcast -1 (exact: b * -1 is exact, one rounding of the sum);
+// FADD2 has no operand-negate modifier, so a negated pair would cost two scalar FADDs.
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 splat2(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 clamp2(float2 u, float2 t) {
+  return make_float2(fminf(fmaxf(u.x, -t.x), t.x), fminf(fmaxf(u.y, -t.y), t.y));
 }
-__device__ __forceinline__ float4 lds_volatile4(const float *p) {
-  float4 v;
-  asm volatile("ld.volatile.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+#define HOPF_SLOT(arr, j) (((j) & 1) ? (arr)[(j) >> 1].y : (arr)[(j) >> 1].x)
+
+// kappa pair p of this lane from shared memory (non-union kernels).  ld.volatile keeps the
+// load inside the loop (no hoisting back into registers): kappa is the same for every point,
+// so it is held once per CTA instead of occupying CPL registers per thread.
+__device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
+  float2 v;
+  asm volatile("ld.volatile.shared.v2.f32 {%0,%1}, [%2];"
+               : "=f"(v.x), "=f"(v.y)
                : "r"((unsigned)__cvta_generic_to_shared(p)));
   return v;
 }
@@ -135,12 +142,14 @@ __device__ __forceinline__ float4 lds_volatile4(const float *p) {
 //   UNION = false: K1/K2 (kappa for the whole CTA in shared memory, one solve per point)
 //   UNION = true : K4 (K solves per point, kappa per set in registers, running arg-min,
 //                  optional Y / kstar / phi_k)
-// Loop trips alternate between two register sets for d and v_prev (A -> B, B -> A), so the
-// loop-carried updates are renamings instead of register moves.
+// Slots are processed in pairs (slot j <-> pair j/2, half j&1) with packed FP32x2
+// instructions, and every state variable is updated in place (no loop-carried copies):
+//   d <- d + (d' - d), v <- v + (v' - v) reproduce d', v' to within one rounding and keep the
+//   exact zeros of the shrink (d' = 0 gives d - d = 0).
 template <int G, int CPL, int HK, bool UNION>
 __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
   constexpr bool KSM = !UNION;            // kappa in shared memory
-  constexpr int CPL4 = (CPL % 4 == 0) ? CPL / 4 : 0;
+  constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -150,29 +159,26 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
   // slots j < jmax of this lane hold real coordinates (i = gl + G*j < n)
   const int jmax = (n - gl + G - 1) / G;
 
-  // Per-slot registers.
-  float xh[CPL], dA[CPL], dB[CPL], b[CPL], vA[CPL], vB[CPL];
-  float kap[KSM ? 1 : CPL];
-  float tau[HK == HK_WL1 ? CPL : 1];
-  float xr[UNION ? CPL : 1];   // union: the raw point x (sets translate it by c_k)
-  float bd[UNION ? CPL : 1];   // union: grad of the best set so far
+  // Per-slot registers (pairs).
+  float2 xh[NP], d[NP], b[NP], v[NP];
+  float2 kap[KSM ? 1 : NP];
+  float2 tau[HK == HK_WL1 ? NP : 1];
+  float2 xr[UNION ? NP : 1];   // union: the raw point x (sets translate it by c_k)
+  float2 bd[UNION ? NP : 1];   // union: grad of the best set so far
 
-  // kappa_i = lambda/(D_i+lambda), layout [j/4][G][4] so a lane reads 4 slots with one LDS.128
-  __shared__ __align__(16) float kap_s[KSM ? CPL * G : 1];
+  // kappa_i = lambda/(D_i+lambda), layout [pair][G] of float2
+  __shared__ __align__(16) float2 kap_s[KSM ? NP * G : 1];
   if (KSM) {
-    for (int e = threadIdx.x; e < CPL * G; e += blockDim.x) {
-      int j, l;
-      if (CPL4) { j = (e / (4 * G)) * 4 + (e & 3); l = (e / 4) % G; }
-      else { j = e / G; l = e % G; }
-      const int i = l + G * j;
-      kap_s[e] = (i < n) ? __fdividef(lam, __ldg(p.D + i) + lam) : 0.f;
+    for (int e = threadIdx.x; e < NP * G; e += blockDim.x) {
+      const int pp = e / G, l = e % G;
+      const int i0 = l + G * (2 * pp), i1 = l + G * (2 * pp + 1);
+      float2 kv;
+      kv.x = (2 * pp < CPL && i0 < n) ? __fdividef(lam, __ldg(p.D + i0) + lam) : 0.f;
+      kv.y = (2 * pp + 1 < CPL && i1 < n) ? __fdividef(lam, __ldg(p.D + i1) + lam) : 0.f;
+      kap_s[e] = kv;
     }
     __syncthreads();
   }
-  auto kappa_ptr = [&](int j) -> const float * {
-    if (CPL4) return kap_s + (j / 4) * 4 * G + gl * 4 + (j & 3);
-    return kap_s + j * G + gl;
-  };
 
   int64_t pt = gid;
   bool have = pt < p.M;
@@ -194,11 +200,12 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
       bad = !(tt >= 0.f) || !finite_f(tt);
       const float *xrow = p.X + pt * (int64_t)n;
 #pragma unroll
-      for (int j = 0; j < CPL; j++) {
-        const int i = gl + G * j;
-        const float xv = (j < jmax) ? __ldg(xrow + i) : 0.f;
-        bad |= !finite_f(xv);
-        if (UNION) xr[j] = xv; else xh[j] = xv;
+      for (int q = 0; q < NP; q++) {
+        const int j0 = 2 * q, j1 = 2 * q + 1;
+        const float x0 = (j0 < CPL && j0 < jmax) ? __ldg(xrow + gl + G * j0) : 0.f;
+        const float x1 = (j1 < CPL && j1 < jmax) ? __ldg(xrow + gl + G * j1) : 0.f;
+        bad |= !finite_f(x0) || !finite_f(x1);
+        if (UNION) xr[q] = make_float2(x0, x1); else xh[q] = make_float2(x0, x1);
       }
     }
     bad = group_any<G>(bad);
@@ -209,30 +216,28 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
   };
 
   // ---- set up one solve: centred start v0 = d0 = x - c, b0 = 0 (reading R5) -------
-  // Writes the "current" register set (d, v) that the next trip reads.
-  auto setup_solve = [&](float (&d)[CPL], float (&vp)[CPL]) {
+  auto setup_solve = [&]() {
     const float *Dp = UNION ? p.D + (size_t)kset * n : p.D;
     const float *cp = UNION ? p.c + (size_t)kset * n : p.c;
-    // stage D, c (and w) into registers that are re-initialised below
-#pragma unroll
-    for (int j = 0; j < CPL; j++) {
-      const int i = gl + G * j;
-      d[j] = (j < jmax) ? __ldg(Dp + i) : 1.f;
-      b[j] = (cp && j < jmax) ? __ldg(cp + i) : 0.f;
-      if (HK == HK_WL1) tau[j] = (j < jmax) ? __ldg(p.w + i) : 0.f;
-    }
     const float tl = tt / lam;
 #pragma unroll
-    for (int j = 0; j < CPL; j++) {
-      const float xv = UNION ? xr[j] : xh[j];
-      const float xt = (j < jmax) ? xv - b[j] : 0.f;
-      const float dinv = __fdividef(1.f, d[j] + lam);
-      if (!KSM) kap[j] = (j < jmax) ? lam * dinv : 0.f;
-      if (HK == HK_WL1) tau[j] *= tl;
-      xh[j] = xt * dinv;
-      d[j] = xt;                          // d^0 = x - c
-      b[j] = (HK == HK_L2) ? xt : 0.f;    // l2: pending u with s = 1 reproduces d^0, b^0 = 0
-      vp[j] = xt;                         // v^0 = x - c
+    for (int q = 0; q < NP; q++) {
+      const int j0 = 2 * q, j1 = 2 * q + 1;
+      const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
+      const int i0 = gl + G * j0, i1 = gl + G * j1;
+      const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
+      const float c0 = (cp && ok0) ? __ldg(cp + i0) : 0.f, c1 = (cp && ok1) ? __ldg(cp + i1) : 0.f;
+      const float2 xv = UNION ? xr[q] : xh[q];
+      const float xt0 = ok0 ? xv.x - c0 : 0.f, xt1 = ok1 ? xv.y - c1 : 0.f;
+      const float di0 = __fdividef(1.f, D0 + lam), di1 = __fdividef(1.f, D1 + lam);
+      if (!KSM) kap[q] = make_float2(ok0 ? lam * di0 : 0.f, ok1 ? lam * di1 : 0.f);
+      if (HK == HK_WL1)
+        tau[q] = make_float2(ok0 ? tl * __ldg(p.w + i0) : 0.f, ok1 ? tl * __ldg(p.w + i1) : 0.f);
+      const float2 xt = make_float2(xt0, xt1);
+      xh[q] = make_float2(xt0 * di0, xt1 * di1);
+      d[q] = xt;                                  // d^0 = x - c
+      b[q] = (HK == HK_L2) ? xt : splat2(0.f);    // l2: pending u with s = 1 gives d^0, b^0 = 0
+      v[q] = xt;                                  // v^0 = x - c
     }
     it = 0;
     s_cur = 1.f;
@@ -241,137 +246,126 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
 
   load_point(have);
   if (have) {
-    setup_solve(dA, vA);
+    setup_solve();
     if (UNION) { best = __int_as_float(0x7f800000); bestk = -1; bestit = 0; }
   } else {
 #pragma unroll
-    for (int j = 0; j < CPL; j++) { xh[j] = 0.f; dA[j] = 0.f; b[j] = 0.f; vA[j] = 0.f; if (!KSM) kap[j] = 0.f; }
+    for (int q = 0; q < NP; q++) {
+      xh[q] = d[q] = b[q] = v[q] = splat2(0.f);
+      if (!KSM) kap[q] = splat2(0.f);
+    }
   }
 
-  // ---- one loop trip: reads (di, vi), writes (dO, vO) ------------------------------------
-  // l1/wl1: the full iteration k = it+1, one reduction of (sd, sb, sv).
-  // l2: software-pipelined so that one reduction per iteration suffices: the trip finishes
-  //     iteration k = it ((3.4b), (3.4c) with the shrink factor s_k reduced in the previous
-  //     trip, plus the test sums sd_k, sb_k) and starts iteration k+1 ((3.4a), u_{k+1}, the
-  //     test sum sv_{k+1} and ||u_{k+1}||^2); the four sums are reduced together.  Between trips
-  //     b[j] holds u_{k+1}; dO = d_k is not touched by the (3.4a) half, so a point that stops at
-  //     k outputs d_k.  After setup_solve the first trip's (3.4b) half is the identity (s = 1,
-  //     u = x - c) and its test is skipped.
   bool conv = false;
-  int kdone = 0;
-  auto trip = [&](const float (&di)[CPL], float (&dO)[CPL], const float (&vi)[CPL], float (&vO)[CPL]) {
-    float pa0 = 0.f, pa1 = 0.f, pb0 = 0.f, pb1 = 0.f, pc0 = 0.f, pc1 = 0.f, pr0 = 0.f, pr1 = 0.f;
-    float kv[4];
+  int kdone = 0;   // iteration whose test the last trip decided (0 = none)
+
+  while (__any_sync(0xffffffffu, have)) {
+    // ================= one loop trip (all lanes, branch-free) ===============================
+    // l1/wl1: the full iteration k = it+1, one reduction of (sd, sb, sv).
+    // l2: software-pipelined so that one reduction per iteration suffices: the trip finishes
+    //     iteration k = it ((3.4b), (3.4c) with the shrink factor s_k reduced in the previous
+    //     trip, plus the test sums sd_k, sb_k) and starts iteration k+1 ((3.4a), u_{k+1}, the
+    //     test sum sv_{k+1} and ||u_{k+1}||^2); the four sums are reduced together.  Between trips
+    //     b holds u_{k+1}; d = d_k is not touched by the (3.4a) half, so a point that stops at
+    //     k outputs d_k.  After setup_solve the first trip's (3.4b) half is the identity
+    //     (s = 1, u = x - c) and its test is skipped.
+    float2 a0 = splat2(0.f), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0, r0 = a0, r1 = a0;
+    const float2 sP = splat2(s_cur), tP = splat2(tauS);
 #pragma unroll
-    for (int j = 0; j < CPL; j++) {
-      float kj;
-      if (KSM) {
-        if (CPL4) {
-          if ((j & 3) == 0) { const float4 k4 = lds_volatile4(kappa_ptr(j)); kv[0] = k4.x; kv[1] = k4.y; kv[2] = k4.z; kv[3] = k4.w; }
-          kj = kv[j & 3];
-        } else {
-          kj = lds_volatile(kappa_ptr(j));
-        }
-      } else {
-        kj = kap[j];
-      }
+    for (int q = 0; q < NP; q++) {
+      const float2 kq = KSM ? lds_volatile2(kap_s + q * G + gl) : kap[q];
       if (HK == HK_L2) {
-        const float u = b[j];
-        const float dn = s_cur * u;                // (3.4b) shrink_2 of iteration k
-        const float dd = dn - di[j];
-        const float dmv = dn - vi[j];              // d^k - v^k
-        const float bn = u - dn;                   // (3.4c): b + v - d' = u - d'
-        if (j & 1) { pa1 = fmaf(dd, dd, pa1); pb1 = fmaf(dmv, dmv, pb1); }
-        else       { pa0 = fmaf(dd, dd, pa0); pb0 = fmaf(dmv, dmv, pb0); }
-        dO[j] = dn;
-        const float a = dn - bn;
-        const float v = fmaf(kj, a, xh[j]);        // (3.4a) of iteration k+1
-        const float dv = v - vi[j];
-        const float un = v + bn;                   // u_{k+1}, argument of the next (3.4b)
-        if (j & 1) { pc1 = fmaf(dv, dv, pc1); pr1 = fmaf(un, un, pr1); }
-        else       { pc0 = fmaf(dv, dv, pc0); pr0 = fmaf(un, un, pr0); }
-        vO[j] = v;
-        b[j] = un;
+        const float2 dd = sub2(fma2(sP, b[q], splat2(0.f)), d[q]);         // d_k - d_{k-1}, d_k = s_k u_k (3.4b)
+        d[q] = add2(d[q], dd);                                            // d_k
+        const float2 dmv = sub2(d[q], v[q]);                              // d^k - v^k
+        b[q] = sub2(b[q], d[q]);                                          // (3.4c): b_k = u_k - d_k
+        const float2 a = sub2(d[q], b[q]);
+        const float2 t = sub2(xh[q], v[q]);
+        const float2 dv = fma2(kq, a, t);                                 // (3.4a): v_{k+1} - v_k
+        v[q] = add2(v[q], dv);                                            // v_{k+1}
+        b[q] = add2(v[q], b[q]);                                          // u_{k+1} = v_{k+1} + b_k
+        if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
+        else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
       } else {
-        const float a = di[j] - b[j];
-        const float v = fmaf(kj, a, xh[j]);        // (3.4a)
-        const float dv = v - vi[j];
-        vO[j] = v;
-        const float u = v + b[j];
-        const float tj = (HK == HK_WL1) ? tau[j] : tauS;
-        const float bn = fminf(fmaxf(u, -tj), tj); // projection on the box [-tau, tau] (Moreau)
-        const float dn = u - bn;                   // (3.4b) shrink_1; (3.4c) b' = u - d' = bn
-        const float dd = dn - di[j];
-        const float dmv = dn - v;                  // d^k - v^k
-        if (j & 1) { pa1 = fmaf(dd, dd, pa1); pb1 = fmaf(dmv, dmv, pb1); pc1 = fmaf(dv, dv, pc1); }
-        else       { pa0 = fmaf(dd, dd, pa0); pb0 = fmaf(dmv, dmv, pb0); pc0 = fmaf(dv, dv, pc0); }
-        dO[j] = dn;
-        b[j] = bn;
+        const float2 a = sub2(d[q], b[q]);
+        const float2 t = sub2(xh[q], v[q]);
+        const float2 dv = fma2(kq, a, t);                                 // (3.4a): v^k - v^{k-1}
+        v[q] = add2(v[q], dv);                                            // v^k
+        const float2 u = add2(v[q], b[q]);
+        b[q] = clamp2(u, HK == HK_WL1 ? tau[q] : tP);                      // projection on [-tau, tau]
+        const float2 dn = sub2(u, b[q]);                                  // (3.4b) shrink_1; b^k = u - d^k
+        const float2 dd = sub2(dn, d[q]);
+        d[q] = add2(d[q], dd);                                            // d^k (exact zeros kept)
+        const float2 dmv = sub2(d[q], v[q]);                              // d^k - v^k
+        if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); }
+        else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); }
       }
     }
-    if (HK == HK_L2) {
+    const float psd = (a0.x + a0.y) + (a1.x + a1.y), psb = (b0.x + b0.y) + (b1.x + b1.y);
+    const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
+    {
       float r2;
       bool ok_sd, ok_sb, ok_sv;
-      group_reduce4<G>(pa0 + pa1, pb0 + pb1, pc0 + pc1, pr0 + pr1, tol, r2, ok_sd, ok_sb, ok_sv);
-      kdone = it;
-      conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it
-      sv_ok = ok_sv;                                  // ||v^{k+1} - v^k||^2 <= tol, for the next trip
-      const float r = sqrtf(r2);
-      s_cur = (r > tauS) ? (r - tauS) / r : 0.f;     // shrink_2 factor of iteration k+1
-      it++;
-    } else {
-      float dummy;
-      bool ok_sd, ok_sb, ok_sv;
-      group_reduce4<G>(pa0 + pa1, pb0 + pb1, pc0 + pc1, 0.f, tol, dummy, ok_sd, ok_sb, ok_sv);
-      it++;
-      kdone = it;
-      conv = ok_sd && ok_sb && ok_sv;
+      group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
+      if (HK == HK_L2) {
+        kdone = it;
+        conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it
+        sv_ok = ok_sv;                                  // ||v^{k+1} - v^k||^2 <= tol, next trip
+        const float r = sqrtf(r2);
+        s_cur = (r > tauS) ? (r - tauS) / r : 0.f;     // shrink_2 factor of k+1
+        it++;
+      } else {
+        it++;
+        kdone = it;
+        conv = ok_sd && ok_sb && ok_sv;
+      }
     }
-  };
+    const bool done = have && (spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)));
+    if (!__any_sync(0xffffffffu, done)) continue;
 
-  // ---- finalize the groups whose solve stopped, refill them (collective) ------------------
-  // d = the current d^k, vp = the current v register set (scratch for done groups).
-  auto finalize = [&](float (&d)[CPL], float (&vp)[CPL], bool done) {
+    // ============ finalize (all lanes compute; done groups store and refill) =================
     // phi = <x - c, d> - 1/2 <d, D d> - t H(d) + gamma   ((3.3) at d, reading R2)
     // t == 0: phi = J(x) = 1/2 <x-c, D^{-1}(x-c)> + gamma, grad = D^{-1}(x-c) (reading R6)
     const float *Dp = UNION ? p.D + (size_t)kset * n : p.D;
     const float *cp = UNION ? p.c + (size_t)kset * n : p.c;
     const float *xrow = p.X + pt * (int64_t)n;
-    float q = 0.f, hsum = 0.f;
+    float qs = 0.f, hsum = 0.f;
     if (done && spec != 2) {
-      // the solve state of a done group is dead: stage x - c in vp and D in xh
+      // the solve state of a done group is dead: compute from pairs, grad J(x) into d for t == 0
 #pragma unroll
-      for (int j = 0; j < CPL; j++) {
-        const int i = gl + G * j;
-        if (j < jmax) {
-          const float xv = UNION ? xr[j] : __ldg(xrow + i);
-          vp[j] = cp ? xv - __ldg(cp + i) : xv;
-          xh[j] = __ldg(Dp + i);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < CPL; j++) {
-        if (j < jmax) {
-          const float xt = vp[j], Dv = xh[j];
-          if (spec == 1) {
-            d[j] = __fdividef(xt, Dv);   // grad J(x)
-            q = fmaf(0.5f * xt, d[j], q);
-          } else {
-            q = fmaf(xt, d[j], q);
-            q = fmaf(-0.5f * Dv * d[j], d[j], q);
-            if (HK == HK_L2) hsum = fmaf(d[j], d[j], hsum);
-            else if (HK == HK_WL1) hsum = fmaf(__ldg(p.w + gl + G * j), fabsf(d[j]), hsum);
-            else hsum += fabsf(d[j]);
-          }
+      for (int q = 0; q < NP; q++) {
+        const int j0 = 2 * q, j1 = 2 * q + 1;
+        const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
+        const int i0 = gl + G * j0, i1 = gl + G * j1;
+        const float2 xv = UNION ? xr[q] : make_float2(ok0 ? __ldg(xrow + i0) : 0.f,
+                                                      ok1 ? __ldg(xrow + i1) : 0.f);
+        const float xt0 = (cp && ok0) ? xv.x - __ldg(cp + i0) : xv.x;
+        const float xt1 = (cp && ok1) ? xv.y - __ldg(cp + i1) : xv.y;
+        const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
+        float2 dq = d[q];
+        if (spec == 1) {
+          dq = make_float2(ok0 ? __fdividef(xt0, D0) : 0.f, ok1 ? __fdividef(xt1, D1) : 0.f);
+          qs = fmaf(0.5f * xt0, dq.x, fmaf(0.5f * xt1, dq.y, qs));
+          d[q] = dq;
+        } else {
+          qs = fmaf(xt0, dq.x, qs);
+          qs = fmaf(-0.5f * D0 * dq.x, dq.x, qs);
+          qs = fmaf(xt1, dq.y, qs);
+          qs = fmaf(-0.5f * D1 * dq.y, dq.y, qs);
+          if (HK == HK_L2) hsum = fmaf(dq.x, dq.x, fmaf(dq.y, dq.y, hsum));
+          else if (HK == HK_WL1)
+            hsum = fmaf(ok0 ? __ldg(p.w + i0) : 0.f, fabsf(dq.x),
+                        fmaf(ok1 ? __ldg(p.w + i1) : 0.f, fabsf(dq.y), hsum));
+          else hsum += fabsf(dq.x) + fabsf(dq.y);
         }
       }
     }
-    q = group_sum<G>(q);
+    qs = group_sum<G>(qs);
     hsum = group_sum<G>(hsum);
     const float gam = UNION ? __ldg(p.gk + kset) : p.gamma;
     float phiv;
-    if (spec == 1) phiv = q + gam;
-    else phiv = q - tt * (HK == HK_L2 ? sqrtf(hsum) : hsum) + gam;
+    if (spec == 1) phiv = qs + gam;
+    else phiv = qs - tt * (HK == HK_L2 ? sqrtf(hsum) : hsum) + gam;
     int status = (spec == 1) ? 0 : (conv ? kdone : -p.max_iter);
     if (spec == 2) { phiv = __int_as_float(0x7fc00000); status = INT32_MIN; }
 
@@ -382,14 +376,14 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
         if (phiv < best) {   // strict: lowest k wins ties (R19); NaN never wins
           best = phiv; bestk = kset; bestit = status;
 #pragma unroll
-          for (int j = 0; j < CPL; j++) bd[j] = d[j];
+          for (int q = 0; q < NP; q++) bd[q] = d[q];
         }
         point_done = (spec == 2) || (kset + 1 >= p.K);
       }
       // ||grad|| of the winner for y (all lanes participate in the reduction)
       float gn = 0.f;
 #pragma unroll
-      for (int j = 0; j < CPL; j++) gn = fmaf(bd[j], bd[j], gn);
+      for (int q = 0; q < NP; q++) gn = fmaf(bd[q].x, bd[q].x, fmaf(bd[q].y, bd[q].y, gn));
       gn = sqrtf(group_sum<G>(gn));
       const float ign = (gn > 0.f) ? __fdividef(1.f, gn) : 0.f;
       if (point_done) {
@@ -405,12 +399,13 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
         for (int j = 0; j < CPL; j++) {
           const int i = gl + G * j;
           if (j < jmax) {
-            grow[i] = nanpt ? __int_as_float(0x7fc00000) : bd[j];
+            const float gj = HOPF_SLOT(bd, j);
+            grow[i] = nanpt ? __int_as_float(0x7fc00000) : gj;
             if (yrow) {
               float y;
               if (nanpt) y = __int_as_float(0x7fc00000);
-              else if (gn > 0.f) y = xr[j] - tt * (bd[j] * ign);
-              else y = __ldg(p.c + (size_t)bestk * n + i);                // reading R18
+              else if (gn > 0.f) y = HOPF_SLOT(xr, j) - tt * (gj * ign);
+              else y = __ldg(p.c + (size_t)bestk * n + i);                  // reading R18
               yrow[i] = y;
             }
           }
@@ -422,10 +417,10 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
 #pragma unroll
       for (int j = 0; j < CPL; j++) {
         const int i = gl + G * j;
-        if (j < jmax) grow[i] = (spec == 2) ? __int_as_float(0x7fc00000) : d[j];
+        if (j < jmax) grow[i] = (spec == 2) ? __int_as_float(0x7fc00000) : HOPF_SLOT(d, j);
       }
     }
-    // ---- refill: the next set of the point (union) or the next point of this group -------
+    // ---- refill: the next set of the point (union) or the next point of this group ---------
     if (point_done) {
       pt += ngroups;
       have = pt < p.M;
@@ -435,29 +430,13 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
       if (have) {
         kset = point_done ? 0 : kset + 1;
         if (UNION && point_done) { best = __int_as_float(0x7f800000); bestk = -1; bestit = 0; }
-        setup_solve(d, vp);
+        setup_solve();
       } else {
 #pragma unroll
-        for (int j = 0; j < CPL; j++) { xh[j] = 0.f; d[j] = 0.f; b[j] = 0.f; vp[j] = 0.f; }
+        for (int q = 0; q < NP; q++) xh[q] = d[q] = b[q] = v[q] = splat2(0.f);
         spec = 0;
+        kdone = 0;
       }
-    }
-  };
-
-  auto done_now = [&]() {
-    return have && (spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)));
-  };
-
-  while (__any_sync(0xffffffffu, have)) {
-    trip(dA, dB, vA, vB);
-    {
-      const bool done = done_now();
-      if (__any_sync(0xffffffffu, done)) finalize(dB, vB, done);
-    }
-    trip(dB, dA, vB, vA);
-    {
-      const bool done = done_now();
-      if (__any_sync(0xffffffffu, done)) finalize(dA, vA, done);
     }
   }
 }

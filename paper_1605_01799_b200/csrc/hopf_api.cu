@@ -56,11 +56,17 @@ struct Variant {
   KernFn fn[3][2];  // [h kind][union]
 };
 
+// union kernels keep x and the best grad resident too: only CPL <= 16 is instantiated
+template <int G, int C, int H>
+constexpr KernFn union_fn() {
+  if constexpr (C <= 16) return hopf_diag_kernel<G, C, H, true>;
+  else return nullptr;
+}
 #define HOPF_VARIANT(G_, C_)                                                                 \
   {G_, C_,                                                                                   \
-   {{hopf_diag_kernel<G_, C_, HK_L1, false>, hopf_diag_kernel<G_, C_, HK_L1, true>},         \
-    {hopf_diag_kernel<G_, C_, HK_WL1, false>, hopf_diag_kernel<G_, C_, HK_WL1, true>},       \
-    {hopf_diag_kernel<G_, C_, HK_L2, false>, hopf_diag_kernel<G_, C_, HK_L2, true>}}}
+   {{hopf_diag_kernel<G_, C_, HK_L1, false>, union_fn<G_, C_, HK_L1>()},                     \
+    {hopf_diag_kernel<G_, C_, HK_WL1, false>, union_fn<G_, C_, HK_WL1>()},                   \
+    {hopf_diag_kernel<G_, C_, HK_L2, false>, union_fn<G_, C_, HK_L2>()}}}
 
 // Ordered by padded width G*CPL, then G: the first variant with G*CPL >= n is used.
 static const Variant kVariants[] = {
@@ -70,10 +76,9 @@ static const Variant kVariants[] = {
     HOPF_VARIANT(16, 32), HOPF_VARIANT(32, 32)};
 
 static const Variant *pick_variant(int n, bool is_union) {
-  // union keeps x and the best grad resident too: cap CPL at 16 for register room
   for (const Variant &v : kVariants) {
     if (v.G * v.CPL < n) continue;
-    if (is_union && v.CPL > 16 && n > 16) continue;
+    if (is_union && v.fn[0][1] == nullptr) continue;
     return &v;
   }
   return nullptr;
@@ -84,13 +89,27 @@ static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
   const Variant *v = pick_variant(p.n, is_union);
   if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
   KernFn fn = v->fn[(int)h][is_union ? 1 : 0];
-  const int threads = 256;
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0);
-  if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+  // Block size: the one that keeps the most warps resident per SM (register-limited kernels
+  // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
+  struct Occ { int threads, per_sm; };
+  static thread_local KernFn cached_fn = nullptr;
+  static thread_local Occ cached{256, 1};
+  if (cached_fn != fn) {
+    Occ bestc{256, 0};
+    for (int th : {256, 128, 64, 32}) {
+      if (th < v->G) continue;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, th, 0) != cudaSuccess) continue;
+      if (per_sm * th > bestc.per_sm * bestc.threads) bestc = {th, per_sm};
+    }
+    if (bestc.per_sm < 1) bestc = {256, 1};
+    cached = bestc;
+    cached_fn = fn;
+  }
+  const int threads = cached.threads;
   const int64_t groups_needed = p.M;
   const int64_t blocks_needed = (groups_needed * v->G + threads - 1) / threads;
-  int64_t blocks = (int64_t)num_sms() * per_sm;
+  int64_t blocks = (int64_t)num_sms() * cached.per_sm;
   if (blocks > blocks_needed) blocks = blocks_needed;
   if (blocks < 1) blocks = 1;
   fn<<<(unsigned)blocks, threads, 0, stream>>>(p);
