@@ -243,6 +243,10 @@ def main():
     torch.cuda.synchronize(dev)
     iters_np = iters.cpu().numpy()
     launches_per_step = hb.last_launch_count()
+    import ctypes
+    _th, _bl = ctypes.c_int32(0), ctypes.c_int32(0)
+    L.hopf_last_launch_config(ctypes.byref(_th), ctypes.byref(_bl))
+    launch_cfg = {"threads_per_block": _th.value, "blocks": _bl.value}
 
     uuid = None
     try:
@@ -353,6 +357,7 @@ def main():
             "data": "synthetic (seeded; BASELINE config law)", "config": config_dict(wl, ws),
             "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
+            "launch": launch_cfg if wl.kind != "dense" else None,
             "iters": {"min": int(conv.min()) if conv.size else None,
                       "mean": float(conv.mean()) if conv.size else None,
                       "max": int(conv.max()) if conv.size else None,

@@ -115,7 +115,7 @@ int hopf_eval_dense(int64_t M, int32_t n, const float *X, const float *t,
  * pointers as above.  The call splits the points into chunks and pipelines
  * host->device copies, kernels and device->host copies on internal streams of the
  * current device; it returns after all results are in host memory (synchronous).
- * Device work buffers are allocated per call.                                              */
+ * Device work buffers and streams are cached per device (grown on demand).                                              */
 int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host, const float *t_host,
                         const float *Dj, const float *c, float gamma, hopf_h_kind h,
                         const float *w, float lambda, int32_t max_iter, float tol,
@@ -123,6 +123,10 @@ int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host, const float *
 
 /* Number of kernel launches the most recent successful call made on this thread. */
 int32_t hopf_last_launch_count(void);
+
+/* Launch shape of the most recent diag/union kernel launch on this thread (threads per block,
+ * blocks); returns hopf_last_launch_count().  Either pointer may be NULL. */
+int32_t hopf_last_launch_config(int32_t *threads_per_block, int32_t *blocks);
 
 /* Text of the most recent error on this thread ("" if none) and a static string for a code. */
 const char *hopf_last_error(void);

@@ -53,6 +53,8 @@ def lib():
         L.hopf_strerror.restype = ctypes.c_char_p
         L.hopf_strerror.argtypes = [ctypes.c_int]
         L.hopf_last_launch_count.restype = ctypes.c_int32
+        L.hopf_last_launch_config.restype = ctypes.c_int32
+        L.hopf_last_launch_config.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         L.hopf_version.restype = ctypes.c_int32
         _lib = L
     return _lib

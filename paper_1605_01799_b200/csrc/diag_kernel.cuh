@@ -115,7 +115,7 @@ __device__ __forceinline__ void group_reduce4(float v0, float v1, float v2, floa
   }
 }
 
-// ---- packed fp32x2 helpers (sm_100 FADD2 / FFMA2: two lanes' worth of FP32 work per issue) --
+// ---- packed fp32x2 helpers (sm_100 FADD2 / FFMA2: two slots of FP32 work per issue) --------
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 // a - b as one FFMA2 with a broadcast -1 (exact: b * -1 is exact, one rounding of the sum);
 // FADD2 has no operand-negate modifier, so a negated pair would cost two scalar FADDs.
@@ -125,11 +125,12 @@ __device__ __forceinline__ float2 splat2(float s) { return make_float2(s, s); }
 __device__ __forceinline__ float2 clamp2(float2 u, float2 t) {
   return make_float2(fminf(fmaxf(u.x, -t.x), t.x), fminf(fmaxf(u.y, -t.y), t.y));
 }
+
 #define HOPF_SLOT(arr, j) (((j) & 1) ? (arr)[(j) >> 1].y : (arr)[(j) >> 1].x)
 
-// kappa pair p of this lane from shared memory (non-union kernels).  ld.volatile keeps the
-// load inside the loop (no hoisting back into registers): kappa is the same for every point,
-// so it is held once per CTA instead of occupying CPL registers per thread.
+// kappa pair of this lane from shared memory (non-union kernels).  ld.volatile keeps the load
+// inside the loop (no hoisting back into registers): kappa is the same for every point, so it
+// is held once per CTA instead of occupying CPL registers per thread.
 __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
   float2 v;
   asm volatile("ld.volatile.shared.v2.f32 {%0,%1}, [%2];"
@@ -142,14 +143,23 @@ __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
 //   UNION = false: K1/K2 (kappa for the whole CTA in shared memory, one solve per point)
 //   UNION = true : K4 (K solves per point, kappa per set in registers, running arg-min,
 //                  optional Y / kstar / phi_k)
+//
 // Slots are processed in pairs (slot j <-> pair j/2, half j&1) with packed FP32x2
 // instructions, and every state variable is updated in place (no loop-carried copies):
 //   d <- d + (d' - d), v <- v + (v' - v) reproduce d', v' to within one rounding and keep the
-//   exact zeros of the shrink (d' = 0 gives d - d = 0).
+//   exact zeros of the shrink (d' = 0 gives d - d = 0).  The l2 path carries nd = -d and the
+//   CTA holds -kappa, so that every subtraction it needs is a plain FADD2/FFMA2.
+//
+// Per-point stop handling: a group whose solve stops (paper test, max_iter, t == 0, invalid)
+// freezes its d (the in-place update is multiplied by live = 0) and waits; the warp runs the
+// finalize/refill branch once at least half of its groups wait (or all of its remaining ones),
+// so that with G < 32 the branch is shared by several groups instead of run once per group.
 template <int G, int CPL, int HK, bool UNION>
 __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
-  constexpr bool KSM = !UNION;            // kappa in shared memory
+  constexpr bool KSM = !UNION;            // -kappa in shared memory
   constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
+  constexpr int GPW = 32 / G;             // groups per warp
+  constexpr int WAIT_THRESHOLD = GPW > 1 ? GPW / 2 : 1;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -159,22 +169,23 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
   // slots j < jmax of this lane hold real coordinates (i = gl + G*j < n)
   const int jmax = (n - gl + G - 1) / G;
 
-  // Per-slot registers (pairs).
+  // Per-slot registers (pairs).  d holds -d on the l2 path.
   float2 xh[NP], d[NP], b[NP], v[NP];
-  float2 kap[KSM ? 1 : NP];
+  float2 kap[KSM ? 1 : NP];    // union: -kappa (l2) / kappa (l1) of the current set
   float2 tau[HK == HK_WL1 ? NP : 1];
   float2 xr[UNION ? NP : 1];   // union: the raw point x (sets translate it by c_k)
   float2 bd[UNION ? NP : 1];   // union: grad of the best set so far
 
-  // kappa_i = lambda/(D_i+lambda), layout [pair][G] of float2
+  // -kappa_i (l2) or kappa_i (l1) = lambda/(D_i+lambda), layout [pair][G] of float2
   __shared__ __align__(16) float2 kap_s[KSM ? NP * G : 1];
+  const float ksign = (HK == HK_L2) ? -1.f : 1.f;
   if (KSM) {
     for (int e = threadIdx.x; e < NP * G; e += blockDim.x) {
       const int pp = e / G, l = e % G;
       const int i0 = l + G * (2 * pp), i1 = l + G * (2 * pp + 1);
       float2 kv;
-      kv.x = (2 * pp < CPL && i0 < n) ? __fdividef(lam, __ldg(p.D + i0) + lam) : 0.f;
-      kv.y = (2 * pp + 1 < CPL && i1 < n) ? __fdividef(lam, __ldg(p.D + i1) + lam) : 0.f;
+      kv.x = (2 * pp < CPL && i0 < n) ? ksign * __fdividef(lam, __ldg(p.D + i0) + lam) : 0.f;
+      kv.y = (2 * pp + 1 < CPL && i1 < n) ? ksign * __fdividef(lam, __ldg(p.D + i1) + lam) : 0.f;
       kap_s[e] = kv;
     }
     __syncthreads();
@@ -182,13 +193,15 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
 
   int64_t pt = gid;
   bool have = pt < p.M;
-  int it = 0;         // completed (3.4a) half-steps (l2) / iterations (l1) of the current solve
-  int kset = 0;       // union: current set
-  float tt = 0.f;     // t of the current point
-  float tauS = 0.f;   // scalar threshold t/lambda
-  int spec = 0;       // 0 normal, 1 t == 0, 2 invalid
-  float s_cur = 1.f;  // l2: shrink factor of the pending (3.4b)
-  bool sv_ok = false; // l2: ||v^k - v^{k-1}||^2 <= tol of the pending iteration
+  bool waiting = false; // the current solve stopped; d is frozen until the warp finalizes
+  int wstatus = 0;      // its status (iteration, 0, -max_iter or INT32_MIN)
+  int it = 0;           // completed (3.4a) half-steps (l2) / iterations (l1) of the solve
+  int kset = 0;         // union: current set
+  float tt = 0.f;       // t of the current point
+  float tauS = 0.f;     // scalar threshold t/lambda
+  int spec = 0;         // 0 normal, 1 t == 0, 2 invalid
+  float s_cur = 1.f;    // l2: shrink factor of the pending (3.4b)
+  bool sv_ok = false;   // l2: ||v^k - v^{k-1}||^2 <= tol of the pending iteration
   float best = 0.f;
   int bestk = -1, bestit = 0;
 
@@ -230,18 +243,24 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
       const float2 xv = UNION ? xr[q] : xh[q];
       const float xt0 = ok0 ? xv.x - c0 : 0.f, xt1 = ok1 ? xv.y - c1 : 0.f;
       const float di0 = __fdividef(1.f, D0 + lam), di1 = __fdividef(1.f, D1 + lam);
-      if (!KSM) kap[q] = make_float2(ok0 ? lam * di0 : 0.f, ok1 ? lam * di1 : 0.f);
+      if (!KSM) kap[q] = make_float2(ok0 ? ksign * lam * di0 : 0.f, ok1 ? ksign * lam * di1 : 0.f);
       if (HK == HK_WL1)
         tau[q] = make_float2(ok0 ? tl * __ldg(p.w + i0) : 0.f, ok1 ? tl * __ldg(p.w + i1) : 0.f);
       const float2 xt = make_float2(xt0, xt1);
       xh[q] = make_float2(xt0 * di0, xt1 * di1);
-      d[q] = xt;                                  // d^0 = x - c
-      b[q] = (HK == HK_L2) ? xt : splat2(0.f);    // l2: pending u with s = 1 gives d^0, b^0 = 0
-      v[q] = xt;                                  // v^0 = x - c
+      if (HK == HK_L2) {
+        d[q] = make_float2(-xt0, -xt1);   // -d^0 = -(x - c)
+        b[q] = xt;                        // pending u with s = 1 reproduces d^0 and b^0 = 0
+      } else {
+        d[q] = xt;                        // d^0 = x - c
+        b[q] = splat2(0.f);               // b^0 = 0
+      }
+      v[q] = xt;                          // v^0 = x - c
     }
     it = 0;
     s_cur = 1.f;
     sv_ok = false;
+    waiting = false;
   };
 
   load_point(have);
@@ -256,9 +275,6 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
     }
   }
 
-  bool conv = false;
-  int kdone = 0;   // iteration whose test the last trip decided (0 = none)
-
   while (__any_sync(0xffffffffu, have)) {
     // ================= one loop trip (all lanes, branch-free) ===============================
     // l1/wl1: the full iteration k = it+1, one reduction of (sd, sb, sv).
@@ -271,38 +287,42 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
     //     (s = 1, u = x - c) and its test is skipped.
     float2 a0 = splat2(0.f), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0, r0 = a0, r1 = a0;
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
+    const float live = waiting ? 0.f : 1.f;
 #pragma unroll
     for (int q = 0; q < NP; q++) {
       const float2 kq = KSM ? lds_volatile2(kap_s + q * G + gl) : kap[q];
       if (HK == HK_L2) {
-        const float2 dd = sub2(fma2(sP, b[q], splat2(0.f)), d[q]);         // d_k - d_{k-1}, d_k = s_k u_k (3.4b)
-        d[q] = add2(d[q], dd);                                            // d_k
-        const float2 dmv = sub2(d[q], v[q]);                              // d^k - v^k
-        b[q] = sub2(b[q], d[q]);                                          // (3.4c): b_k = u_k - d_k
-        const float2 a = sub2(d[q], b[q]);
+        // d[q] = -d_{k-1}, kq = -kappa
+        const float2 dd = fma2(sP, b[q], d[q]);        // d_k - d_{k-1}, d_k = s_k u_k (3.4b)
+        d[q] = fma2(dd, splat2(-live), d[q]);          // -d_k (frozen while waiting)
+        const float2 dmv = add2(d[q], v[q]);           // v^k - d^k
+        b[q] = add2(b[q], d[q]);                       // (3.4c): b_k = u_k - d_k
+        const float2 na = add2(d[q], b[q]);            // -(d_k - b_k)
         const float2 t = sub2(xh[q], v[q]);
-        const float2 dv = fma2(kq, a, t);                                 // (3.4a): v_{k+1} - v_k
-        v[q] = add2(v[q], dv);                                            // v_{k+1}
-        b[q] = add2(v[q], b[q]);                                          // u_{k+1} = v_{k+1} + b_k
+        const float2 dv = fma2(kq, na, t);             // (3.4a): v_{k+1} - v_k
+        v[q] = add2(v[q], dv);                         // v_{k+1}
+        b[q] = add2(v[q], b[q]);                       // u_{k+1} = v_{k+1} + b_k
         if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
         else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
       } else {
         const float2 a = sub2(d[q], b[q]);
         const float2 t = sub2(xh[q], v[q]);
-        const float2 dv = fma2(kq, a, t);                                 // (3.4a): v^k - v^{k-1}
-        v[q] = add2(v[q], dv);                                            // v^k
+        const float2 dv = fma2(kq, a, t);              // (3.4a): v^k - v^{k-1}
+        v[q] = add2(v[q], dv);                         // v^k
         const float2 u = add2(v[q], b[q]);
-        b[q] = clamp2(u, HK == HK_WL1 ? tau[q] : tP);                      // projection on [-tau, tau]
-        const float2 dn = sub2(u, b[q]);                                  // (3.4b) shrink_1; b^k = u - d^k
+        b[q] = clamp2(u, HK == HK_WL1 ? tau[q] : tP);  // projection on [-tau, tau] (Moreau)
+        const float2 dn = sub2(u, b[q]);               // (3.4b) shrink_1; b^k = u - d^k
         const float2 dd = sub2(dn, d[q]);
-        d[q] = add2(d[q], dd);                                            // d^k (exact zeros kept)
-        const float2 dmv = sub2(d[q], v[q]);                              // d^k - v^k
+        d[q] = fma2(dd, splat2(live), d[q]);           // d^k (exact zeros kept; frozen while waiting)
+        const float2 dmv = sub2(d[q], v[q]);           // d^k - v^k
         if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); }
         else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); }
       }
     }
     const float psd = (a0.x + a0.y) + (a1.x + a1.y), psb = (b0.x + b0.y) + (b1.x + b1.y);
     const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
+    bool conv;
+    int kdone;
     {
       float r2;
       bool ok_sd, ok_sb, ok_sv;
@@ -320,33 +340,36 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
         conv = ok_sd && ok_sb && ok_sv;
       }
     }
-    const bool done = have && (spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)));
-    if (!__any_sync(0xffffffffu, done)) continue;
+    if (have && !waiting && (spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)))) {
+      waiting = true;
+      wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -p.max_iter));
+    }
+    {
+      const unsigned gbit = (gl == 0) ? 1u : 0u;
+      const int nwait = __popc(__ballot_sync(0xffffffffu, waiting && gbit));
+      const int nhave = __popc(__ballot_sync(0xffffffffu, have && gbit));
+      if (nwait == 0 || (nwait < WAIT_THRESHOLD && nwait < nhave)) continue;
+    }
+    const bool done = waiting;
 
-    // ============ finalize (all lanes compute; done groups store and refill) =================
-    // phi = <x - c, d> - 1/2 <d, D d> - t H(d) + gamma   ((3.3) at d, reading R2)
+    // ============ finalize (all lanes compute; waiting groups store and refill) ==============
+    // phi = <x - c, d> - 1/2 <d, D d> - t H(d) + gamma   ((3.3) at d, reading R2), with
+    //   x - c = x_hat (D + lambda) recovered from registers.
     // t == 0: phi = J(x) = 1/2 <x-c, D^{-1}(x-c)> + gamma, grad = D^{-1}(x-c) (reading R6)
     const float *Dp = UNION ? p.D + (size_t)kset * n : p.D;
-    const float *cp = UNION ? p.c + (size_t)kset * n : p.c;
-    const float *xrow = p.X + pt * (int64_t)n;
     float qs = 0.f, hsum = 0.f;
     if (done && spec != 2) {
-      // the solve state of a done group is dead: compute from pairs, grad J(x) into d for t == 0
 #pragma unroll
       for (int q = 0; q < NP; q++) {
         const int j0 = 2 * q, j1 = 2 * q + 1;
         const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
         const int i0 = gl + G * j0, i1 = gl + G * j1;
-        const float2 xv = UNION ? xr[q] : make_float2(ok0 ? __ldg(xrow + i0) : 0.f,
-                                                      ok1 ? __ldg(xrow + i1) : 0.f);
-        const float xt0 = (cp && ok0) ? xv.x - __ldg(cp + i0) : xv.x;
-        const float xt1 = (cp && ok1) ? xv.y - __ldg(cp + i1) : xv.y;
         const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
-        float2 dq = d[q];
+        const float xt0 = xh[q].x * (D0 + lam), xt1 = xh[q].y * (D1 + lam);
+        float2 dq = (HK == HK_L2) ? make_float2(0.f - d[q].x, 0.f - d[q].y) : d[q];
         if (spec == 1) {
           dq = make_float2(ok0 ? __fdividef(xt0, D0) : 0.f, ok1 ? __fdividef(xt1, D1) : 0.f);
           qs = fmaf(0.5f * xt0, dq.x, fmaf(0.5f * xt1, dq.y, qs));
-          d[q] = dq;
         } else {
           qs = fmaf(xt0, dq.x, qs);
           qs = fmaf(-0.5f * D0 * dq.x, dq.x, qs);
@@ -358,6 +381,7 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
                         fmaf(ok1 ? __ldg(p.w + i1) : 0.f, fabsf(dq.y), hsum));
           else hsum += fabsf(dq.x) + fabsf(dq.y);
         }
+        d[q] = dq;   // from here on d holds the solve's gradient (+d)
       }
     }
     qs = group_sum<G>(qs);
@@ -366,15 +390,14 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
     float phiv;
     if (spec == 1) phiv = qs + gam;
     else phiv = qs - tt * (HK == HK_L2 ? sqrtf(hsum) : hsum) + gam;
-    int status = (spec == 1) ? 0 : (conv ? kdone : -p.max_iter);
-    if (spec == 2) { phiv = __int_as_float(0x7fc00000); status = INT32_MIN; }
+    if (spec == 2) phiv = __int_as_float(0x7fc00000);
 
     bool point_done = done;
     if (UNION) {
       if (done) {
         if (p.phik && gl == 0) p.phik[pt * p.K + kset] = phiv;
         if (phiv < best) {   // strict: lowest k wins ties (R19); NaN never wins
-          best = phiv; bestk = kset; bestit = status;
+          best = phiv; bestk = kset; bestit = wstatus;
 #pragma unroll
           for (int q = 0; q < NP; q++) bd[q] = d[q];
         }
@@ -412,7 +435,7 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
         }
       }
     } else if (done) {
-      if (gl == 0) { p.phi[pt] = phiv; p.iters[pt] = status; }
+      if (gl == 0) { p.phi[pt] = phiv; p.iters[pt] = wstatus; }
       float *grow = p.grad + pt * (int64_t)n;
 #pragma unroll
       for (int j = 0; j < CPL; j++) {
@@ -435,7 +458,7 @@ __global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
 #pragma unroll
         for (int q = 0; q < NP; q++) xh[q] = d[q] = b[q] = v[q] = splat2(0.f);
         spec = 0;
-        kdone = 0;
+        waiting = false;
       }
     }
   }

@@ -18,6 +18,7 @@ namespace hopf {
 
 thread_local std::string g_last_error;
 thread_local int32_t g_launches = 0;
+thread_local int32_t g_last_threads = 0, g_last_blocks = 0;
 
 int set_error(int code, const char *fmt, ...) {
   char buf[512];
@@ -95,6 +96,10 @@ static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
   static thread_local KernFn cached_fn = nullptr;
   static thread_local Occ cached{256, 1};
   if (cached_fn != fn) {
+    // kappa lives in static shared memory: ask for the full carveout so that several small
+    // blocks fit per SM (the default carveout only fits one block's 4 KB + reserved 1 KB)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     Occ bestc{256, 0};
     for (int th : {256, 128, 64, 32}) {
       if (th < v->G) continue;
@@ -114,6 +119,8 @@ static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
   if (blocks < 1) blocks = 1;
   fn<<<(unsigned)blocks, threads, 0, stream>>>(p);
   g_launches += 1;
+  g_last_threads = threads;
+  g_last_blocks = (int)blocks;
   return check_launch("hopf_diag_kernel");
 }
 
@@ -173,6 +180,12 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
 }
 
 int32_t hopf_last_launch_count(void) { return g_launches; }
+
+int32_t hopf_last_launch_config(int32_t *threads_per_block, int32_t *blocks) {
+  if (threads_per_block) *threads_per_block = g_last_threads;
+  if (blocks) *blocks = g_last_blocks;
+  return g_launches;
+}
 
 const char *hopf_last_error(void) { return g_last_error.c_str(); }
 
