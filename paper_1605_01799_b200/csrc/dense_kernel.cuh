@@ -22,6 +22,9 @@ struct DenseParams {
   float tol;
   float *phi, *grad;
   int *iters;
+  // optional index list (fix-up pass): process points idx[0 .. *idx_count) only
+  const int *idx = nullptr;
+  const int *idx_count = nullptr;
 };
 
 struct DensePlanDev {
@@ -29,6 +32,12 @@ struct DensePlanDev {
   float *Ml = nullptr;    // [n*n] fp32 M_lambda
   float *Ainv = nullptr;  // [n*n] fp32 A^{-1}
   float *A = nullptr;     // [n*n] fp32 A
+  // tensor-core operands (n == 256): fp16 hi/lo blocks of 2^s M_lambda in smem order
+  void *tc_blocks = nullptr;
+  float tc_scale_inv = 0.f;
+  // fix-up list workspace [count, idx...] (grown on demand)
+  int *fix = nullptr;
+  int64_t fix_cap = 0;
 };
 
 bool dense_supported_n(int n);
@@ -36,6 +45,9 @@ const char *dense_supported_list();
 int dense_plan_upload(int n, const double *Ml, const double *Ainv, const double *A,
                       DensePlanDev *out);
 void dense_plan_free(DensePlanDev *d);
-int dense_launch(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream_t stream);
+int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t stream);
+int dense_tc_prepare(int n, const double *Ml, void **blocks_dev, float *mscale_inv);
+int dense_tc_launch(const DenseParams &p, int hk, const void *blocks, float mscale_inv,
+                    int *fix_count, int *fix_list, cudaStream_t stream);
 
 }  // namespace hopf

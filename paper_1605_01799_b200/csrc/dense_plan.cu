@@ -98,5 +98,6 @@ extern "C" int hopf_eval_dense(int64_t M, int32_t n, const float *X, const float
   DenseParams p{};
   p.M = M; p.n = n; p.X = X; p.t = t; p.w = w; p.gamma = gamma; p.lambda = lambda;
   p.max_iter = max_iter; p.tol = tol; p.phi = phi; p.grad = grad; p.iters = iters;
-  return dense_launch(p, (int)h, plan->dev, (cudaStream_t)stream);
+  // the fix-up workspace is per-plan scratch (calls on one plan must share a stream)
+  return dense_launch(p, (int)h, const_cast<hopf_dense_plan *>(plan)->dev, (cudaStream_t)stream);
 }

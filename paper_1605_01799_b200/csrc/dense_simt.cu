@@ -25,6 +25,10 @@ int dense_plan_upload(int n, const double *Ml, const double *Ainv, const double 
   }
   for (size_t i = 0; i < nn; i++) a[i] = (float)Amat[i];
   out->n = n;
+  if (n == 256) {   // tensor-core operands for the tcgen05 kernel
+    const int rc = dense_tc_prepare(n, Ml, &out->tc_blocks, &out->tc_scale_inv);
+    if (rc != HOPF_OK) return rc;
+  }
   if (cudaMalloc(&out->Ml, nn * 4) != cudaSuccess || cudaMalloc(&out->Ainv, nn * 4) != cudaSuccess ||
       cudaMalloc(&out->A, nn * 4) != cudaSuccess) {
     dense_plan_free(out);
@@ -45,7 +49,12 @@ void dense_plan_free(DensePlanDev *d) {
   if (d->Ml) cudaFree(d->Ml);
   if (d->Ainv) cudaFree(d->Ainv);
   if (d->A) cudaFree(d->A);
+  if (d->tc_blocks) cudaFree(d->tc_blocks);
+  if (d->fix) cudaFree(d->fix);
   d->Ml = d->Ainv = d->A = nullptr;
+  d->tc_blocks = nullptr;
+  d->fix = nullptr;
+  d->fix_cap = 0;
 }
 
 namespace {
@@ -77,7 +86,7 @@ __global__ void __launch_bounds__(NT, 1)
   const int64_t stride = (int64_t)gridDim.x * TP;
 
   // per-row bookkeeping, owned by the row's warp (lane-replicated)
-  int64_t pt[4];
+  int64_t pt[4], pos[4];
   int it[4], spec[4];
   float tt[4];
   bool have[4];
@@ -113,10 +122,20 @@ __global__ void __launch_bounds__(NT, 1)
     it[r] = 0;
   };
 
+  const int64_t nlist = p.idx ? (int64_t)*p.idx_count : 0;
+  auto position = [&](int r) {   // global point of list position pos[r]
+    if (p.idx) {
+      have[r] = pos[r] < nlist;
+      pt[r] = have[r] ? (int64_t)p.idx[pos[r]] : 0;
+    } else {
+      pt[r] = pos[r];
+      have[r] = pt[r] < p.M;
+    }
+  };
 #pragma unroll
   for (int r = 0; r < 4; r++) {
-    pt[r] = (int64_t)blockIdx.x * TP + warp * 4 + r;
-    have[r] = pt[r] < p.M;
+    pos[r] = (int64_t)blockIdx.x * TP + warp * 4 + r;
+    position(r);
     load_row(r);
   }
   __syncthreads();
@@ -249,8 +268,8 @@ __global__ void __launch_bounds__(NT, 1)
           p.iters[pt[r]] = st;
         }
         __syncwarp();
-        pt[r] += stride;
-        have[r] = pt[r] < p.M;
+        pos[r] += stride;
+        position(r);
         load_row(r);
       }
     }
@@ -260,6 +279,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 template <int NW>
 int launch_nw(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream_t stream) {
+  // list mode: the count is on the device, so the grid is the resident maximum
   const size_t smem = (size_t)(5 * TP + KC) * NW * 32 * sizeof(float);
   void (*fn)(const DenseParams, const float *, const float *, const float *) =
       hk == HK_L1 ? hopf_dense_simt_kernel<NW, HK_L1>
@@ -270,14 +290,14 @@ int launch_nw(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)num_sms() * per_sm;
   const int64_t need = (p.M + TP - 1) / TP;
-  if (blocks > need) blocks = need;
+  if (!p.idx && blocks > need) blocks = need;
   fn<<<(unsigned)blocks, NT, smem, stream>>>(p, plan.Ml, plan.Ainv, plan.A);
   g_launches += 1;
   return check_launch("hopf_dense_simt_kernel");
 }
 }  // namespace
 
-int dense_launch(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream_t stream) {
+static int launch_simt(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream_t stream) {
   switch (p.n / 32) {
     case 1: return launch_nw<1>(p, hk, plan, stream);
     case 2: return launch_nw<2>(p, hk, plan, stream);
@@ -289,6 +309,28 @@ int dense_launch(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStr
     case 8: return launch_nw<8>(p, hk, plan, stream);
   }
   return set_error(HOPF_EUNSUPPORTED, "dense n=%d", p.n);
+}
+
+// n == 256 and H in {l1, wl1}: tcgen05 kernel, then the exact SIMT kernel on its fix-up list
+// (t == 0, invalid points, fp16 overflow, no convergence within max_iter).  Otherwise SIMT.
+int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t stream) {
+  const bool use_tc = plan.tc_blocks && p.n == 256 && hk != HK_L2 && p.M <= 0x7fffffffLL;
+  if (!use_tc) return launch_simt(p, hk, plan, stream);
+  if (plan.fix_cap < p.M + 1) {
+    if (plan.fix) cudaFree(plan.fix);
+    plan.fix = nullptr;
+    plan.fix_cap = 0;
+    if (cudaMalloc(&plan.fix, sizeof(int) * (size_t)(p.M + 1)) != cudaSuccess)
+      return set_error(HOPF_ECUDA, "cudaMalloc of the fix-up list failed");
+    plan.fix_cap = p.M + 1;
+  }
+  cudaMemsetAsync(plan.fix, 0, sizeof(int), stream);
+  int rc = dense_tc_launch(p, hk, plan.tc_blocks, plan.tc_scale_inv, plan.fix, plan.fix + 1, stream);
+  if (rc != HOPF_OK) return rc;
+  DenseParams q = p;
+  q.idx = plan.fix + 1;
+  q.idx_count = plan.fix;
+  return launch_simt(q, hk, plan, stream);
 }
 
 }  // namespace hopf

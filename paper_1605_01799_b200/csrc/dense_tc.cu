@@ -1,0 +1,450 @@
+// dense_tc.cu — tensor-core dense v-update (K3, v2): tcgen05.mma (kind::f16, TMEM accumulator)
+// for n = 256 and H in {l1, wl1}, fused with the shrink / Bregman / stopping-test epilogue.
+//
+// Paper: (3.4a) for J = 1/2<x,Ax> is the quadratic prox v = M_lambda (x + lambda (d - b)),
+// M_lambda = (A^{-1} + lambda I)^{-1}; (3.4b) shrink_1
+// (P:239-247); (3.4c); stopping rule P:1595-1601.
+//
+// Layout (one CTA per SM, 32 points per CTA, 8 warps; MMA and epilogue alternate, thread 0
+// issues the 96 MMAs of an iteration after the epilogue barrier):
+//  * D^T = M_lambda U^T: the MMA M dimension is the coordinate (two M = 128 halves), N = the 32
+//    points of the CTA, K = 256.  The fp32 accumulators D0 (coordinates 0-127) and D1
+//    (128-255) live in TMEM columns [0,32) and [32,64).
+//  * M_lambda stays resident in shared memory for the whole kernel: it is symmetric, so only the
+//    blocks A11, A12, A22 are stored (A21 = A12^T is the same bytes read through an MN-major
+//    descriptor), each as fp16 hi + lo of 2^s M_lambda (s fixed by the plan): 6 x 32 KB.
+//  * U^T (32 points x 256) is the B operand, fp16 hi + lo, MN-major (points contiguous), 32 KB,
+//    rewritten by the epilogue every iteration.
+//  * 3 MMAs per K-step (Mh Uh + Mh Ul + Ml Uh) reproduce the fp32 product to ~2^-22 relative
+//    (plain fp16/TF32 products stall the paper's 1e-8 test in a limit cycle).
+//  * Epilogue thread (warp w, lane l): coordinates c = 32 (w % 4) + l and c + 128 (a float2),
+//    for the 16 points of half w / 4.  x, u (pre-shrink), v_prev of those 16 points stay in
+//    registers; per-point sums (three test sums and the phi partial) are reduced with a
+//    transposed butterfly per warp and across the 4 warps of the half through shared memory.
+//  * phi at convergence uses g = A^{-1} v^k = U^k - lambda v^k (exact consequence of (3.4a)):
+//      1/2<d, A^{-1} d> = <g, d - v/2> + 1/2<d - v, A^{-1}(d - v)>,
+//    the last term <= lambda_max(A^{-1}) tol / 2 is dropped (reading R23).
+//  * Points with t == 0, non-finite sums (invalid input, fp16 overflow) or no convergence within
+//    max_iter are appended to a fix-up list that the exact FP32 SIMT kernel re-solves.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/hopf.h"
+#include "common.cuh"
+#include "dense_kernel.cuh"
+#include "diag_kernel.cuh"  // HK_* constants
+
+namespace hopf {
+namespace tc {
+
+constexpr int N_DIM = 256;
+constexpr int NT = 32;                       // points per CTA
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = EPI_WARPS * 32;
+constexpr int BLK_BYTES = 128 * 128 * 2;     // one fp16 128x128 block
+constexpr int SM_MLAM = 6 * BLK_BYTES;       // A11h, A12h, A22h, A11l, A12l, A22l
+constexpr int SM_U = NT * N_DIM * 2;         // one of U hi / U lo
+constexpr int OFF_UH = SM_MLAM;
+constexpr int OFF_UL = SM_MLAM + SM_U;
+constexpr int OFF_RED = OFF_UL + SM_U;       // [2 halves][4 warps][16 points][4 q] floats
+constexpr int RED_BYTES = 2 * 4 * 16 * 4 * 4;
+constexpr int OFF_CTRL = OFF_RED + RED_BYTES;
+struct Ctrl {
+  long long pt;   // global point index or -1
+  float t;
+  int it;         // iterations completed
+  int first;      // 1: the next epilogue is iteration 1 (b_old = 0, d_old = x)
+  int done;       // set by the finaliser: 1 converged, 2 sent to fix-up
+  int pad[2];
+};
+constexpr int OFF_MISC = OFF_CTRL + NT * (int)sizeof(Ctrl);
+constexpr int SMEM_BYTES = OFF_MISC + 64;
+
+// element (m, k) of a 128x128 K-major no-swizzle block (core matrix 8 rows x 16 bytes)
+__host__ __device__ inline uint32_t a_off(int m, int k) {
+  return (m >> 3) * 2048 + (k >> 3) * 128 + (m & 7) * 16 + (k & 7) * 2;
+}
+// element (point p, coordinate c) of U^T, MN-major no swizzle: 8 points contiguous (16 bytes)
+__device__ inline uint32_t u_off(int p, int c) {
+  return (c >> 3) * 512 + (p >> 3) * 128 + (c & 7) * 16 + (p & 7) * 2;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // descriptor version (sm_100)
+  return d;                 // base offset 0, lbo mode 0, SWIZZLE_NONE
+}
+__device__ __forceinline__ uint32_t make_idesc(int a_mn_major) {
+  uint32_t d = 0;
+  d |= 1u << 4;                      // accumulate in F32
+  d |= (uint32_t)a_mn_major << 15;   // A major (0 K, 1 MN); A, B formats F16 (0)
+  d |= 1u << 16;                     // B (U^T) is MN-major
+  d |= (uint32_t)(NT >> 3) << 17;    // N
+  d |= (uint32_t)(128 >> 4) << 24;   // M
+  return d;
+}
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}"
+               :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 "selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(smem_u32(bar)), "r"(phase));
+  }
+}
+// 8 consecutive TMEM columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; i++) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ float clampf(float u, float t) { return fminf(fmaxf(u, -t), t); }
+
+// split x into fp16 hi + lo (x ~ hi + lo to ~2^-22 relative)
+__device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(x - __half2float(hi));
+}
+
+template <int HK>
+__global__ void __launch_bounds__(THREADS, 1)
+    hopf_dense_tc_kernel(const DenseParams p, const uint4 *__restrict__ mlam_blocks,
+                         float mscale_inv, int *__restrict__ fix_count,
+                         int *__restrict__ fix_list) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  Ctrl *ctrl = reinterpret_cast<Ctrl *>(smem + OFF_CTRL);
+  float *red = reinterpret_cast<float *>(smem + OFF_RED);
+  uint64_t *mma_done = reinterpret_cast<uint64_t *>(smem + OFF_MISC);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mma_done + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const float lam = p.lambda, tol = p.tol;
+  const int64_t stride = (int64_t)gridDim.x * NT;
+
+  // ---- one-time setup: M_lambda blocks -> smem, barrier, TMEM ------------------------------
+  for (int e = tid; e < SM_MLAM / 16; e += THREADS)
+    reinterpret_cast<uint4 *>(smem)[e] = __ldg(mlam_blocks + e);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(smem_u32(tmem_slot)), "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (lane == 0) {
+      mbar_init(mma_done, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sm0 = smem_u32(smem);
+
+  // ---- the 96 MMAs of one iteration (thread 0) -------------------------------------------
+  auto issue_mmas = [&]() {
+    const uint32_t id_k = make_idesc(0), id_mn = make_idesc(1);
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+      const uint32_t dt = tmem + (uint32_t)(h * 32);   // column offset
+#pragma unroll 1
+      for (int ks = 0; ks < 16; ks++) {
+        // A block and descriptor for coordinates [128h, 128h+128) x K [16ks, 16ks+16)
+        uint64_t ah, al;
+        uint32_t idesc;
+        if (h == 0 && ks < 8) {          // A11, K-major
+          ah = make_sdesc(sm0 + 0 * BLK_BYTES + ks * 256, 128, 2048);
+          al = make_sdesc(sm0 + 3 * BLK_BYTES + ks * 256, 128, 2048);
+          idesc = id_k;
+        } else if (h == 0) {             // A12, K-major
+          ah = make_sdesc(sm0 + 1 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
+          al = make_sdesc(sm0 + 4 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
+          idesc = id_k;
+        } else if (ks < 8) {             // A21 = A12^T: A12 bytes read MN-major
+          ah = make_sdesc(sm0 + 1 * BLK_BYTES + ks * 2 * 2048, 2048, 128);
+          al = make_sdesc(sm0 + 4 * BLK_BYTES + ks * 2 * 2048, 2048, 128);
+          idesc = id_mn;
+        } else {                         // A22, K-major
+          ah = make_sdesc(sm0 + 2 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
+          al = make_sdesc(sm0 + 5 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
+          idesc = id_k;
+        }
+        const uint64_t uh = make_sdesc(sm0 + OFF_UH + ks * 2 * 512, 512, 128);
+        const uint64_t ul = make_sdesc(sm0 + OFF_UL + ks * 2 * 512, 512, 128);
+        mma_f16(dt, ah, uh, idesc, ks > 0 ? 1u : 0u);   // Mh Uh
+        mma_f16(dt, ah, ul, idesc, 1u);                 // Mh Ul
+        mma_f16(dt, al, uh, idesc, 1u);                 // Ml Uh
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(mma_done)));
+  };
+
+  const int half = warp >> 2;                 // points [16 half, 16 half + 16)
+  const int wq = warp & 3;                    // TMEM lane quarter
+  const int c0 = 32 * wq + lane, c1 = c0 + 128;   // this thread's two coordinates
+  const uint32_t t_lane = tmem + ((uint32_t)(32 * wq) << 16);
+  float w0 = 1.f, w1 = 1.f;
+  if (HK == HK_WL1) { w0 = __ldg(p.w + c0); w1 = __ldg(p.w + c1); }
+  float2 xs[16], us[16], vs[16];   // per point (c0, c1): x, u (pre-shrink), v_prev
+
+  // ---- load the point of a (re)admitted slot (p16 = 0..15 within this half) ---------------
+  auto load_slot = [&](int p16) {
+    const int slot = 16 * half + p16;
+    const long long pt = ctrl[slot].pt;
+    float2 x = make_float2(0.f, 0.f);
+    if (pt >= 0) {
+      const float *xr = p.X + pt * (int64_t)N_DIM;
+      x = make_float2(__ldg(xr + c0), __ldg(xr + c1));
+    }
+    xs[p16] = x;
+    us[p16] = make_float2(0.f, 0.f);
+    vs[p16] = x;                                   // v^0 = x
+    // U^1 = x + lambda (d^0 - b^0) = (1 + lambda) x
+    const float U0 = fmaf(lam, x.x, x.x), U1 = fmaf(lam, x.y, x.y);
+    __half h0, l0, h1, l1;
+    split_h(U0, h0, l0);
+    split_h(U1, h1, l1);
+    *reinterpret_cast<__half *>(smem + OFF_UH + u_off(slot, c0)) = h0;
+    *reinterpret_cast<__half *>(smem + OFF_UL + u_off(slot, c0)) = l0;
+    *reinterpret_cast<__half *>(smem + OFF_UH + u_off(slot, c1)) = h1;
+    *reinterpret_cast<__half *>(smem + OFF_UL + u_off(slot, c1)) = l1;
+  };
+
+  // slot admission (one thread per slot): t == 0 / invalid-t points go to the fix-up list
+  auto admit = [&](int slot, long long pt) {
+    while (pt >= 0 && pt < p.M) {
+      const float tv = __ldg(p.t + pt);
+      if (tv > 0.f && tv <= 3.402823466e38f) break;
+      fix_list[atomicAdd(fix_count, 1)] = (int)pt;
+      pt += stride;
+    }
+    if (pt >= p.M) pt = -1;
+    Ctrl c{};
+    c.pt = pt;
+    c.t = pt >= 0 ? __ldg(p.t + pt) : 0.f;
+    c.it = 0; c.first = 1; c.done = 0;
+    ctrl[slot] = c;
+  };
+
+  if (tid < NT) admit(tid, (long long)blockIdx.x * NT + tid);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 16; q++) load_slot(q);
+  asm volatile("fence.proxy.async.shared::cta;");
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    issue_mmas();
+  }
+
+  uint32_t phase = 0;
+  while (true) {
+    mbar_wait(mma_done, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---- elementwise update for 16 points in two chunks of 8 ------------------------------
+#pragma unroll
+    for (int ch = 0; ch < 2; ch++) {
+      float va[8], vb[8];
+      tmem_ld8(t_lane + (uint32_t)(16 * half + 8 * ch), va);        // D0: coordinate c0
+      tmem_ld8(t_lane + (uint32_t)(32 + 16 * half + 8 * ch), vb);   // D1: coordinate c1
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      float qv[32];   // [point j][quantity]: sd, sb, sv, phi partial
+      uint32_t ph0[4], pl0[4], ph1[4], pl1[4];   // packed fp16 U^{k+1} for the 8 points
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int p16 = 8 * ch + j, slot = 16 * half + p16;
+        const float tt = ctrl[slot].t;
+        const int first = ctrl[slot].first;
+        const float ta = tt * w0 / lam, tb = tt * w1 / lam;
+        const float v0 = va[j] * mscale_inv, v1 = vb[j] * mscale_inv;
+        const float2 x = xs[p16], u = us[p16], vp = vs[p16];
+        // previous d, b (from u, or the initial d^0 = x, b^0 = 0)
+        const float bo0 = first ? 0.f : clampf(u.x, ta), bo1 = first ? 0.f : clampf(u.y, tb);
+        const float do0 = first ? x.x : u.x - bo0, do1 = first ? x.y : u.y - bo1;
+        const float un0 = v0 + bo0, un1 = v1 + bo1;                 // argument of (3.4b)
+        const float bn0 = clampf(un0, ta), bn1 = clampf(un1, tb);   // b^k
+        const float dn0 = un0 - bn0, dn1 = un1 - bn1;               // d^k = shrink_1
+        const float e0 = dn0 - do0, e1 = dn1 - do1;                 // d^k - d^{k-1}
+        const float f0 = dn0 - v0, f1 = dn1 - v1;                   // d^k - v^k
+        const float g0 = v0 - vp.x, g1 = v1 - vp.y;                 // v^k - v^{k-1}
+        // phi partial: <x,d> - <A^{-1} v, d - v/2> - t w |d|, A^{-1} v = U^k - lambda v
+        const float Uk0 = fmaf(lam, do0 - bo0, x.x), Uk1 = fmaf(lam, do1 - bo1, x.y);
+        const float gi0 = fmaf(-lam, v0, Uk0), gi1 = fmaf(-lam, v1, Uk1);
+        float ph = x.x * dn0 + x.y * dn1;
+        ph = fmaf(-gi0, fmaf(-0.5f, v0, dn0), ph);
+        ph = fmaf(-gi1, fmaf(-0.5f, v1, dn1), ph);
+        ph = fmaf(-tt, w0 * fabsf(dn0) + w1 * fabsf(dn1), ph);
+        qv[4 * j + 0] = fmaf(e0, e0, e1 * e1);
+        qv[4 * j + 1] = fmaf(f0, f0, f1 * f1);
+        qv[4 * j + 2] = fmaf(g0, g0, g1 * g1);
+        qv[4 * j + 3] = ph;
+        us[p16] = make_float2(un0, un1);
+        vs[p16] = make_float2(v0, v1);
+        // next operand U^{k+1} = x + lambda (d^k - b^k), split into fp16 hi + lo
+        const float Un0 = fmaf(lam, dn0 - bn0, x.x), Un1 = fmaf(lam, dn1 - bn1, x.y);
+        __half h0, l0, h1, l1;
+        split_h(Un0, h0, l0);
+        split_h(Un1, h1, l1);
+        const uint32_t sh = (j & 1) * 16;
+        if ((j & 1) == 0) { ph0[j >> 1] = 0u; pl0[j >> 1] = 0u; ph1[j >> 1] = 0u; pl1[j >> 1] = 0u; }
+        ph0[j >> 1] |= (uint32_t)__half_as_ushort(h0) << sh;
+        pl0[j >> 1] |= (uint32_t)__half_as_ushort(l0) << sh;
+        ph1[j >> 1] |= (uint32_t)__half_as_ushort(h1) << sh;
+        pl1[j >> 1] |= (uint32_t)__half_as_ushort(l1) << sh;
+      }
+      // 8 points are contiguous in the MN-major U^T layout: one 16-byte store per (c, hi/lo)
+      {
+        const int pg = 16 * half + 8 * ch;
+        *reinterpret_cast<uint4 *>(smem + OFF_UH + u_off(pg, c0)) = make_uint4(ph0[0], ph0[1], ph0[2], ph0[3]);
+        *reinterpret_cast<uint4 *>(smem + OFF_UL + u_off(pg, c0)) = make_uint4(pl0[0], pl0[1], pl0[2], pl0[3]);
+        *reinterpret_cast<uint4 *>(smem + OFF_UH + u_off(pg, c1)) = make_uint4(ph1[0], ph1[1], ph1[2], ph1[3]);
+        *reinterpret_cast<uint4 *>(smem + OFF_UL + u_off(pg, c1)) = make_uint4(pl1[0], pl1[1], pl1[2], pl1[3]);
+      }
+      // transposed butterfly: afterwards lane l holds the warp total of qv index l = 4 j + q
+#pragma unroll
+      for (int lev = 16; lev >= 1; lev >>= 1) {
+        const bool up = lane & lev;
+#pragma unroll
+        for (int i = 0; i < lev; i++) {
+          const float send = up ? qv[i] : qv[i + lev];
+          const float keep = up ? qv[i + lev] : qv[i];
+          qv[i] = keep + __shfl_xor_sync(0xffffffffu, send, lev);
+        }
+      }
+      red[((half * 4 + wq) * 16 + (8 * ch + (lane >> 2))) * 4 + (lane & 3)] = qv[0];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    // ---- finaliser: one thread per point slot -------------------------------------------
+    if (tid < NT) {
+      const int slot = tid, hf = slot >> 4, p16 = slot & 15;
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int w4 = 0; w4 < 4; w4++)
+#pragma unroll
+        for (int qq = 0; qq < 4; qq++) s4[qq] += red[((hf * 4 + w4) * 16 + p16) * 4 + qq];
+      Ctrl c = ctrl[slot];
+      c.done = 0;
+      if (c.pt >= 0) {
+        c.it += 1;
+        c.first = 0;
+        const bool finite = fabsf(s4[0] + s4[1] + s4[2] + s4[3]) <= 3.402823466e38f;
+        const bool conv = finite && s4[0] <= tol && s4[1] <= tol && s4[2] <= tol;
+        if (conv) {
+          p.phi[c.pt] = s4[3] + p.gamma;
+          p.iters[c.pt] = c.it;
+          c.done = 1;
+        } else if (!finite || c.it >= p.max_iter) {
+          fix_list[atomicAdd(fix_count, 1)] = (int)c.pt;   // exact FP32 re-solve
+          c.done = 2;
+        }
+      }
+      ctrl[slot] = c;
+    }
+    __syncthreads();
+    // ---- outputs of converged slots: grad := d^k = u - clamp(u) --------------------------
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int slot = 16 * half + q;
+      if (ctrl[slot].done == 1) {
+        const float tt = ctrl[slot].t;
+        const float ta = tt * w0 / lam, tb = tt * w1 / lam;
+        float *g = p.grad + ctrl[slot].pt * (int64_t)N_DIM;
+        g[c0] = us[q].x - clampf(us[q].x, ta);
+        g[c1] = us[q].y - clampf(us[q].y, tb);
+      }
+    }
+    __syncthreads();
+    if (tid < NT && ctrl[tid].done) admit(tid, ctrl[tid].pt + stride);
+    __syncthreads();
+    int busy = 0;
+#pragma unroll
+    for (int q = 0; q < 16; q++)
+      if (ctrl[16 * half + q].first && ctrl[16 * half + q].it == 0 && ctrl[16 * half + q].pt >= 0) load_slot(q);
+#pragma unroll 1
+    for (int s = 0; s < NT; s++) busy |= (ctrl[s].pt >= 0);
+    if (!busy) break;
+    asm volatile("fence.proxy.async.shared::cta;");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      issue_mmas();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(64));
+}
+
+}  // namespace tc
+
+// host side -----------------------------------------------------------------------------------
+// M_lambda blocks in smem order: fp16 hi/lo of 2^s M (A11, A12, A22), K-major no-swizzle.
+int dense_tc_prepare(int n, const double *Ml, void **blocks_dev, float *mscale_inv) {
+  if (n != tc::N_DIM) return HOPF_EUNSUPPORTED;
+  double mx = 0.0;
+  for (int i = 0; i < n * n; i++) mx = fmax(mx, fabs(Ml[i]));
+  int s = 0;
+  while (mx * ldexp(1.0, s + 1) < 16384.0 && s < 60) s++;
+  const double sc = ldexp(1.0, s);
+  std::vector<__half> hb(6 * 128 * 128);
+  const int blk_r[3] = {0, 0, 128}, blk_c[3] = {0, 128, 128};
+  for (int b = 0; b < 3; b++)
+    for (int m = 0; m < 128; m++)
+      for (int k = 0; k < 128; k++) {
+        const double v = Ml[(size_t)(blk_r[b] + m) * n + blk_c[b] + k] * sc;
+        const __half hi = __float2half_rn((float)v);
+        const __half lo = __float2half_rn((float)(v - (double)__half2float(hi)));
+        const uint32_t off = tc::a_off(m, k) / 2;
+        hb[(size_t)b * 128 * 128 + off] = hi;
+        hb[(size_t)(b + 3) * 128 * 128 + off] = lo;
+      }
+  if (cudaMalloc(blocks_dev, hb.size() * sizeof(__half)) != cudaSuccess)
+    return set_error(HOPF_ECUDA, "cudaMalloc for tensor-core operands failed");
+  cudaMemcpy(*blocks_dev, hb.data(), hb.size() * sizeof(__half), cudaMemcpyHostToDevice);
+  *mscale_inv = (float)ldexp(1.0, -s);
+  return HOPF_OK;
+}
+
+int dense_tc_launch(const DenseParams &p, int hk, const void *blocks, float mscale_inv,
+                    int *fix_count, int *fix_list, cudaStream_t stream) {
+  auto fn = hk == HK_WL1 ? tc::hopf_dense_tc_kernel<HK_WL1> : tc::hopf_dense_tc_kernel<HK_L1>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[hk == HK_WL1]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    attr_set[hk == HK_WL1] = true;
+  }
+  int64_t blocks_n = num_sms();
+  const int64_t need = (p.M + tc::NT - 1) / tc::NT;
+  if (blocks_n > need) blocks_n = need;
+  if (blocks_n < 1) blocks_n = 1;
+  fn<<<(unsigned)blocks_n, tc::THREADS, tc::SMEM_BYTES, stream>>>(
+      p, reinterpret_cast<const uint4 *>(blocks), mscale_inv, fix_count, fix_list);
+  g_launches += 1;
+  return check_launch("hopf_dense_tc_kernel");
+}
+
+}  // namespace hopf

@@ -205,7 +205,8 @@ def test_dense_c4_subset(hb):
     check(*g, *o)
 
 
-@pytest.mark.parametrize("n,h", [(32, "l2"), (64, "wl1"), (96, "l1"), (160, "l2")])
+@pytest.mark.parametrize("n,h", [(32, "l2"), (64, "wl1"), (96, "l1"), (160, "l2"), (256, "l1"),
+                                 (256, "wl1"), (256, "l2")])
 def test_dense_shapes_and_edges(hb, n, h):
     rng = np.random.default_rng(n)
     Q = inputs.haar_orthogonal(rng, n)
@@ -258,6 +259,22 @@ def test_full_size_c5_sampled(hb):
     idx = np.sort(np.random.default_rng(2).choice(wl.M, 300, replace=False))
     o = oracle.eval_union(X[idx], t[idx], wl.Dk, wl.Ck, wl.gammak, "l2")
     check_union(phi[idx], grad[idx], it[idx], Y[idx], ks[idx], pk[idx], o, t[idx])
+
+
+def test_dense_tensor_core_fixup_paths(hb):
+    """n = 256 runs on tcgen05; t == 0, invalid points, and max_iter exhaustion are re-solved by
+    the exact FP32 kernel through the fix-up list — results must still match the oracle."""
+    wl = inputs.config("c4")
+    X, t = inputs.points(wl, 0, 700)
+    X = X.copy(); t = t.copy()
+    t[5] = 0.0; t[17] = -1.0; X[23, 100] = np.nan; X[31] = 0.0; t[40] = 50.0
+    plan = hb.DensePlan(wl.Q, wl.Lam)
+    for mi in (1000, 20):
+        g = hb.eval_dense(dev(X), dev(t), plan, 0.0, "l1", max_iter=mi)
+        o = oracle.eval_dense(X, t, wl.Q, wl.Lam, 0.0, "l1", max_iter=mi)
+        check(*g, *o)
+        it = g[2].cpu().numpy()
+        assert it[5] == 0 and it[17] == oracle.INVALID and it[23] == oracle.INVALID
 
 
 def test_full_size_c4_sampled(hb):
