@@ -59,10 +59,10 @@ struct Ctrl {
   int it;         // iterations completed
   int first;      // 1: the next epilogue is iteration 1 (b_old = 0, d_old = x)
   int done;       // set by the finaliser: 1 converged, 2 sent to fix-up
-  int pad[2];
 };
 constexpr int OFF_MISC = OFF_CTRL + NT * (int)sizeof(Ctrl);
 constexpr int SMEM_BYTES = OFF_MISC + 64;
+static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB dynamic shared memory of a CTA");
 
 // element (m, k) of a 128x128 K-major no-swizzle block (core matrix 8 rows x 16 bytes)
 __host__ __device__ inline uint32_t a_off(int m, int k) {

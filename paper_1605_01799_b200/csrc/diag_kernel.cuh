@@ -62,10 +62,13 @@ __device__ __forceinline__ float group_sum(float v) {
 template <int G>
 __device__ __forceinline__ bool group_any(bool f) {
   const unsigned bal = __ballot_sync(0xffffffffu, f);
-  if (G == 32) return bal != 0u;
-  const int lane = threadIdx.x & 31;
-  const unsigned gm = ((1u << G) - 1u) << (lane & ~(G - 1));
-  return (bal & gm) != 0u;
+  if constexpr (G == 32) {
+    return bal != 0u;
+  } else {
+    const int lane = threadIdx.x & 31;
+    const unsigned gm = ((1u << G) - 1u) << (lane & ~(G - 1));
+    return (bal & gm) != 0u;
+  }
 }
 
 __device__ __forceinline__ bool finite_f(float x) { return fabsf(x) <= 3.402823466e38f; }
@@ -154,8 +157,11 @@ __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
 // freezes its d (the in-place update is multiplied by live = 0) and waits; the warp runs the
 // finalize/refill branch once at least half of its groups wait (or all of its remaining ones),
 // so that with G < 32 the branch is shared by several groups instead of run once per group.
+// __launch_bounds__(128, 3): at most 168 registers, i.e. 3 warps per SM sub-partition (each
+// SMSP has a 16K-register file); the widest variants otherwise take ~195 registers and only
+// 2 warps per SMSP, which leaves the dependent FP32x2 chains exposed.
 template <int G, int CPL, int HK, bool UNION>
-__global__ void __launch_bounds__(256) hopf_diag_kernel(const DiagParams p) {
+__global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
   constexpr bool KSM = !UNION;            // -kappa in shared memory
   constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
   constexpr int GPW = 32 / G;             // groups per warp

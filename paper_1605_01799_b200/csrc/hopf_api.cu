@@ -94,20 +94,20 @@ static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
   // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
   struct Occ { int threads, per_sm; };
   static thread_local KernFn cached_fn = nullptr;
-  static thread_local Occ cached{256, 1};
+  static thread_local Occ cached{128, 1};
   if (cached_fn != fn) {
     // kappa lives in static shared memory: ask for the full carveout so that several small
     // blocks fit per SM (the default carveout only fits one block's 4 KB + reserved 1 KB)
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    Occ bestc{256, 0};
-    for (int th : {256, 128, 64, 32}) {
+    Occ bestc{128, 0};
+    for (int th : {128, 64, 32}) {   // the kernels are built with __launch_bounds__(128, 3)
       if (th < v->G) continue;
       int per_sm = 0;
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, th, 0) != cudaSuccess) continue;
       if (per_sm * th > bestc.per_sm * bestc.threads) bestc = {th, per_sm};
     }
-    if (bestc.per_sm < 1) bestc = {256, 1};
+    if (bestc.per_sm < 1) bestc = {128, 1};
     cached = bestc;
     cached_fn = fn;
   }
