@@ -104,7 +104,12 @@ int hopf_dense_plan_create(int32_t n, const double *Q_host, const double *Lambda
                            float lambda, hopf_dense_plan **out);
 int hopf_dense_plan_destroy(hopf_dense_plan *plan);
 
-/* Dense evaluation; arguments as hopf_eval_diag, lambda must equal the plan's. */
+/* Dense evaluation; arguments as hopf_eval_diag, lambda must equal the plan's.
+ * n == 256 with H in {l1, wl1} runs the tensor-core kernel (tcgen05, fp16 hi/lo split of
+ * M_lambda and of x + lambda (d - b), fp32 accumulation in TMEM); its points with t == 0,
+ * invalid input or no convergence are re-solved by the FP32 kernel from a device-side list.
+ * Other n (multiples of 32 up to 256) and H = l2 run the FP32 SIMT kernel.  The plan owns that
+ * list: calls that share a plan must be ordered on one stream. */
 int hopf_eval_dense(int64_t M, int32_t n, const float *X, const float *t,
                     const hopf_dense_plan *plan, float gamma, hopf_h_kind h, const float *w,
                     float lambda, int32_t max_iter, float tol, float *phi, float *grad,
