@@ -54,11 +54,11 @@ constexpr int OFF_RED = OFF_UL + SM_U;       // [2 halves][4 warps][16 points][4
 constexpr int RED_BYTES = 2 * 4 * 16 * 4 * 4;
 constexpr int OFF_CTRL = OFF_RED + RED_BYTES;
 struct Ctrl {
-  long long pt;   // global point index or -1
+  long long pt;   // global point index (mode 1, 2)
   float t;
   int it;         // iterations completed
-  int first;      // 1: the next epilogue is iteration 1 (b_old = 0, d_old = x)
-  int done;       // set by the finaliser: 1 converged, 2 sent to fix-up
+  int mode;       // 0 empty, 1 loading (x in flight; U column 0), 2 active
+  int done;       // set by the finaliser this iteration: 1 converged (write grad)
 };
 constexpr int OFF_MISC = OFF_CTRL + NT * (int)sizeof(Ctrl);
 constexpr int SMEM_BYTES = OFF_MISC + 64;
@@ -138,9 +138,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   float *red = reinterpret_cast<float *>(smem + OFF_RED);
   uint64_t *mma_done = reinterpret_cast<uint64_t *>(smem + OFF_MISC);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mma_done + 2);
+  volatile int *busy_flag = reinterpret_cast<volatile int *>(mma_done + 3);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const float lam = p.lambda, tol = p.tol;
+  const float lam = p.lambda, tol = p.tol, ilam = 1.f / p.lambda;
   const int64_t stride = (int64_t)gridDim.x * NT;
 
   // ---- one-time setup: M_lambda blocks -> smem, barrier, TMEM ------------------------------
@@ -162,38 +163,29 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t sm0 = smem_u32(smem);
 
   // ---- the 96 MMAs of one iteration (thread 0) -------------------------------------------
+  // Descriptors are formed once; consecutive K-steps only advance the start-address field
+  // (bits [0,14), 16-byte units), so the issue loop is one add and one UTCHMMA per MMA.
+  const uint32_t id_k = make_idesc(0), id_mn = make_idesc(1);
+  const uint64_t a_seg[4] = {make_sdesc(sm0 + 0 * BLK_BYTES, 128, 2048),    // A11 (h 0, K 0-127)
+                             make_sdesc(sm0 + 1 * BLK_BYTES, 128, 2048),    // A12 (h 0, K 128-255)
+                             make_sdesc(sm0 + 1 * BLK_BYTES, 2048, 128),    // A21 = A12^T, MN-major
+                             make_sdesc(sm0 + 2 * BLK_BYTES, 128, 2048)};   // A22
+  const uint64_t lo_off = (uint64_t)(3 * BLK_BYTES) >> 4;                  // hi -> lo block
+  const uint64_t b_h0 = make_sdesc(sm0 + OFF_UH, 512, 128), b_l0 = make_sdesc(sm0 + OFF_UL, 512, 128);
   auto issue_mmas = [&]() {
-    const uint32_t id_k = make_idesc(0), id_mn = make_idesc(1);
-#pragma unroll 1
-    for (int h = 0; h < 2; h++) {
-      const uint32_t dt = tmem + (uint32_t)(h * 32);   // column offset
-#pragma unroll 1
-      for (int ks = 0; ks < 16; ks++) {
-        // A block and descriptor for coordinates [128h, 128h+128) x K [16ks, 16ks+16)
-        uint64_t ah, al;
-        uint32_t idesc;
-        if (h == 0 && ks < 8) {          // A11, K-major
-          ah = make_sdesc(sm0 + 0 * BLK_BYTES + ks * 256, 128, 2048);
-          al = make_sdesc(sm0 + 3 * BLK_BYTES + ks * 256, 128, 2048);
-          idesc = id_k;
-        } else if (h == 0) {             // A12, K-major
-          ah = make_sdesc(sm0 + 1 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
-          al = make_sdesc(sm0 + 4 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
-          idesc = id_k;
-        } else if (ks < 8) {             // A21 = A12^T: A12 bytes read MN-major
-          ah = make_sdesc(sm0 + 1 * BLK_BYTES + ks * 2 * 2048, 2048, 128);
-          al = make_sdesc(sm0 + 4 * BLK_BYTES + ks * 2 * 2048, 2048, 128);
-          idesc = id_mn;
-        } else {                         // A22, K-major
-          ah = make_sdesc(sm0 + 2 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
-          al = make_sdesc(sm0 + 5 * BLK_BYTES + (ks - 8) * 256, 128, 2048);
-          idesc = id_k;
-        }
-        const uint64_t uh = make_sdesc(sm0 + OFF_UH + ks * 2 * 512, 512, 128);
-        const uint64_t ul = make_sdesc(sm0 + OFF_UL + ks * 2 * 512, 512, 128);
-        mma_f16(dt, ah, uh, idesc, ks > 0 ? 1u : 0u);   // Mh Uh
-        mma_f16(dt, ah, ul, idesc, 1u);                 // Mh Ul
-        mma_f16(dt, al, uh, idesc, 1u);                 // Ml Uh
+#pragma unroll
+    for (int seg = 0; seg < 4; seg++) {
+      const uint32_t dt = tmem + (uint32_t)((seg >> 1) * 32);   // D0 or D1 columns
+      const uint32_t idesc = seg == 2 ? id_mn : id_k;
+      const uint64_t a_step = seg == 2 ? (2 * 2048) >> 4 : 256 >> 4;
+      uint64_t ah = a_seg[seg], al = a_seg[seg] + lo_off;
+      uint64_t bh = b_h0 + (uint64_t)(((seg & 1) * 8 * 1024) >> 4), bl = b_l0 + (uint64_t)(((seg & 1) * 8 * 1024) >> 4);
+#pragma unroll
+      for (int k8 = 0; k8 < 8; k8++) {
+        mma_f16(dt, ah, bh, idesc, ((seg & 1) | k8) ? 1u : 0u);   // Mh Uh
+        mma_f16(dt, ah, bl, idesc, 1u);                            // Mh Ul
+        mma_f16(dt, al, bh, idesc, 1u);                            // Ml Uh
+        ah += a_step; al += a_step; bh += 1024 >> 4; bl += 1024 >> 4;
       }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -208,49 +200,44 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (HK == HK_WL1) { w0 = __ldg(p.w + c0); w1 = __ldg(p.w + c1); }
   float2 xs[16], us[16], vs[16];   // per point (c0, c1): x, u (pre-shrink), v_prev
 
-  // ---- load the point of a (re)admitted slot (p16 = 0..15 within this half) ---------------
-  auto load_slot = [&](int p16) {
-    const int slot = 16 * half + p16;
-    const long long pt = ctrl[slot].pt;
-    float2 x = make_float2(0.f, 0.f);
-    if (pt >= 0) {
-      const float *xr = p.X + pt * (int64_t)N_DIM;
-      x = make_float2(__ldg(xr + c0), __ldg(xr + c1));
-    }
-    xs[p16] = x;
-    us[p16] = make_float2(0.f, 0.f);
-    vs[p16] = x;                                   // v^0 = x
-    // U^1 = x + lambda (d^0 - b^0) = (1 + lambda) x
-    const float U0 = fmaf(lam, x.x, x.x), U1 = fmaf(lam, x.y, x.y);
-    __half h0, l0, h1, l1;
-    split_h(U0, h0, l0);
-    split_h(U1, h1, l1);
-    *reinterpret_cast<__half *>(smem + OFF_UH + u_off(slot, c0)) = h0;
-    *reinterpret_cast<__half *>(smem + OFF_UL + u_off(slot, c0)) = l0;
-    *reinterpret_cast<__half *>(smem + OFF_UH + u_off(slot, c1)) = h1;
-    *reinterpret_cast<__half *>(smem + OFF_UL + u_off(slot, c1)) = l1;
+  // Slot life cycle (one thread of warp 0 per slot owns the control word):
+  //   loading: the finaliser picked the slot's next point; every thread issues its two x loads
+  //            into xs[] and the owner loads t, all in the shadow of the next MMA (the slot's U
+  //            column is 0 for that MMA); the following epilogue initialises the state, writes
+  //            U^1 = (1 + lambda) x and validates t (t <= 0 / non-finite -> fix-up list).
+  //   active:  split Bregman iterations; converged -> grad/phi/iters; max_iter or non-finite
+  //            sums -> fix-up list; either way the slot goes back to loading (or empty).
+  float t_pending = 0.f;   // owner lane: t of the point being loaded
+  auto zero_u = [&](int slot) {
+    const __half z = __float2half_rn(0.f);
+    *reinterpret_cast<__half *>(smem + OFF_UH + u_off(slot, c0)) = z;
+    *reinterpret_cast<__half *>(smem + OFF_UL + u_off(slot, c0)) = z;
+    *reinterpret_cast<__half *>(smem + OFF_UH + u_off(slot, c1)) = z;
+    *reinterpret_cast<__half *>(smem + OFF_UL + u_off(slot, c1)) = z;
+  };
+  auto issue_loads = [&](int p16) {   // x of the slot's new point into registers (no wait)
+    const long long pt = ctrl[16 * half + p16].pt;
+    const float *xr = p.X + pt * (int64_t)N_DIM;
+    xs[p16] = make_float2(__ldg(xr + c0), __ldg(xr + c1));
   };
 
-  // slot admission (one thread per slot): t == 0 / invalid-t points go to the fix-up list
-  auto admit = [&](int slot, long long pt) {
-    while (pt >= 0 && pt < p.M) {
-      const float tv = __ldg(p.t + pt);
-      if (tv > 0.f && tv <= 3.402823466e38f) break;
-      fix_list[atomicAdd(fix_count, 1)] = (int)pt;
-      pt += stride;
-    }
-    if (pt >= p.M) pt = -1;
+  // initial admission: slot s takes point blockIdx.x * NT + s
+  if (tid < NT) {
     Ctrl c{};
-    c.pt = pt;
-    c.t = pt >= 0 ? __ldg(p.t + pt) : 0.f;
-    c.it = 0; c.first = 1; c.done = 0;
-    ctrl[slot] = c;
-  };
-
-  if (tid < NT) admit(tid, (long long)blockIdx.x * NT + tid);
+    c.pt = (long long)blockIdx.x * NT + tid;
+    c.mode = c.pt < p.M ? 1 : 0;
+    c.it = 0; c.t = 0.f; c.done = 0;
+    if (c.mode) t_pending = __ldg(p.t + c.pt);
+    ctrl[tid] = c;
+  }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < 16; q++) load_slot(q);
+  for (int q = 0; q < 16; q++) {
+    zero_u(16 * half + q);
+    xs[q] = make_float2(0.f, 0.f);
+    us[q] = vs[q] = xs[q];
+    if (ctrl[16 * half + q].mode == 1) issue_loads(q);
+  }
   asm volatile("fence.proxy.async.shared::cta;");
   __syncthreads();
   if (tid == 0) {
@@ -275,35 +262,49 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int j = 0; j < 8; j++) {
         const int p16 = 8 * ch + j, slot = 16 * half + p16;
+        const int mode = ctrl[slot].mode;
+        const int first = ctrl[slot].it == 0;
         const float tt = ctrl[slot].t;
-        const int first = ctrl[slot].first;
-        const float ta = tt * w0 / lam, tb = tt * w1 / lam;
+        const float ta = tt * w0 * ilam, tb = tt * w1 * ilam;
         const float v0 = va[j] * mscale_inv, v1 = vb[j] * mscale_inv;
-        const float2 x = xs[p16], u = us[p16], vp = vs[p16];
-        // previous d, b (from u, or the initial d^0 = x, b^0 = 0)
-        const float bo0 = first ? 0.f : clampf(u.x, ta), bo1 = first ? 0.f : clampf(u.y, tb);
-        const float do0 = first ? x.x : u.x - bo0, do1 = first ? x.y : u.y - bo1;
-        const float un0 = v0 + bo0, un1 = v1 + bo1;                 // argument of (3.4b)
-        const float bn0 = clampf(un0, ta), bn1 = clampf(un1, tb);   // b^k
-        const float dn0 = un0 - bn0, dn1 = un1 - bn1;               // d^k = shrink_1
-        const float e0 = dn0 - do0, e1 = dn1 - do1;                 // d^k - d^{k-1}
-        const float f0 = dn0 - v0, f1 = dn1 - v1;                   // d^k - v^k
-        const float g0 = v0 - vp.x, g1 = v1 - vp.y;                 // v^k - v^{k-1}
-        // phi partial: <x,d> - <A^{-1} v, d - v/2> - t w |d|, A^{-1} v = U^k - lambda v
-        const float Uk0 = fmaf(lam, do0 - bo0, x.x), Uk1 = fmaf(lam, do1 - bo1, x.y);
-        const float gi0 = fmaf(-lam, v0, Uk0), gi1 = fmaf(-lam, v1, Uk1);
-        float ph = x.x * dn0 + x.y * dn1;
-        ph = fmaf(-gi0, fmaf(-0.5f, v0, dn0), ph);
-        ph = fmaf(-gi1, fmaf(-0.5f, v1, dn1), ph);
-        ph = fmaf(-tt, w0 * fabsf(dn0) + w1 * fabsf(dn1), ph);
-        qv[4 * j + 0] = fmaf(e0, e0, e1 * e1);
-        qv[4 * j + 1] = fmaf(f0, f0, f1 * f1);
-        qv[4 * j + 2] = fmaf(g0, g0, g1 * g1);
-        qv[4 * j + 3] = ph;
-        us[p16] = make_float2(un0, un1);
-        vs[p16] = make_float2(v0, v1);
-        // next operand U^{k+1} = x + lambda (d^k - b^k), split into fp16 hi + lo
-        const float Un0 = fmaf(lam, dn0 - bn0, x.x), Un1 = fmaf(lam, dn1 - bn1, x.y);
+        float2 x = xs[p16];
+        if (mode != 2) {   // loading (x has landed): v^0 = x; empty: zeros
+          if (mode == 0) x = make_float2(0.f, 0.f);
+          us[p16] = make_float2(0.f, 0.f);
+          vs[p16] = x;
+        }
+        const float2 u = us[p16], vp = vs[p16];
+        float Un0, Un1;
+        if (mode == 2) {
+          // previous d, b (from u, or the initial d^0 = x, b^0 = 0)
+          const float bo0 = first ? 0.f : clampf(u.x, ta), bo1 = first ? 0.f : clampf(u.y, tb);
+          const float do0 = first ? x.x : u.x - bo0, do1 = first ? x.y : u.y - bo1;
+          const float un0 = v0 + bo0, un1 = v1 + bo1;                 // argument of (3.4b)
+          const float bn0 = clampf(un0, ta), bn1 = clampf(un1, tb);   // b^k
+          const float dn0 = un0 - bn0, dn1 = un1 - bn1;               // d^k = shrink_1
+          const float e0 = dn0 - do0, e1 = dn1 - do1;                 // d^k - d^{k-1}
+          const float f0 = dn0 - v0, f1 = dn1 - v1;                   // d^k - v^k
+          const float g0 = v0 - vp.x, g1 = v1 - vp.y;                 // v^k - v^{k-1}
+          // phi partial: <x,d> - <A^{-1} v, d - v/2> - t w |d|, A^{-1} v = U^k - lambda v
+          const float Uk0 = fmaf(lam, do0 - bo0, x.x), Uk1 = fmaf(lam, do1 - bo1, x.y);
+          const float gi0 = fmaf(-lam, v0, Uk0), gi1 = fmaf(-lam, v1, Uk1);
+          float ph = x.x * dn0 + x.y * dn1;
+          ph = fmaf(-gi0, fmaf(-0.5f, v0, dn0), ph);
+          ph = fmaf(-gi1, fmaf(-0.5f, v1, dn1), ph);
+          ph = fmaf(-tt, w0 * fabsf(dn0) + w1 * fabsf(dn1), ph);
+          qv[4 * j + 0] = fmaf(e0, e0, e1 * e1);
+          qv[4 * j + 1] = fmaf(f0, f0, f1 * f1);
+          qv[4 * j + 2] = fmaf(g0, g0, g1 * g1);
+          qv[4 * j + 3] = ph;
+          us[p16] = make_float2(un0, un1);
+          vs[p16] = make_float2(v0, v1);
+          Un0 = fmaf(lam, dn0 - bn0, x.x);   // next operand U^{k+1} = x + lambda (d^k - b^k)
+          Un1 = fmaf(lam, dn1 - bn1, x.y);
+        } else {
+          qv[4 * j + 0] = qv[4 * j + 1] = qv[4 * j + 2] = qv[4 * j + 3] = 0.f;
+          Un0 = fmaf(lam, x.x, x.x);         // U^1 = (1 + lambda) x of a loaded point
+          Un1 = fmaf(lam, x.y, x.y);
+        }
         __half h0, l0, h1, l1;
         split_h(Un0, h0, l0);
         split_h(Un1, h1, l1);
@@ -337,55 +338,69 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    // ---- finaliser: one thread per point slot -------------------------------------------
+    // ---- finaliser: one thread per point slot (warp 0) ------------------------------------
     if (tid < NT) {
       const int slot = tid, hf = slot >> 4, p16 = slot & 15;
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int w4 = 0; w4 < 4; w4++)
-#pragma unroll
-        for (int qq = 0; qq < 4; qq++) s4[qq] += red[((hf * 4 + w4) * 16 + p16) * 4 + qq];
       Ctrl c = ctrl[slot];
       c.done = 0;
-      if (c.pt >= 0) {
+      bool reload = false;
+      if (c.mode == 2) {
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int w4 = 0; w4 < 4; w4++)
+#pragma unroll
+          for (int qq = 0; qq < 4; qq++) s4[qq] += red[((hf * 4 + w4) * 16 + p16) * 4 + qq];
         c.it += 1;
-        c.first = 0;
         const bool finite = fabsf(s4[0] + s4[1] + s4[2] + s4[3]) <= 3.402823466e38f;
         const bool conv = finite && s4[0] <= tol && s4[1] <= tol && s4[2] <= tol;
         if (conv) {
           p.phi[c.pt] = s4[3] + p.gamma;
           p.iters[c.pt] = c.it;
           c.done = 1;
+          reload = true;
         } else if (!finite || c.it >= p.max_iter) {
           fix_list[atomicAdd(fix_count, 1)] = (int)c.pt;   // exact FP32 re-solve
-          c.done = 2;
+          reload = true;
+        }
+      } else if (c.mode == 1) {
+        // the point's x landed in this epilogue (its state and U^1 are set); validate t
+        if (t_pending > 0.f && t_pending <= 3.402823466e38f) {
+          c.t = t_pending; c.it = 0; c.mode = 2;
+        } else {
+          fix_list[atomicAdd(fix_count, 1)] = (int)c.pt;   // t == 0, t < 0, non-finite t
+          reload = true;
         }
       }
+      if (reload) {
+        c.pt += stride;
+        c.mode = c.pt < p.M ? 1 : 0;
+        c.it = 0;
+        if (c.mode) t_pending = __ldg(p.t + c.pt);   // consumed by the next finaliser
+      }
       ctrl[slot] = c;
+      const unsigned act = __ballot_sync(0xffffffffu, c.mode != 0);
+      if (tid == 0) *busy_flag = act != 0u;
     }
     __syncthreads();
-    // ---- outputs of converged slots: grad := d^k = u - clamp(u) --------------------------
+    // ---- converged slots: grad := d^k = u - clamp(u); reloads: x in flight, U column 0 ----
 #pragma unroll
     for (int q = 0; q < 16; q++) {
       const int slot = 16 * half + q;
-      if (ctrl[slot].done == 1) {
-        const float tt = ctrl[slot].t;
-        const float ta = tt * w0 / lam, tb = tt * w1 / lam;
-        float *g = p.grad + ctrl[slot].pt * (int64_t)N_DIM;
+      const Ctrl c = ctrl[slot];
+      if (c.done == 1) {
+        const float ta = c.t * w0 * ilam, tb = c.t * w1 * ilam;
+        float *g = p.grad + (c.pt - stride) * (int64_t)N_DIM;   // the finaliser advanced pt
         g[c0] = us[q].x - clampf(us[q].x, ta);
         g[c1] = us[q].y - clampf(us[q].y, tb);
       }
     }
-    __syncthreads();
-    if (tid < NT && ctrl[tid].done) admit(tid, ctrl[tid].pt + stride);
-    __syncthreads();
-    int busy = 0;
 #pragma unroll
-    for (int q = 0; q < 16; q++)
-      if (ctrl[16 * half + q].first && ctrl[16 * half + q].it == 0 && ctrl[16 * half + q].pt >= 0) load_slot(q);
-#pragma unroll 1
-    for (int s = 0; s < NT; s++) busy |= (ctrl[s].pt >= 0);
-    if (!busy) break;
+    for (int q = 0; q < 16; q++) {
+      const int slot = 16 * half + q;
+      if (ctrl[slot].mode == 1) { zero_u(slot); issue_loads(q); }
+      else if (ctrl[slot].mode == 0) zero_u(slot);
+    }
+    if (!*busy_flag) break;
     asm volatile("fence.proxy.async.shared::cta;");
     __syncthreads();
     if (tid == 0) {
