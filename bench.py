@@ -334,14 +334,22 @@ def main():
             roof["frac_at_measured_clock"] = achieved / (sms * FP32_LANES_PER_SM * 2 *
                                                          clocks["sm_mhz"] * 1e6 / 1e12)
     else:
-        flops = float(np.abs(iters_np).sum()) * 2.0 * n * n
+        # dense: the v-update GEMM dominates: algorithmic 2 n^2 flops per point-iteration; the
+        # tensor-core kernel executes 3 fp16 products (hi/lo split) per algorithmic one
+        it_sum = float(np.abs(iters_np[iters_np != inputs_invalid()]).sum())
+        flops = it_sum * 2.0 * n * n
         achieved = flops / (ms_step / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "unit": "TFLOP/s",
-                "peak": sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12,
-                "traffic": load_traffic(wl.name), "note": "v1 SIMT FP32 dense GEMM; flops = 2 n^2 "
-                "per point-iteration (the v-update GEMM)"}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-
+        tc = (n == 256 and wl.h != "l2")
+        bf16 = float(peaks.get("bf16_tflops", 1645.3))
+        peak = bf16 if tc else sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+        roof = {"bound": "tensor" if tc else "alu", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(wl.name),
+                "peak_basis": ("measured dense bf16 cuBLAS burst (MEASURED_PEAKS.json); fp16 "
+                               "kind::f16 runs at the bf16 rate") if tc else "FP32 SIMT peak",
+                "algorithmic_flops_per_launch": flops,
+                "executed_tensor_flops_per_launch": 3 * flops if tc else None,
+                "executed_frac": 3 * achieved / peak if tc else None,
+                "mean_iters": float(conv.mean()) if conv.size else None}
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         sample = min(args.cpu_sample or CPU_SAMPLE[wl.name], wl.M)
