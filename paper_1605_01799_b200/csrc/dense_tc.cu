@@ -5,7 +5,7 @@
 // M_lambda = (A^{-1} + lambda I)^{-1}; (3.4b) shrink_1
 // (P:239-247); (3.4c); stopping rule P:1595-1601.
 //
-// Layout (one CTA per SM, 32 points per CTA, 8 warps; MMA and epilogue alternate, thread 0
+// Layout (one CTA per SM, 32 points per CTA, 16 warps; MMA and epilogue alternate, thread 0
 // issues the 96 MMAs of an iteration after the epilogue barrier):
 //  * D^T = M_lambda U^T: the MMA M dimension is the coordinate (two M = 128 halves), N = the 32
 //    points of the CTA, K = 256.  The fp32 accumulators D0 (coordinates 0-127) and D1
@@ -17,10 +17,10 @@
 //    rewritten by the epilogue every iteration.
 //  * 3 MMAs per K-step (Mh Uh + Mh Ul + Ml Uh) reproduce the fp32 product to ~2^-22 relative
 //    (plain fp16/TF32 products stall the paper's 1e-8 test in a limit cycle).
-//  * Epilogue thread (warp w, lane l): coordinates c = 32 (w % 4) + l and c + 128 (a float2),
-//    for the 16 points of half w / 4.  x, u (pre-shrink), v_prev of those 16 points stay in
-//    registers; per-point sums (three test sums and the phi partial) are reduced with a
-//    transposed butterfly per warp and across the 4 warps of the half through shared memory.
+//  * Epilogue thread (warp w of 16, lane l): coordinates c = 32 (w % 4) + l and c + 128 (a
+//    float2), for the 8 points of group w / 4.  x, u (pre-shrink), v_prev of those 8 points stay
+//    in registers; per-point sums (three test sums and the phi partial) are reduced with a
+//    transposed butterfly per warp and across the 4 warps of the group through shared memory.
 //  * phi at convergence uses g = A^{-1} v^k = U^k - lambda v^k (exact consequence of (3.4a)):
 //      1/2<d, A^{-1} d> = <g, d - v/2> + 1/2<d - v, A^{-1}(d - v)>,
 //    the last term <= lambda_max(A^{-1}) tol / 2 is dropped (reading R23).
@@ -43,15 +43,18 @@ namespace tc {
 
 constexpr int N_DIM = 256;
 constexpr int NT = 32;                       // points per CTA
-constexpr int EPI_WARPS = 8;
+constexpr int EPI_WARPS = 16;
 constexpr int THREADS = EPI_WARPS * 32;
+constexpr int GROUPS = EPI_WARPS / 4;        // warp groups; group g owns points [PPG g, PPG g + PPG)
+constexpr int PPG = NT / GROUPS;             // points per group (8)
+constexpr int NCH = PPG / 8;                 // chunks of 8 points per thread
 constexpr int BLK_BYTES = 128 * 128 * 2;     // one fp16 128x128 block
 constexpr int SM_MLAM = 6 * BLK_BYTES;       // A11h, A12h, A22h, A11l, A12l, A22l
 constexpr int SM_U = NT * N_DIM * 2;         // one of U hi / U lo
 constexpr int OFF_UH = SM_MLAM;
 constexpr int OFF_UL = SM_MLAM + SM_U;
-constexpr int OFF_RED = OFF_UL + SM_U;       // [2 halves][4 warps][16 points][4 q] floats
-constexpr int RED_BYTES = 2 * 4 * 16 * 4 * 4;
+constexpr int OFF_RED = OFF_UL + SM_U;       // [GROUPS][4 warps][PPG points][4 q] floats
+constexpr int RED_BYTES = GROUPS * 4 * PPG * 4 * 4;
 constexpr int OFF_CTRL = OFF_RED + RED_BYTES;
 struct Ctrl {
   long long pt;   // global point index (mode 1, 2)
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   auto issue_mmas = [&]() {
 #pragma unroll
     for (int seg = 0; seg < 4; seg++) {
-      const uint32_t dt = tmem + (uint32_t)((seg >> 1) * 32);   // D0 or D1 columns
+      const uint32_t dt = tmem + (uint32_t)((seg >> 1) * NT);   // D0 or D1 columns
       const uint32_t idesc = seg == 2 ? id_mn : id_k;
       const uint64_t a_step = seg == 2 ? (2 * 2048) >> 4 : 256 >> 4;
       uint64_t ah = a_seg[seg], al = a_seg[seg] + lo_off;
@@ -192,13 +195,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                  :: "r"(smem_u32(mma_done)));
   };
 
-  const int half = warp >> 2;                 // points [16 half, 16 half + 16)
+  const int half = warp >> 2;                 // group: points [PPG half, PPG half + PPG)
   const int wq = warp & 3;                    // TMEM lane quarter
   const int c0 = 32 * wq + lane, c1 = c0 + 128;   // this thread's two coordinates
   const uint32_t t_lane = tmem + ((uint32_t)(32 * wq) << 16);
   float w0 = 1.f, w1 = 1.f;
   if (HK == HK_WL1) { w0 = __ldg(p.w + c0); w1 = __ldg(p.w + c1); }
-  float2 xs[16], us[16], vs[16];   // per point (c0, c1): x, u (pre-shrink), v_prev
+  float2 xs[PPG], us[PPG], vs[PPG];   // per point (c0, c1): x, u (pre-shrink), v_prev
 
   // Slot life cycle (one thread of warp 0 per slot owns the control word):
   //   loading: the finaliser picked the slot's next point; every thread issues its two x loads
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     *reinterpret_cast<__half *>(smem + OFF_UL + u_off(slot, c1)) = z;
   };
   auto issue_loads = [&](int p16) {   // x of the slot's new point into registers (no wait)
-    const long long pt = ctrl[16 * half + p16].pt;
+    const long long pt = ctrl[PPG * half + p16].pt;
     const float *xr = p.X + pt * (int64_t)N_DIM;
     xs[p16] = make_float2(__ldg(xr + c0), __ldg(xr + c1));
   };
@@ -232,11 +235,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < 16; q++) {
-    zero_u(16 * half + q);
+  for (int q = 0; q < PPG; q++) {
+    zero_u(PPG * half + q);
     xs[q] = make_float2(0.f, 0.f);
     us[q] = vs[q] = xs[q];
-    if (ctrl[16 * half + q].mode == 1) issue_loads(q);
+    if (ctrl[PPG * half + q].mode == 1) issue_loads(q);
   }
   asm volatile("fence.proxy.async.shared::cta;");
   __syncthreads();
@@ -252,16 +255,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     // ---- elementwise update for 16 points in two chunks of 8 ------------------------------
 #pragma unroll
-    for (int ch = 0; ch < 2; ch++) {
+    for (int ch = 0; ch < NCH; ch++) {
       float va[8], vb[8];
-      tmem_ld8(t_lane + (uint32_t)(16 * half + 8 * ch), va);        // D0: coordinate c0
-      tmem_ld8(t_lane + (uint32_t)(32 + 16 * half + 8 * ch), vb);   // D1: coordinate c1
+      tmem_ld8(t_lane + (uint32_t)(PPG * half + 8 * ch), va);        // D0: coordinate c0
+      tmem_ld8(t_lane + (uint32_t)(NT + PPG * half + 8 * ch), vb);   // D1: coordinate c1
       asm volatile("tcgen05.wait::ld.sync.aligned;");
       float qv[32];   // [point j][quantity]: sd, sb, sv, phi partial
       uint32_t ph0[4], pl0[4], ph1[4], pl1[4];   // packed fp16 U^{k+1} for the 8 points
 #pragma unroll
       for (int j = 0; j < 8; j++) {
-        const int p16 = 8 * ch + j, slot = 16 * half + p16;
+        const int p16 = 8 * ch + j, slot = PPG * half + p16;
         const int mode = ctrl[slot].mode;
         const int first = ctrl[slot].it == 0;
         const float tt = ctrl[slot].t;
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       // 8 points are contiguous in the MN-major U^T layout: one 16-byte store per (c, hi/lo)
       {
-        const int pg = 16 * half + 8 * ch;
+        const int pg = PPG * half + 8 * ch;
         *reinterpret_cast<uint4 *>(smem + OFF_UH + u_off(pg, c0)) = make_uint4(ph0[0], ph0[1], ph0[2], ph0[3]);
         *reinterpret_cast<uint4 *>(smem + OFF_UL + u_off(pg, c0)) = make_uint4(pl0[0], pl0[1], pl0[2], pl0[3]);
         *reinterpret_cast<uint4 *>(smem + OFF_UH + u_off(pg, c1)) = make_uint4(ph1[0], ph1[1], ph1[2], ph1[3]);
@@ -334,13 +337,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           qv[i] = keep + __shfl_xor_sync(0xffffffffu, send, lev);
         }
       }
-      red[((half * 4 + wq) * 16 + (8 * ch + (lane >> 2))) * 4 + (lane & 3)] = qv[0];
+      red[((half * 4 + wq) * PPG + (8 * ch + (lane >> 2))) * 4 + (lane & 3)] = qv[0];
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     // ---- finaliser: one thread per point slot (warp 0) ------------------------------------
     if (tid < NT) {
-      const int slot = tid, hf = slot >> 4, p16 = slot & 15;
+      const int slot = tid, hf = slot / PPG, p16 = slot % PPG;
       Ctrl c = ctrl[slot];
       c.done = 0;
       bool reload = false;
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int w4 = 0; w4 < 4; w4++)
 #pragma unroll
-          for (int qq = 0; qq < 4; qq++) s4[qq] += red[((hf * 4 + w4) * 16 + p16) * 4 + qq];
+          for (int qq = 0; qq < 4; qq++) s4[qq] += red[((hf * 4 + w4) * PPG + p16) * 4 + qq];
         c.it += 1;
         const bool finite = fabsf(s4[0] + s4[1] + s4[2] + s4[3]) <= 3.402823466e38f;
         const bool conv = finite && s4[0] <= tol && s4[1] <= tol && s4[2] <= tol;
@@ -384,8 +387,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     // ---- converged slots: grad := d^k = u - clamp(u); reloads: x in flight, U column 0 ----
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
-      const int slot = 16 * half + q;
+    for (int q = 0; q < PPG; q++) {
+      const int slot = PPG * half + q;
       const Ctrl c = ctrl[slot];
       if (c.done == 1) {
         const float ta = c.t * w0 * ilam, tb = c.t * w1 * ilam;
@@ -395,8 +398,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
 #pragma unroll
-    for (int q = 0; q < 16; q++) {
-      const int slot = 16 * half + q;
+    for (int q = 0; q < PPG; q++) {
+      const int slot = PPG * half + q;
       if (ctrl[slot].mode == 1) { zero_u(slot); issue_loads(q); }
       else if (ctrl[slot].mode == 0) zero_u(slot);
     }
