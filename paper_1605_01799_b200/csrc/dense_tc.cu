@@ -57,11 +57,11 @@ constexpr int OFF_RED = OFF_UL + SM_U;       // [GROUPS][4 warps][PPG points][4 
 constexpr int RED_BYTES = GROUPS * 4 * PPG * 4 * 4;
 constexpr int OFF_CTRL = OFF_RED + RED_BYTES;
 struct Ctrl {
-  long long pt;   // global point index (mode 1, 2)
   float t;
   int it;         // iterations completed
   int mode;       // 0 empty, 1 loading (x in flight; U column 0), 2 active
   int done;       // set by the finaliser this iteration: 1 converged (write grad)
+  long long pt;   // global point index (mode 1, 2)
 };
 constexpr int OFF_MISC = OFF_CTRL + NT * (int)sizeof(Ctrl);
 constexpr int SMEM_BYTES = OFF_MISC + 64;
@@ -124,6 +124,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; i++) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ float clampf(float u, float t) { return fminf(fmaxf(u, -t), t); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 clamp2(float2 u, float2 t) {
+  return make_float2(clampf(u.x, t.x), clampf(u.y, t.y));
+}
 
 // split x into fp16 hi + lo (x ~ hi + lo to ~2^-22 relative)
 __device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_wait(mma_done, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;");
-    // ---- elementwise update for 16 points in two chunks of 8 ------------------------------
+    // ---- elementwise update, 8 points per chunk, packed FP32x2 over the coordinate pair ---
 #pragma unroll
     for (int ch = 0; ch < NCH; ch++) {
       float va[8], vb[8];
@@ -262,61 +268,69 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;");
       float qv[32];   // [point j][quantity]: sd, sb, sv, phi partial
       uint32_t ph0[4], pl0[4], ph1[4], pl1[4];   // packed fp16 U^{k+1} for the 8 points
+      const float2 msc = make_float2(mscale_inv, mscale_inv);
+      const float2 lam2 = make_float2(lam, lam), nlam2 = make_float2(-lam, -lam);
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const int p16 = 8 * ch + j, slot = PPG * half + p16;
-        const int mode = ctrl[slot].mode;
-        const int first = ctrl[slot].it == 0;
-        const float tt = ctrl[slot].t;
-        const float ta = tt * w0 * ilam, tb = tt * w1 * ilam;
-        const float v0 = va[j] * mscale_inv, v1 = vb[j] * mscale_inv;
-        float2 x = xs[p16];
-        if (mode != 2) {   // loading (x has landed): v^0 = x; empty: zeros
-          if (mode == 0) x = make_float2(0.f, 0.f);
-          us[p16] = make_float2(0.f, 0.f);
-          vs[p16] = x;
+      for (int jj = 0; jj < 4; jj++) {
+        float2 Unj[2];
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          const int j = 2 * jj + e;
+          const int p16 = 8 * ch + j, slot = PPG * half + p16;
+          const float2 tm = *reinterpret_cast<const float2 *>(&ctrl[slot].t);   // t, it
+          const int2 md = *reinterpret_cast<const int2 *>(&ctrl[slot].mode);    // mode, done
+          const float tt = tm.x;
+          const int mode = md.x, first = __float_as_int(tm.y) == 0;
+          const float2 tau = make_float2(tt * w0 * ilam, tt * w1 * ilam);
+          const float2 v = __fmul2_rn(make_float2(va[j], vb[j]), msc);
+          float2 x = xs[p16];
+          if (mode != 2) {   // loading (x has landed): v^0 = x; empty: zeros
+            if (mode == 0) x = make_float2(0.f, 0.f);
+            us[p16] = make_float2(0.f, 0.f);
+            vs[p16] = x;
+          }
+          const float2 u = us[p16], vp = vs[p16];
+          if (mode == 2) {
+            // previous d, b (from u, or the initial d^0 = x, b^0 = 0)
+            const float2 bo = first ? make_float2(0.f, 0.f) : clamp2(u, tau);
+            const float2 dprev = first ? x : sub2(u, bo);
+            const float2 un = add2(v, bo);                         // argument of (3.4b)
+            const float2 bn = clamp2(un, tau);                     // b^k
+            const float2 dn = sub2(un, bn);                        // d^k = shrink_1
+            const float2 ed = sub2(dn, dprev);                     // d^k - d^{k-1}
+            const float2 fd = sub2(dn, v);                         // d^k - v^k
+            const float2 gd = sub2(v, vp);                         // v^k - v^{k-1}
+            // phi partial: <x,d> - <A^{-1} v, d - v/2> - t w |d|, A^{-1} v = U^k - lambda v
+            const float2 Uk = fma2(lam2, sub2(dprev, bo), x);
+            const float2 gi = fma2(nlam2, v, Uk);
+            const float2 hv = fma2(make_float2(-0.5f, -0.5f), v, dn);
+            float2 q = __fmul2_rn(x, dn);
+            q = sub2(q, __fmul2_rn(gi, hv));
+            float ph = q.x + q.y;
+            ph = fmaf(-tt, fmaf(w0, fabsf(dn.x), w1 * fabsf(dn.y)), ph);
+            const float2 e2 = __fmul2_rn(ed, ed), f2 = __fmul2_rn(fd, fd), g2 = __fmul2_rn(gd, gd);
+            qv[4 * j + 0] = e2.x + e2.y;
+            qv[4 * j + 1] = f2.x + f2.y;
+            qv[4 * j + 2] = g2.x + g2.y;
+            qv[4 * j + 3] = ph;
+            us[p16] = un;
+            vs[p16] = v;
+            Unj[e] = fma2(lam2, sub2(dn, bn), x);   // next operand U^{k+1} = x + lambda (d^k - b^k)
+          } else {
+            qv[4 * j + 0] = qv[4 * j + 1] = qv[4 * j + 2] = qv[4 * j + 3] = 0.f;
+            Unj[e] = fma2(lam2, x, x);              // U^1 = (1 + lambda) x of a loaded point
+          }
         }
-        const float2 u = us[p16], vp = vs[p16];
-        float Un0, Un1;
-        if (mode == 2) {
-          // previous d, b (from u, or the initial d^0 = x, b^0 = 0)
-          const float bo0 = first ? 0.f : clampf(u.x, ta), bo1 = first ? 0.f : clampf(u.y, tb);
-          const float do0 = first ? x.x : u.x - bo0, do1 = first ? x.y : u.y - bo1;
-          const float un0 = v0 + bo0, un1 = v1 + bo1;                 // argument of (3.4b)
-          const float bn0 = clampf(un0, ta), bn1 = clampf(un1, tb);   // b^k
-          const float dn0 = un0 - bn0, dn1 = un1 - bn1;               // d^k = shrink_1
-          const float e0 = dn0 - do0, e1 = dn1 - do1;                 // d^k - d^{k-1}
-          const float f0 = dn0 - v0, f1 = dn1 - v1;                   // d^k - v^k
-          const float g0 = v0 - vp.x, g1 = v1 - vp.y;                 // v^k - v^{k-1}
-          // phi partial: <x,d> - <A^{-1} v, d - v/2> - t w |d|, A^{-1} v = U^k - lambda v
-          const float Uk0 = fmaf(lam, do0 - bo0, x.x), Uk1 = fmaf(lam, do1 - bo1, x.y);
-          const float gi0 = fmaf(-lam, v0, Uk0), gi1 = fmaf(-lam, v1, Uk1);
-          float ph = x.x * dn0 + x.y * dn1;
-          ph = fmaf(-gi0, fmaf(-0.5f, v0, dn0), ph);
-          ph = fmaf(-gi1, fmaf(-0.5f, v1, dn1), ph);
-          ph = fmaf(-tt, w0 * fabsf(dn0) + w1 * fabsf(dn1), ph);
-          qv[4 * j + 0] = fmaf(e0, e0, e1 * e1);
-          qv[4 * j + 1] = fmaf(f0, f0, f1 * f1);
-          qv[4 * j + 2] = fmaf(g0, g0, g1 * g1);
-          qv[4 * j + 3] = ph;
-          us[p16] = make_float2(un0, un1);
-          vs[p16] = make_float2(v0, v1);
-          Un0 = fmaf(lam, dn0 - bn0, x.x);   // next operand U^{k+1} = x + lambda (d^k - b^k)
-          Un1 = fmaf(lam, dn1 - bn1, x.y);
-        } else {
-          qv[4 * j + 0] = qv[4 * j + 1] = qv[4 * j + 2] = qv[4 * j + 3] = 0.f;
-          Un0 = fmaf(lam, x.x, x.x);         // U^1 = (1 + lambda) x of a loaded point
-          Un1 = fmaf(lam, x.y, x.y);
-        }
-        __half h0, l0, h1, l1;
-        split_h(Un0, h0, l0);
-        split_h(Un1, h1, l1);
-        const uint32_t sh = (j & 1) * 16;
-        if ((j & 1) == 0) { ph0[j >> 1] = 0u; pl0[j >> 1] = 0u; ph1[j >> 1] = 0u; pl1[j >> 1] = 0u; }
-        ph0[j >> 1] |= (uint32_t)__half_as_ushort(h0) << sh;
-        pl0[j >> 1] |= (uint32_t)__half_as_ushort(l0) << sh;
-        ph1[j >> 1] |= (uint32_t)__half_as_ushort(h1) << sh;
-        pl1[j >> 1] |= (uint32_t)__half_as_ushort(l1) << sh;
+        // fp16 hi/lo of the pair of points (jj, jj+1) for each coordinate: packed conversions
+        const __half2 h0 = __floats2half2_rn(Unj[0].x, Unj[1].x);   // coordinate c0
+        const __half2 h1 = __floats2half2_rn(Unj[0].y, Unj[1].y);   // coordinate c1
+        const float2 hb0 = __half22float2(h0), hb1 = __half22float2(h1);
+        const __half2 l0 = __floats2half2_rn(Unj[0].x - hb0.x, Unj[1].x - hb0.y);
+        const __half2 l1 = __floats2half2_rn(Unj[0].y - hb1.x, Unj[1].y - hb1.y);
+        ph0[jj] = *reinterpret_cast<const uint32_t *>(&h0);
+        pl0[jj] = *reinterpret_cast<const uint32_t *>(&l0);
+        ph1[jj] = *reinterpret_cast<const uint32_t *>(&h1);
+        pl1[jj] = *reinterpret_cast<const uint32_t *>(&l1);
       }
       // 8 points are contiguous in the MN-major U^T layout: one 16-byte store per (c, hi/lo)
       {
