@@ -134,10 +134,6 @@ __device__ __forceinline__ float2 clamp2(float2 u, float2 t) {
 // kappa pair of this lane from shared memory (non-union kernels).  ld.volatile keeps the load
 // inside the loop (no hoisting back into registers): kappa is the same for every point, so it
 // is held once per CTA instead of occupying CPL registers per thread.
-__device__ __forceinline__ void sts_volatile2(float2 *p, float2 v) {
-  asm volatile("st.volatile.shared.v2.f32 [%0], {%1,%2};"
-               :: "r"((unsigned)__cvta_generic_to_shared(p)), "f"(v.x), "f"(v.y));
-}
 __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
   float2 v;
   asm volatile("ld.volatile.shared.v2.f32 {%0,%1}, [%2];"
@@ -161,11 +157,11 @@ __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
 // freezes its d (the in-place update is multiplied by live = 0) and waits; the warp runs the
 // finalize/refill branch once at least half of its groups wait (or all of its remaining ones),
 // so that with G < 32 the branch is shared by several groups instead of run once per group.
-// __launch_bounds__(128, 4) (union: 3): at most 128 (168) registers, i.e. 4 (3) warps per SM
-// sub-partition (each SMSP has a 16K-register file); with ~195 registers only 2 warps per SMSP
-// were resident, which leaves the dependent FP32x2 chains exposed.
+// __launch_bounds__(128, 3): at most 168 registers, i.e. 3 warps per SM sub-partition (each
+// SMSP has a 16K-register file); the widest variants otherwise take ~195 registers and only
+// 2 warps per SMSP, which leaves the dependent FP32x2 chains exposed.
 template <int G, int CPL, int HK, bool UNION>
-__global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const DiagParams p) {
+__global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
   constexpr bool KSM = !UNION;            // -kappa in shared memory
   constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
   constexpr int GPW = 32 / G;             // groups per warp
@@ -179,15 +175,8 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
   // slots j < jmax of this lane hold real coordinates (i = gl + G*j < n)
   const int jmax = (n - gl + G - 1) / G;
 
-  // Per-slot registers (pairs).  d holds -d on the l2 path.  x_hat is read-only during a
-  // solve: the non-union kernels keep it in shared memory (lane-private slots, 8 bytes per pair)
-  // so that the three iterated vectors alone occupy registers (<= 128 => 4 warps per SMSP).
-  constexpr bool XSM = !UNION;
-  float2 xh_r[XSM ? 1 : NP], d[NP], b[NP], v[NP];
-  __shared__ __align__(16) float2 xh_s[XSM ? 4 * NP * 32 : 1];   // [warp in block][pair][lane]
-  float2 *xh_my = xh_s + (XSM ? ((threadIdx.x >> 5) * NP * 32 + (threadIdx.x & 31)) : 0);
-  auto XH = [&](int q) -> float2 { return XSM ? lds_volatile2(xh_my + q * 32) : xh_r[q]; };
-  auto XH_SET = [&](int q, float2 val) { if (XSM) sts_volatile2(xh_my + q * 32, val); else xh_r[q] = val; };
+  // Per-slot registers (pairs).  d holds -d on the l2 path.
+  float2 xh[NP], d[NP], b[NP], v[NP];
   float2 kap[KSM ? 1 : NP];    // union: -kappa (l2) / kappa (l1) of the current set
   float2 tau[HK == HK_WL1 ? NP : 1];
   float2 xr[UNION ? NP : 1];   // union: the raw point x (sets translate it by c_k)
@@ -235,7 +224,7 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
         const float x0 = (j0 < CPL && j0 < jmax) ? __ldg(xrow + gl + G * j0) : 0.f;
         const float x1 = (j1 < CPL && j1 < jmax) ? __ldg(xrow + gl + G * j1) : 0.f;
         bad |= !finite_f(x0) || !finite_f(x1);
-        if (UNION) xr[q] = make_float2(x0, x1); else XH_SET(q, make_float2(x0, x1));
+        if (UNION) xr[q] = make_float2(x0, x1); else xh[q] = make_float2(x0, x1);
       }
     }
     bad = group_any<G>(bad);
@@ -257,14 +246,14 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
       const int i0 = gl + G * j0, i1 = gl + G * j1;
       const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
       const float c0 = (cp && ok0) ? __ldg(cp + i0) : 0.f, c1 = (cp && ok1) ? __ldg(cp + i1) : 0.f;
-      const float2 xv = UNION ? xr[q] : XH(q);
+      const float2 xv = UNION ? xr[q] : xh[q];
       const float xt0 = ok0 ? xv.x - c0 : 0.f, xt1 = ok1 ? xv.y - c1 : 0.f;
       const float di0 = __fdividef(1.f, D0 + lam), di1 = __fdividef(1.f, D1 + lam);
       if (!KSM) kap[q] = make_float2(ok0 ? ksign * lam * di0 : 0.f, ok1 ? ksign * lam * di1 : 0.f);
       if (HK == HK_WL1)
         tau[q] = make_float2(ok0 ? tl * __ldg(p.w + i0) : 0.f, ok1 ? tl * __ldg(p.w + i1) : 0.f);
       const float2 xt = make_float2(xt0, xt1);
-      XH_SET(q, make_float2(xt0 * di0, xt1 * di1));
+      xh[q] = make_float2(xt0 * di0, xt1 * di1);
       if (HK == HK_L2) {
         d[q] = make_float2(-xt0, -xt1);   // -d^0 = -(x - c)
         b[q] = xt;                        // pending u with s = 1 reproduces d^0 and b^0 = 0
@@ -287,8 +276,7 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
   } else {
 #pragma unroll
     for (int q = 0; q < NP; q++) {
-      XH_SET(q, splat2(0.f));
-      d[q] = b[q] = v[q] = splat2(0.f);
+      xh[q] = d[q] = b[q] = v[q] = splat2(0.f);
       if (!KSM) kap[q] = splat2(0.f);
     }
   }
@@ -316,7 +304,7 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
         const float2 dmv = add2(d[q], v[q]);           // v^k - d^k
         b[q] = add2(b[q], d[q]);                       // (3.4c): b_k = u_k - d_k
         const float2 na = add2(d[q], b[q]);            // -(d_k - b_k)
-        const float2 t = sub2(XH(q), v[q]);
+        const float2 t = sub2(xh[q], v[q]);
         const float2 dv = fma2(kq, na, t);             // (3.4a): v_{k+1} - v_k
         v[q] = add2(v[q], dv);                         // v_{k+1}
         b[q] = add2(v[q], b[q]);                       // u_{k+1} = v_{k+1} + b_k
@@ -324,7 +312,7 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
         else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
       } else {
         const float2 a = sub2(d[q], b[q]);
-        const float2 t = sub2(XH(q), v[q]);
+        const float2 t = sub2(xh[q], v[q]);
         const float2 dv = fma2(kq, a, t);              // (3.4a): v^k - v^{k-1}
         v[q] = add2(v[q], dv);                         // v^k
         const float2 u = add2(v[q], b[q]);
@@ -383,8 +371,7 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
         const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
         const int i0 = gl + G * j0, i1 = gl + G * j1;
         const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
-        const float2 xq = XH(q);
-        const float xt0 = xq.x * (D0 + lam), xt1 = xq.y * (D1 + lam);
+        const float xt0 = xh[q].x * (D0 + lam), xt1 = xh[q].y * (D1 + lam);
         float2 dq = (HK == HK_L2) ? make_float2(0.f - d[q].x, 0.f - d[q].y) : d[q];
         if (spec == 1) {
           dq = make_float2(ok0 ? __fdividef(xt0, D0) : 0.f, ok1 ? __fdividef(xt1, D1) : 0.f);
@@ -475,7 +462,7 @@ __global__ void __launch_bounds__(128, UNION ? 3 : 4) hopf_diag_kernel(const Dia
         setup_solve();
       } else {
 #pragma unroll
-        for (int q = 0; q < NP; q++) { XH_SET(q, splat2(0.f)); d[q] = b[q] = v[q] = splat2(0.f); }
+        for (int q = 0; q < NP; q++) xh[q] = d[q] = b[q] = v[q] = splat2(0.f);
         spec = 0;
         waiting = false;
       }
