@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../../include/hopf.h"
@@ -25,8 +27,10 @@ int dense_plan_upload(int n, const double *Ml, const double *Ainv, const double 
   }
   for (size_t i = 0; i < nn; i++) a[i] = (float)Amat[i];
   out->n = n;
-  if (n == 256) {   // tensor-core operands for the tcgen05 kernel
-    const int rc = dense_tc_prepare(n, Ml, &out->tc_blocks, &out->tc_scale_inv);
+  if (n == 256) {   // tensor-core operands for the tcgen05 kernels
+    int rc = dense_tc_prepare(n, Ml, &out->tc_blocks, &out->tc_scale_inv);
+    if (rc != HOPF_OK) return rc;
+    rc = dense_tc2_prepare(n, Ml, &out->tc2_rows, &out->tc2_scale_inv);
     if (rc != HOPF_OK) return rc;
   }
   if (cudaMalloc(&out->Ml, nn * 4) != cudaSuccess || cudaMalloc(&out->Ainv, nn * 4) != cudaSuccess ||
@@ -50,6 +54,8 @@ void dense_plan_free(DensePlanDev *d) {
   if (d->Ainv) cudaFree(d->Ainv);
   if (d->A) cudaFree(d->A);
   if (d->tc_blocks) cudaFree(d->tc_blocks);
+  if (d->tc2_rows) cudaFree(d->tc2_rows);
+  d->tc2_rows = nullptr;
   if (d->fix) cudaFree(d->fix);
   d->Ml = d->Ainv = d->A = nullptr;
   d->tc_blocks = nullptr;
@@ -325,7 +331,11 @@ int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t 
     plan.fix_cap = p.M + 1;
   }
   cudaMemsetAsync(plan.fix, 0, sizeof(int), stream);
-  int rc = dense_tc_launch(p, hk, plan.tc_blocks, plan.tc_scale_inv, plan.fix, plan.fix + 1, stream);
+  // HOPF_DENSE_KERNEL=tc1 selects the single-CTA kernel (comparison / fallback)
+  static const char *sel = getenv("HOPF_DENSE_KERNEL");
+  const bool use_tc1 = sel && strcmp(sel, "tc1") == 0;
+  int rc = use_tc1 ? dense_tc_launch(p, hk, plan.tc_blocks, plan.tc_scale_inv, plan.fix, plan.fix + 1, stream)
+                   : dense_tc2_launch(p, hk, plan.tc2_rows, plan.tc2_scale_inv, plan.fix, plan.fix + 1, stream);
   if (rc != HOPF_OK) return rc;
   DenseParams q = p;
   q.idx = plan.fix + 1;
