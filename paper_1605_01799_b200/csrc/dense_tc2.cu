@@ -98,13 +98,17 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count));
 }
+// Poll with CTA-scope acquire (a cluster-scope try_wait makes ptxas emit an L1 invalidation,
+// CCTL.IVALL, on every poll), then one cluster-scope acquire fence for the remote stores
+// (busy / terminate flags) that were released before the remote arrive.
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
-    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
                  "selp.u32 %0, 1, 0, p;\n}"
                  : "=r"(done) : "r"(bar), "r"(phase) : "memory");
   }
+  asm volatile("fence.acq_rel.cluster;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(cluster_addr) : "memory");
