@@ -35,8 +35,10 @@ struct DensePlanDev {
   // tensor-core operands (n == 256): fp16 hi/lo blocks of 2^s M_lambda in smem order
   void *tc_blocks = nullptr;   // single-CTA kernel (dense_tc.cu)
   float tc_scale_inv = 0.f;
-  void *tc2_rows = nullptr;    // CTA-pair kernel (dense_tc2.cu), the default
+  void *tc2_rows = nullptr;    // CTA-pair kernel v3 (dense_tc2.cu)
   float tc2_scale_inv = 0.f;
+  void *tc3_rows = nullptr;    // CTA-pair pipelined kernel v4 (dense_tc3.cu), the default
+  float tc3_scale_inv = 0.f;
   // fix-up list workspace [count, idx...] (grown on demand)
   int *fix = nullptr;
   int64_t fix_cap = 0;
@@ -53,6 +55,9 @@ int dense_tc_launch(const DenseParams &p, int hk, const void *blocks, float msca
                     int *fix_count, int *fix_list, cudaStream_t stream);
 int dense_tc2_prepare(int n, const double *Ml, void **rows_dev, float *mscale_inv);
 int dense_tc2_launch(const DenseParams &p, int hk, const void *rows, float mscale_inv,
+                     int *fix_count, int *fix_list, cudaStream_t stream);
+int dense_tc3_prepare(int n, const double *Ml, void **rows_dev, float *mscale_inv);
+int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscale_inv,
                      int *fix_count, int *fix_list, cudaStream_t stream);
 
 }  // namespace hopf

@@ -32,6 +32,8 @@ int dense_plan_upload(int n, const double *Ml, const double *Ainv, const double 
     if (rc != HOPF_OK) return rc;
     rc = dense_tc2_prepare(n, Ml, &out->tc2_rows, &out->tc2_scale_inv);
     if (rc != HOPF_OK) return rc;
+    rc = dense_tc3_prepare(n, Ml, &out->tc3_rows, &out->tc3_scale_inv);
+    if (rc != HOPF_OK) return rc;
   }
   if (cudaMalloc(&out->Ml, nn * 4) != cudaSuccess || cudaMalloc(&out->Ainv, nn * 4) != cudaSuccess ||
       cudaMalloc(&out->A, nn * 4) != cudaSuccess) {
@@ -56,6 +58,8 @@ void dense_plan_free(DensePlanDev *d) {
   if (d->tc_blocks) cudaFree(d->tc_blocks);
   if (d->tc2_rows) cudaFree(d->tc2_rows);
   d->tc2_rows = nullptr;
+  if (d->tc3_rows) cudaFree(d->tc3_rows);
+  d->tc3_rows = nullptr;
   if (d->fix) cudaFree(d->fix);
   d->Ml = d->Ainv = d->A = nullptr;
   d->tc_blocks = nullptr;
@@ -320,7 +324,7 @@ static int launch_simt(const DenseParams &p, int hk, const DensePlanDev &plan, c
 // n == 256 and H in {l1, wl1}: tcgen05 kernel, then the exact SIMT kernel on its fix-up list
 // (t == 0, invalid points, fp16 overflow, no convergence within max_iter).  Otherwise SIMT.
 int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t stream) {
-  const bool use_tc = plan.tc_blocks && p.n == 256 && hk != HK_L2 && p.M <= 0x7fffffffLL;
+  const bool use_tc = plan.tc_blocks && p.n == 256 && hk != HK_L2 && p.M <= 0x7fffffffLL - (1LL << 20);
   if (!use_tc) return launch_simt(p, hk, plan, stream);
   if (plan.fix_cap < p.M + 1) {
     if (plan.fix) cudaFree(plan.fix);
@@ -331,11 +335,15 @@ int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t 
     plan.fix_cap = p.M + 1;
   }
   cudaMemsetAsync(plan.fix, 0, sizeof(int), stream);
-  // HOPF_DENSE_KERNEL=tc1 selects the single-CTA kernel (comparison / fallback)
+  // HOPF_DENSE_KERNEL=tc1 / tc2 select the earlier tensor-core kernels (comparison only)
   static const char *sel = getenv("HOPF_DENSE_KERNEL");
-  const bool use_tc1 = sel && strcmp(sel, "tc1") == 0;
-  int rc = use_tc1 ? dense_tc_launch(p, hk, plan.tc_blocks, plan.tc_scale_inv, plan.fix, plan.fix + 1, stream)
-                   : dense_tc2_launch(p, hk, plan.tc2_rows, plan.tc2_scale_inv, plan.fix, plan.fix + 1, stream);
+  int rc;
+  if (sel && strcmp(sel, "tc1") == 0)
+    rc = dense_tc_launch(p, hk, plan.tc_blocks, plan.tc_scale_inv, plan.fix, plan.fix + 1, stream);
+  else if (sel && strcmp(sel, "tc2") == 0)
+    rc = dense_tc2_launch(p, hk, plan.tc2_rows, plan.tc2_scale_inv, plan.fix, plan.fix + 1, stream);
+  else
+    rc = dense_tc3_launch(p, hk, plan.tc3_rows, plan.tc3_scale_inv, plan.fix, plan.fix + 1, stream);
   if (rc != HOPF_OK) return rc;
   DenseParams q = p;
   q.idx = plan.fix + 1;
