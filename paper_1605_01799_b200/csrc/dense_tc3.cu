@@ -49,7 +49,11 @@ constexpr int N_DIM = 256;
 constexpr int PTS = 64;                  // point slots per CTA (128 per pair)
 constexpr int EPI_WARPS = 16;
 constexpr int EPI_THREADS = EPI_WARPS * 32;
-constexpr int THREADS = EPI_THREADS;
+constexpr int THREADS = EPI_THREADS + 128;   // + one warpgroup whose first warp issues the MMAs
+// setmaxnreg moves registers inside the CTA's own allocation (640 threads x 96 at launch):
+// 16 warps x 112 + 4 warps x 32 = 20 warps x 96 (asking for more never returns)
+constexpr int EPI_REGS = 112, MMA_REGS = 32;
+static_assert(EPI_WARPS * EPI_REGS + 4 * MMA_REGS <= (EPI_WARPS + 4) * 96, "setmaxnreg budget");
 constexpr int OFF_UH = 0;                // U hi: 64 rows x 256 fp16, K-major (32 KB)
 constexpr int OFF_UL = 32768;            // U lo
 constexpr int OFF_BH = 65536;            // M_lambda rows hi: 128 x 256 fp16 (64 KB)
@@ -132,18 +136,19 @@ __device__ __forceinline__ bool mbar_test_cluster(uint32_t bar, uint32_t phase) 
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
-    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n"
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
                  "selp.u32 %0, 1, 0, p;\n}"
-                 : "=r"(done) : "r"(bar), "r"(phase), "r"(0x989680u) : "memory");
+                 : "=r"(done) : "r"(bar), "r"(phase) : "memory");
   }
 }
-// blocking wait with a suspend-time hint: the thread sleeps until the phase completes
+// blocking wait (try_wait suspends the thread for a short hardware-chosen time per poll; an
+// explicit suspend-time hint compiled to NANOSLEEP and woke up late in the round trace)
 __device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
-    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
                  "selp.u32 %0, 1, 0, p;\n}"
-                 : "=r"(done) : "r"(bar), "r"(phase), "r"(0x989680u) : "memory");
+                 : "=r"(done) : "r"(bar), "r"(phase) : "memory");
   }
 }
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
@@ -261,52 +266,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sm0 = smem_u32(smem);
 
-  // MMA issue (leader CTA, warp 0, warp-collective with elect.sync): stages are issued as soon
-  // as their barrier completes, polled without blocking after each of warp 0's own stages
-  const bool issuer_warp = rank == 0 && warp == 0;
-  const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const uint64_t a_h0 = make_sdesc(sm0 + OFF_UH, 128, 4096), a_l0 = make_sdesc(sm0 + OFF_UL, 128, 4096);
-  const uint64_t b_h0 = make_sdesc(sm0 + OFF_BH, 128, 4096), b_l0 = make_sdesc(sm0 + OFF_BL, 128, 4096);
-  int next_issue = 0;      // next stage of the current round to issue
-  bool stopped = false;    // the leader found no work left (no more MMAs)
-  // issue stage s of round r into D[(r+1) % 3] (whole warp 0 of the leader, converged)
-  auto issue_stage = [&](uint32_t r, int s) {
-    if (s == 0) {
-      const int b = busy[r & 1];
-      __syncwarp();
-      if (lane == 0) busy[r & 1] = 0;
-      if (!b) {
-        stopped = true;   // term first, then wake the MMA waiters of both CTAs
-        if (lane == 0) {
-          mbar_arrive_local(bar_term);
-          mbar_arrive_remote(mapa(bar_term, 1));
-          mbar_arrive_local(bar_mma);
-          mbar_arrive_remote(mapa(bar_mma, 1));
+  if (warp >= EPI_WARPS) {
+    // ================= MMA warpgroup: warp 16 of the leader issues, the others idle =========
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(MMA_REGS));
+    if (rank == 0 && warp == EPI_WARPS) {
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const uint64_t a_h0 = make_sdesc(sm0 + OFF_UH, 128, 4096), a_l0 = make_sdesc(sm0 + OFF_UL, 128, 4096);
+      const uint64_t b_h0 = make_sdesc(sm0 + OFF_BH, 128, 4096), b_l0 = make_sdesc(sm0 + OFF_BL, 128, 4096);
+      for (uint32_t r = 0;; r++) {
+        const uint32_t d_tmem = tmem + 128u * ((r + 1) % 3);
+        bool stop = false;
+#pragma unroll 1
+        for (int s = 0; s < 4; s++) {
+          if (lane == 0) mbar_wait_cluster(bar_stage0 + 8 * s, r & 1);
+          __syncwarp();
+          if (s == 0) {
+            const int b = busy[r & 1];
+            __syncwarp();
+            if (lane == 0) busy[r & 1] = 0;
+            if (!b) { stop = true; break; }
+          }
+          asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            const int ks = 4 * s + t;
+            const uint64_t o = (uint64_t)(ks * 16);
+            mma2_f16_elect(d_tmem, a_h0 + o, b_h0 + o, idesc, ks > 0 ? 1u : 0u);   // Uh Mh
+            mma2_f16_elect(d_tmem, a_l0 + o, b_h0 + o, idesc, 1u);                 // Ul Mh
+            mma2_f16_elect(d_tmem, a_h0 + o, b_l0 + o, idesc, 1u);                 // Uh Ml
+          }
         }
-        return;
+        if (stop) {   // no work left in either CTA: term first, then wake the MMA waiters
+          if (lane == 0) {
+            mbar_arrive_local(bar_term);
+            mbar_arrive_remote(mapa(bar_term, 1));
+            mbar_arrive_local(bar_mma);
+            mbar_arrive_remote(mapa(bar_mma, 1));
+          }
+          break;
+        }
+        commit2_elect(bar_mma);
       }
     }
-    if (stopped) return;
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t d_tmem = tmem + 128u * ((r + 1) % 3);
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-      const int ks = 4 * s + t;
-      const uint64_t o = (uint64_t)(ks * 16);
-      mma2_f16_elect(d_tmem, a_h0 + o, b_h0 + o, idesc, ks > 0 ? 1u : 0u);   // Uh Mh
-      mma2_f16_elect(d_tmem, a_l0 + o, b_h0 + o, idesc, 1u);                 // Ul Mh
-      mma2_f16_elect(d_tmem, a_h0 + o, b_l0 + o, idesc, 1u);                 // Uh Ml
-    }
-    if (s == 3) commit2_elect(bar_mma);
-  };
-
-  {
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(EPI_REGS));
     // ================= epilogue warps =======================================================
     const int q = warp & 3, j = warp >> 2;
     const int pl = 32 * (q & 1) + lane;           // local point slot
     const int h = q >> 1;
     const int part = 4 * h + j;                   // which of the 8 partials of the point
-    const bool decider = part == 0;               // warps 0 and 1: one thread per slot
+    const bool decider = part == 7;               // warps 14 and 15 (not the issuer warp 0)
     const int cb = 128 * h + 32 * j;              // first coordinate of this thread
     const uint32_t t_lane = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * j);
     const uint32_t t_x = t_lane + 384u;           // x of the slot's point (TMEM columns 384..511)
@@ -315,11 +324,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int4 *ctrl = reinterpret_cast<int4 *>(smem + OFF_CTRL);
     int *ctrl_n = reinterpret_cast<int *>(smem + OFF_CTRLN);
 
-    // d^{k-1}, b^{k-1} of this thread's 32 coordinates.  A slot that starts a point holds x in
-    // ds (loaded before the MMA wait) and 0 in bs.
-    float2 ds[16], bs[16];
+    // u^{k-1} = v^{k-1} + b^{k-2} (the argument of the previous shrink) of this thread's 32
+    // coordinates: b^{k-1} = clamp(u, tau), d^{k-1} = u - b^{k-1}.  A slot that starts a point
+    // holds x in us (loaded before its first round) and runs that round with tau = 0.
+    float2 us[16];
 #pragma unroll
-    for (int i = 0; i < 16; i++) ds[i] = bs[i] = splat2(0.f);
+    for (int i = 0; i < 16; i++) us[i] = splat2(0.f);
 
     // decider state of the slot (replicated to the other 7 threads through ctrl[pl], ctrl_n[pl])
     int dpt = (int)(pair * 2 * PTS) + (int)rank * PTS + pl - (int)stride;
@@ -414,14 +424,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const float tt = __int_as_float(cc.w);
       const bool st = mode == M_START || mode == M_START_LD, fin = mode == M_FINISH;
       const int nxt = fin ? ctrl_n[pl] : (int)p.M;
-      if (mode == M_START_LD) {   // new point: x into ds (d^0 = x), b^0 = 0
+      if (mode == M_START_LD) {   // new point: x into us
         const float4 *xr = reinterpret_cast<const float4 *>(p.X + pt * (int64_t)N_DIM + cb);
 #pragma unroll
         for (int g = 0; g < 8; g++) {
           const float4 v4 = __ldg(xr + g);
-          ds[2 * g] = make_float2(v4.x, v4.y);
-          ds[2 * g + 1] = make_float2(v4.z, v4.w);
-          bs[2 * g] = bs[2 * g + 1] = splat2(0.f);
+          us[2 * g] = make_float2(v4.x, v4.y);
+          us[2 * g + 1] = make_float2(v4.z, v4.w);
         }
       }
       if (st) {   // its successor into L2
@@ -437,8 +446,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       tmark(r, tid == 0 ? 15 : 14);
       const bool any_st = __any_sync(0xffffffffu, st), any_fin = __any_sync(0xffffffffu, fin);
-      // START: tau = 0 and v := x give u = x, d^0 = x, b^0 = 0 and U^1 = (1 + lambda) x
-      const float tcur = st ? 0.f : tt * ilam;
+      // START: tau_old = tau = 0 and v := x give u = x, d^0 = x, b^0 = 0 and U^1 = (1 + lambda) x;
+      // k = 1: tau_old = 0 gives b^0 = 0, d^0 = u = x (R5), and v_prev = x from TMEM (R3)
+      const bool fst = mode == M_ACTIVE && it == 0;
+      const float tcur = st ? 0.f : tt * ilam, told = (st || fst) ? 0.f : tt * ilam;
       // ---- wait for MMA r (v^k in D[r % 3]) or termination -----------------------------------
       if (r > 0) {
         if (lane == 0) mbar_wait_hint(bar_mma, (r - 1) & 1);
@@ -474,8 +485,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int i2 = 0; i2 < 4; i2++) {
             const int i = 4 * s + i2;
             if (st) {
-              xa[2 * i2] = va[2 * i2] = ds[i].x;
-              xa[2 * i2 + 1] = va[2 * i2 + 1] = ds[i].y;
+              xa[2 * i2] = va[2 * i2] = us[i].x;
+              xa[2 * i2 + 1] = va[2 * i2 + 1] = us[i].y;
             }
           }
           tmem_st8(t_x + 8 * s, xa);
@@ -489,9 +500,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const int i = 4 * s + i2;
             const float2 v = make_float2(va[2 * i2], va[2 * i2 + 1]);
             const float2 x = make_float2(xa[2 * i2], xa[2 * i2 + 1]);
-            const float2 d = ds[i], b = bs[i];
             const float2 wv = (HK == HK_WL1) ? *reinterpret_cast<const float2 *>(w_s + cb + 2 * i)
                                              : splat2(1.f);
+            const float2 b = clamp2(us[i], mul2(splat2(tt * ilam), wv));   // b^k
+            const float2 d = sub2(us[i], b);                                // d^k
             const float2 Uf = fma2(splat2(lam), sub2(d, b), x);
             const float2 g = fma2(splat2(-lam), v, Uf);              // A^{-1} v^{k+1}
             const float2 hv = fma2(splat2(-0.5f), v, d);
@@ -511,20 +523,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const float2 v = make_float2(va[2 * i2], va[2 * i2 + 1]);
           const float2 vp = make_float2(vpa[2 * i2], vpa[2 * i2 + 1]);
           const float2 x = make_float2(xa[2 * i2], xa[2 * i2 + 1]);
-          const float2 tau = (HK == HK_WL1)
-                                 ? mul2(splat2(tcur), *reinterpret_cast<const float2 *>(w_s + cb + 2 * i))
-                                 : splat2(tcur);
-          const float2 un = add2(v, bs[i]);                // argument of (3.4b): v^k + b^{k-1}
-          bs[i] = clamp2(un, tau);                         // b^k (projection, Moreau)
-          const float2 dn = sub2(un, bs[i]);               // d^k = shrink_1
-          const float2 ed = sub2(dn, ds[i]);
+          const float2 wv = (HK == HK_WL1) ? *reinterpret_cast<const float2 *>(w_s + cb + 2 * i)
+                                           : splat2(1.f);
+          const float2 tau = (HK == HK_WL1) ? mul2(splat2(tcur), wv) : splat2(tcur);
+          const float2 tauo = (HK == HK_WL1) ? mul2(splat2(told), wv) : splat2(told);
+          const float2 u = us[i];
+          const float2 bo = clamp2(u, tauo);               // b^{k-1}
+          const float2 dO = sub2(u, bo);                   // d^{k-1}
+          const float2 un = add2(v, bo);                   // argument of (3.4b): v^k + b^{k-1}
+          const float2 bn = clamp2(un, tau);               // b^k (projection, Moreau)
+          const float2 dn = sub2(un, bn);                  // d^k = shrink_1
+          const float2 ed = sub2(dn, dO);
           asd = fma2(ed, ed, asd);
-          ds[i] = dn;
           const float2 fd = sub2(dn, v);
           asb = fma2(fd, fd, asb);
           const float2 gd = sub2(v, vp);
           asv = fma2(gd, gd, asv);
-          const float2 U = fma2(splat2(lam), sub2(dn, bs[i]), x);   // U^{k+1} = x + lambda (d - b)
+          const float2 U = fma2(splat2(lam), sub2(dn, bn), x);   // U^{k+1} = x + lambda (d - b)
+          us[i] = un;
           split2(U, hw[i2], lw[i2]);
         }
         // U^{k+1} of coordinates cb + 8 s .. + 8 -> its K' block: one 16-byte row chunk (hi, lo)
@@ -542,17 +558,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           else mbar_arrive_remote(stage_remote + 8 * s);
         }
         tmark(r, 3 + s);
-        if (issuer_warp) {
-          while (next_issue <= s) {
-            uint32_t ok = 0;
-            if (lane == 0) ok = mbar_test_cluster(bar_stage0 + 8 * next_issue, r & 1);
-            ok = __shfl_sync(0xffffffffu, ok, 0);
-            __syncwarp();
-            if (!ok) break;
-            tmark(r, 8 + next_issue);
-            issue_stage(r, next_issue++);
-          }
-        }
       }
       // ---- partial sums of this round -> red[r & 1]; released through bar_red ---------------
       {
@@ -562,31 +567,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_local(bar_red);
       tmark(r, 7);
-      if (fin && nxt < (int)p.M) {   // the next point of a finished slot: x into ds now (START next round)
+      if (fin && nxt < (int)p.M) {   // the next point of a finished slot: x into us now (START next round)
         const float4 *xr = reinterpret_cast<const float4 *>(p.X + nxt * (int64_t)N_DIM + cb);
 #pragma unroll
         for (int g = 0; g < 8; g++) {
           const float4 v4 = __ldg(xr + g);
-          ds[2 * g] = make_float2(v4.x, v4.y);
-          ds[2 * g + 1] = make_float2(v4.z, v4.w);
-          bs[2 * g] = bs[2 * g + 1] = splat2(0.f);
+          us[2 * g] = make_float2(v4.x, v4.y);
+          us[2 * g + 1] = make_float2(v4.z, v4.w);
         }
-      }
-      if (issuer_warp) {   // the rest of this round's stages, blocking
-        while (next_issue < 4) {
-          if (lane == 0) mbar_wait_cluster(bar_stage0 + 8 * next_issue, r & 1);
-          __syncwarp();
-          tmark(r, 8 + next_issue);
-          issue_stage(r, next_issue++);
-        }
-        next_issue = 0;
-#ifdef HOPF_TC3_TRACE
-        if (trace && r >= TR0 && r < TR0 + 64 && lane == 0) {   // trace only: time the MMA completion
-          while (!mbar_test(bar_mma, r & 1)) {
-          }
-          tmark(r, 14);
-        }
-#endif
       }
     }
   }
