@@ -35,6 +35,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "../../include/hopf.h"
@@ -141,14 +142,11 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) 
                  : "=r"(done) : "r"(bar), "r"(phase) : "memory");
   }
 }
-// blocking wait (try_wait suspends the thread for a short hardware-chosen time per poll; an
-// explicit suspend-time hint compiled to NANOSLEEP and woke up late in the round trace)
+// blocking wait: try_wait suspends the polling thread in hardware between checks, so the
+// waiting warps do not take issue slots from the working ones (one lane per warp waits, the
+// rest sit in __syncwarp)
 __device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t phase) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                 "selp.u32 %0, 1, 0, p;\n}"
-                 : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+  while (!mbar_try(bar, phase)) {
   }
 }
 __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
@@ -197,6 +195,15 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
                   "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])),
                   "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
 }
+// tcgen05.wait::ld that names the destination registers of the loads it waits for, so the
+// compiler cannot read or move them between the (asynchronous) tcgen05.ld and the wait
+__device__ __forceinline__ void tmem_wait_ld3(float (&a)[8], float (&b)[8], float (&c)[8]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(a[0]), "+f"(a[1]), "+f"(a[2]), "+f"(a[3]), "+f"(a[4]), "+f"(a[5]), "+f"(a[6]), "+f"(a[7]),
+                 "+f"(b[0]), "+f"(b[1]), "+f"(b[2]), "+f"(b[3]), "+f"(b[4]), "+f"(b[5]), "+f"(b[6]), "+f"(b[7]),
+                 "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3]), "+f"(c[4]), "+f"(c[5]), "+f"(c[6]), "+f"(c[7])
+               :: "memory");
+}
 __device__ __forceinline__ float clampf(float u, float t) { return fminf(fmaxf(u, -t), t); }
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
@@ -219,6 +226,7 @@ __device__ __forceinline__ void split2(float2 u, uint32_t &hw, uint32_t &lw) {
 // optional per-round timestamps (HOPF_TC3_TRACE=<file>): CTAs 0/1, threads 0 and 160,
 // rounds [TR0, TR0 + 64), events: start, decided, mma ready, stage 0-3 arrived, partials, issue 0-3
 __device__ long long *g_tc3_trace = nullptr;
+__device__ long long *g_tc3_trace2 = nullptr;   // [2 CTAs][16 warps][64 rounds][4]: mma, st0, st3, red
 constexpr int TR0 = 200;
 
 template <int HK, bool SCALED>
@@ -362,13 +370,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
 #ifdef HOPF_TC3_TRACE
     long long *trace = nullptr;
-    if (g_tc3_trace && blockIdx.x < 2 && (tid == 0 || tid == 160))
-      trace = g_tc3_trace + (size_t)(blockIdx.x * 2 + (tid == 160)) * 64 * 16;
+    if (g_tc3_trace && blockIdx.x < 2 && (tid == 0 || tid == 448))
+      trace = g_tc3_trace + (size_t)(blockIdx.x * 2 + (tid == 448)) * 64 * 16;
     auto tmark = [&](uint32_t r, int e) {
       if (trace && r >= TR0 && r < TR0 + 64) trace[(r - TR0) * 16 + e] = clock64();
     };
+    long long *trace2 = nullptr;
+    if (g_tc3_trace2 && blockIdx.x < 2 && lane == 0) trace2 = g_tc3_trace2 + (size_t)(blockIdx.x * 16 + warp) * 64 * 4;
+    auto tmark2 = [&](uint32_t r, int e) {
+      if (trace2 && r >= TR0 && r < TR0 + 64) trace2[(r - TR0) * 4 + e] = clock64();
+    };
 #else
     auto tmark = [](uint32_t, int) {};
+    auto tmark2 = [](uint32_t, int) {};
 #endif
     for (uint32_t r = 0;; r++) {
       tmark(r, 0);
@@ -457,23 +471,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         __syncwarp();
         if (mbar_test(bar_term, 0)) break;
         tmark(r, 2);
+        tmark2(r, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
       }
       const uint32_t tbuf = t_lane + 128u * (r % 3), tpbuf = t_lane + 128u * ((r + 2) % 3);
       float2 asd = splat2(0.f), asb = splat2(0.f), asv = splat2(0.f);
       float aph = 0.f;
+      // TMEM loads are software-pipelined: stage s+1's are issued before stage s's stores,
+      // fences and arrive, into the registers stage s has finished with
+      float va[8], vpa[8], xa[8];
+      if (r > 0) {
+        tmem_ld8(tbuf, va);
+        tmem_ld8(tpbuf, vpa);
+        tmem_ld8(t_x, xa);
+        tmem_wait_ld3(va, vpa, xa);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; e++) va[e] = vpa[e] = xa[e] = 0.f;
+      }
 #pragma unroll
       for (int s = 0; s < 4; s++) {
-        float va[8], vpa[8], xa[8];
-        if (r > 0) {
-          tmem_ld8(tbuf + 8 * s, va);
-          tmem_ld8(tpbuf + 8 * s, vpa);
-          tmem_ld8(t_x + 8 * s, xa);
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; e++) va[e] = vpa[e] = xa[e] = 0.f;
-        }
         if (SCALED) {
 #pragma unroll
           for (int e = 0; e < 8; e++) { va[e] *= mscale_inv; vpa[e] *= mscale_inv; }
@@ -543,6 +560,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           us[i] = un;
           split2(U, hw[i2], lw[i2]);
         }
+        if (s < 3 && r > 0) {
+          tmem_ld8(tbuf + 8 * (s + 1), va);
+          tmem_ld8(tpbuf + 8 * (s + 1), vpa);
+          tmem_ld8(t_x + 8 * (s + 1), xa);
+        }
         // U^{k+1} of coordinates cb + 8 s .. + 8 -> its K' block: one 16-byte row chunk (hi, lo)
         const uint32_t off = kmaj(pl, 64 * s + 32 * h + 8 * j);
         *reinterpret_cast<uint4 *>(smem + OFF_UH + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -558,6 +580,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           else mbar_arrive_remote(stage_remote + 8 * s);
         }
         tmark(r, 3 + s);
+        if (s == 0) tmark2(r, 1);
+        if (s == 3) tmark2(r, 2);
+        if (s < 3 && r > 0) tmem_wait_ld3(va, vpa, xa);
       }
       // ---- partial sums of this round -> red[r & 1]; released through bar_red ---------------
       {
@@ -567,6 +592,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_local(bar_red);
       tmark(r, 7);
+      tmark2(r, 3);
       if (fin && nxt < (int)p.M) {   // the next point of a finished slot: x into us now (START next round)
         const float4 *xr = reinterpret_cast<const float4 *>(p.X + nxt * (int64_t)N_DIM + cb);
 #pragma unroll
@@ -636,12 +662,15 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
 #else
   const char *trace_path = nullptr;
 #endif
-  long long *dtrace = nullptr;
+  long long *dtrace = nullptr, *dtrace2 = nullptr;
   if (trace_path) {
     cudaMalloc(&dtrace, 4 * 64 * 16 * sizeof(long long));
     cudaMemset(dtrace, 0, 4 * 64 * 16 * sizeof(long long));
 #ifdef HOPF_TC3_TRACE
     cudaMemcpyToSymbol(tc3::g_tc3_trace, &dtrace, sizeof(dtrace));
+    cudaMalloc(&dtrace2, 2 * 16 * 64 * 4 * sizeof(long long));
+    cudaMemset(dtrace2, 0, 2 * 16 * 64 * 4 * sizeof(long long));
+    cudaMemcpyToSymbol(tc3::g_tc3_trace2, &dtrace2, sizeof(dtrace2));
 #endif
   }
   fn<<<(unsigned)(2 * pairs), tc3::THREADS, tc3::SMEM_BYTES, stream>>>(
@@ -659,6 +688,15 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
 #ifdef HOPF_TC3_TRACE
     long long *z = nullptr;
     cudaMemcpyToSymbol(tc3::g_tc3_trace, &z, sizeof(z));
+    cudaMemcpyToSymbol(tc3::g_tc3_trace2, &z, sizeof(z));
+    std::vector<long long> h2(2 * 16 * 64 * 4);
+    cudaMemcpy(h2.data(), dtrace2, h2.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    std::string p2 = std::string(trace_path) + ".warps";
+    if (FILE *f = fopen(p2.c_str(), "w")) {
+      for (size_t i = 0; i < h2.size(); i += 4) fprintf(f, "%lld %lld %lld %lld\n", h2[i], h2[i + 1], h2[i + 2], h2[i + 3]);
+      fclose(f);
+    }
+    cudaFree(dtrace2);
 #endif
     cudaFree(dtrace);
   }
