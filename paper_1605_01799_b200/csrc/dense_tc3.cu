@@ -65,8 +65,8 @@ constexpr int OFF_CTRL = OFF_W + N_DIM * 4;          // int4 per slot: pt, it, m
 constexpr int OFF_CTRLN = OFF_CTRL + PTS * 16;      // int per slot: next point (FINISH)
 constexpr int OFF_BAR = OFF_CTRLN + PTS * 4;
 // bars: [0] mma_done, [8] term, [16..48) stage_ready[4], [48] busy[2] (int), [56] tmem base,
-//       [64] red_ready, [72] dec_ready
-constexpr int SMEM_BYTES = OFF_BAR + 80;
+//       [64] red_ready, [72] dec_ready, [80] fin (leader: drain before termination)
+constexpr int SMEM_BYTES = OFF_BAR + 88;
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB dynamic shared memory of a CTA");
 
 // slot states: START = first round of a point whose x is already in ds (loaded at the end of the
@@ -181,6 +181,10 @@ __device__ __forceinline__ void commit2_elect(uint32_t bar) {
                :: "r"(bar), "h"((uint16_t)3));
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+#ifdef HOPF_TC3_EXP_NOLD
+  for (int i = 0; i < 8; i++) v[i] = 0.5f * (taddr & 7);
+  return;
+#endif
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
@@ -190,6 +194,9 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; i++) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+#ifdef HOPF_TC3_EXP_NOST
+  return;
+#endif
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])),
                   "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])),
@@ -227,6 +234,8 @@ __device__ __forceinline__ void split2(float2 u, uint32_t &hw, uint32_t &lw) {
 // rounds [TR0, TR0 + 64), events: start, decided, mma ready, stage 0-3 arrived, partials, issue 0-3
 __device__ long long *g_tc3_trace = nullptr;
 __device__ long long *g_tc3_trace2 = nullptr;   // [2 CTAs][16 warps][64 rounds][4]: mma, st0, st3, red
+__device__ long long *g_tc3_trace3 = nullptr;   // MMA warp: [64 rounds][8]: stage s observed, issued
+__device__ long long *g_tc3_trace4 = nullptr;   // MMA warp, stage 0: [64 rounds][16]: after each MMA
 constexpr int TR0 = 200;
 
 template <int HK, bool SCALED>
@@ -241,7 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   volatile int *busy = reinterpret_cast<volatile int *>(bars + 48);
   volatile uint32_t *tmem_slot = reinterpret_cast<volatile uint32_t *>(bars + 56);
   const uint32_t bar_mma = smem_u32(bars), bar_term = smem_u32(bars + 8);
-  const uint32_t bar_stage0 = smem_u32(bars + 16), bar_red = smem_u32(bars + 64), bar_dec = smem_u32(bars + 72);
+  const uint32_t bar_stage0 = smem_u32(bars + 16), bar_red = smem_u32(bars + 64), bar_dec = smem_u32(bars + 72), bar_fin = smem_u32(bars + 80);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
@@ -264,6 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int s = 0; s < 4; s++) mbar_init(bar_stage0 + 8 * s, 2 * EPI_WARPS);
     mbar_init(bar_red, EPI_WARPS);
     mbar_init(bar_dec, 2);
+    mbar_init(bar_fin, 1);
     busy[0] = busy[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -277,23 +287,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp >= EPI_WARPS) {
     // ================= MMA warpgroup: warp 16 of the leader issues, the others idle =========
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(MMA_REGS));
+#ifdef HOPF_TC3_TRACE
+    long long *const tr3 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace3 : nullptr;
+    long long *const tr4 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace4 : nullptr;
+#endif
     if (rank == 0 && warp == EPI_WARPS) {
       const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const uint64_t a_h0 = make_sdesc(sm0 + OFF_UH, 128, 4096), a_l0 = make_sdesc(sm0 + OFF_UL, 128, 4096);
       const uint64_t b_h0 = make_sdesc(sm0 + OFF_BH, 128, 4096), b_l0 = make_sdesc(sm0 + OFF_BL, 128, 4096);
       for (uint32_t r = 0;; r++) {
         const uint32_t d_tmem = tmem + 128u * ((r + 1) % 3);
-        bool stop = false;
+        int any_busy = 1;
 #pragma unroll 1
         for (int s = 0; s < 4; s++) {
           if (lane == 0) mbar_wait_cluster(bar_stage0 + 8 * s, r & 1);
           __syncwarp();
-          if (s == 0) {
-            const int b = busy[r & 1];
-            __syncwarp();
-            if (lane == 0) busy[r & 1] = 0;
-            if (!b) { stop = true; break; }
-          }
+#ifdef HOPF_TC3_TRACE
+          if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s] = clock64();
+#endif
+          // the busy word is complete once stage 0 has arrived; its value is only needed
+          // after the last stage, so the shared load stays off the MMA issue path
+          if (s == 0) any_busy = busy[r & 1];
           asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
           for (int t = 0; t < 4; t++) {
@@ -303,9 +317,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             mma2_f16_elect(d_tmem, a_l0 + o, b_h0 + o, idesc, 1u);                 // Ul Mh
             mma2_f16_elect(d_tmem, a_h0 + o, b_l0 + o, idesc, 1u);                 // Uh Ml
           }
+#ifdef HOPF_TC3_TRACE
+          if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s + 1] = clock64();
+#endif
         }
-        if (stop) {   // no work left in either CTA: term first, then wake the MMA waiters
+        __syncwarp();
+        if (lane == 0) busy[r & 1] = 0;
+        if (!any_busy) {
+          // no work left in either CTA: let this round's (unneeded) MMAs drain, then term
+          // first and wake the MMA waiters of both CTAs
+          asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+                       "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}"
+                       :: "r"(bar_fin));
           if (lane == 0) {
+            mbar_wait_hint(bar_fin, 0);
             mbar_arrive_local(bar_term);
             mbar_arrive_remote(mapa(bar_term, 1));
             mbar_arrive_local(bar_mma);
@@ -662,7 +687,7 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
 #else
   const char *trace_path = nullptr;
 #endif
-  long long *dtrace = nullptr, *dtrace2 = nullptr;
+  long long *dtrace = nullptr, *dtrace2 = nullptr, *dtrace3 = nullptr, *dtrace4 = nullptr;
   if (trace_path) {
     cudaMalloc(&dtrace, 4 * 64 * 16 * sizeof(long long));
     cudaMemset(dtrace, 0, 4 * 64 * 16 * sizeof(long long));
@@ -671,6 +696,12 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
     cudaMalloc(&dtrace2, 2 * 16 * 64 * 4 * sizeof(long long));
     cudaMemset(dtrace2, 0, 2 * 16 * 64 * 4 * sizeof(long long));
     cudaMemcpyToSymbol(tc3::g_tc3_trace2, &dtrace2, sizeof(dtrace2));
+    cudaMalloc(&dtrace3, 64 * 8 * sizeof(long long));
+    cudaMemset(dtrace3, 0, 64 * 8 * sizeof(long long));
+    cudaMemcpyToSymbol(tc3::g_tc3_trace3, &dtrace3, sizeof(dtrace3));
+    cudaMalloc(&dtrace4, 64 * 16 * sizeof(long long));
+    cudaMemset(dtrace4, 0, 64 * 16 * sizeof(long long));
+    cudaMemcpyToSymbol(tc3::g_tc3_trace4, &dtrace4, sizeof(dtrace4));
 #endif
   }
   fn<<<(unsigned)(2 * pairs), tc3::THREADS, tc3::SMEM_BYTES, stream>>>(
@@ -697,6 +728,30 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
       fclose(f);
     }
     cudaFree(dtrace2);
+    cudaMemcpyToSymbol(tc3::g_tc3_trace3, &z, sizeof(z));
+    std::vector<long long> h3(64 * 8);
+    cudaMemcpy(h3.data(), dtrace3, h3.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    std::string p3 = std::string(trace_path) + ".mma";
+    if (FILE *f = fopen(p3.c_str(), "w")) {
+      for (size_t i = 0; i < h3.size(); i += 8) {
+        for (int e = 0; e < 8; e++) fprintf(f, "%lld ", h3[i + e]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+    cudaFree(dtrace3);
+    cudaMemcpyToSymbol(tc3::g_tc3_trace4, &z, sizeof(z));
+    std::vector<long long> h4(64 * 16);
+    cudaMemcpy(h4.data(), dtrace4, h4.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    std::string p4 = std::string(trace_path) + ".mma0";
+    if (FILE *f = fopen(p4.c_str(), "w")) {
+      for (size_t i = 0; i < h4.size(); i += 16) {
+        for (int e = 0; e < 8; e++) fprintf(f, "%lld ", h4[i + e]);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+    cudaFree(dtrace4);
 #endif
     cudaFree(dtrace);
   }
