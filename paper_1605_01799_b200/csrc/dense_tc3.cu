@@ -236,7 +236,10 @@ __device__ long long *g_tc3_trace = nullptr;
 __device__ long long *g_tc3_trace2 = nullptr;   // [2 CTAs][16 warps][64 rounds][4]: mma, st0, st3, red
 __device__ long long *g_tc3_trace3 = nullptr;   // MMA warp: [64 rounds][8]: stage s observed, issued
 __device__ long long *g_tc3_trace4 = nullptr;   // MMA warp, stage 0: [64 rounds][16]: after each MMA
-constexpr int TR0 = 200;
+#ifndef HOPF_TC3_TR0
+#define HOPF_TC3_TR0 200
+#endif
+constexpr int TR0 = HOPF_TC3_TR0;
 
 template <int HK, bool SCALED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -291,7 +294,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     long long *const tr3 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace3 : nullptr;
     long long *const tr4 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace4 : nullptr;
 #endif
-    if (rank == 0 && warp == EPI_WARPS) {
+    if (rank == 0 && warp == EPI_WARPS && lane == 0) {
+      // one thread issues (an elect.sync form issued by the converged warp ran the round
+      // skeleton 2.5-4x slower: tools/tcgen05_probe/probe_round.cu)
       const uint32_t idesc = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const uint64_t a_h0 = make_sdesc(sm0 + OFF_UH, 128, 4096), a_l0 = make_sdesc(sm0 + OFF_UL, 128, 4096);
       const uint64_t b_h0 = make_sdesc(sm0 + OFF_BH, 128, 4096), b_l0 = make_sdesc(sm0 + OFF_BL, 128, 4096);
@@ -300,8 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         int any_busy = 1;
 #pragma unroll 1
         for (int s = 0; s < 4; s++) {
-          if (lane == 0) mbar_wait_cluster(bar_stage0 + 8 * s, r & 1);
-          __syncwarp();
+          mbar_wait_cluster(bar_stage0 + 8 * s, r & 1);
 #ifdef HOPF_TC3_TRACE
           if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s] = clock64();
 #endif
@@ -313,34 +317,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int t = 0; t < 4; t++) {
             const int ks = 4 * s + t;
             const uint64_t o = (uint64_t)(ks * 16);
-            mma2_f16_elect(d_tmem, a_h0 + o, b_h0 + o, idesc, ks > 0 ? 1u : 0u);   // Uh Mh
-            mma2_f16_elect(d_tmem, a_l0 + o, b_h0 + o, idesc, 1u);                 // Ul Mh
-            mma2_f16_elect(d_tmem, a_h0 + o, b_l0 + o, idesc, 1u);                 // Uh Ml
+            mma2_f16(d_tmem, a_h0 + o, b_h0 + o, idesc, ks > 0 ? 1u : 0u);   // Uh Mh
+            mma2_f16(d_tmem, a_l0 + o, b_h0 + o, idesc, 1u);                 // Ul Mh
+            mma2_f16(d_tmem, a_h0 + o, b_l0 + o, idesc, 1u);                 // Uh Ml
           }
 #ifdef HOPF_TC3_TRACE
           if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s + 1] = clock64();
 #endif
         }
-        __syncwarp();
-        if (lane == 0) busy[r & 1] = 0;
+        busy[r & 1] = 0;
         if (!any_busy) {
           // no work left in either CTA: let this round's (unneeded) MMAs drain, then term
           // first and wake the MMA waiters of both CTAs
-          asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-                       "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}"
+          asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                        :: "r"(bar_fin));
-          if (lane == 0) {
-            mbar_wait_hint(bar_fin, 0);
-            mbar_arrive_local(bar_term);
-            mbar_arrive_remote(mapa(bar_term, 1));
-            mbar_arrive_local(bar_mma);
-            mbar_arrive_remote(mapa(bar_mma, 1));
-          }
+          mbar_wait_hint(bar_fin, 0);
+          mbar_arrive_local(bar_term);
+          mbar_arrive_remote(mapa(bar_term, 1));
+          mbar_arrive_local(bar_mma);
+          mbar_arrive_remote(mapa(bar_mma, 1));
           break;
         }
-        commit2_elect(bar_mma);
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                     :: "r"(bar_mma), "h"((uint16_t)3));
       }
     }
+    __syncwarp();
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(EPI_REGS));
     // ================= epilogue warps =======================================================
@@ -516,6 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
 #pragma unroll
       for (int s = 0; s < 4; s++) {
+#ifndef HOPF_TC3_EXP_EMPTY
         if (SCALED) {
 #pragma unroll
           for (int e = 0; e < 8; e++) { va[e] *= mscale_inv; vpa[e] *= mscale_inv; }
@@ -594,6 +597,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const uint32_t off = kmaj(pl, 64 * s + 32 * h + 8 * j);
         *reinterpret_cast<uint4 *>(smem + OFF_UH + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         *reinterpret_cast<uint4 *>(smem + OFF_UL + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+#endif
 #ifndef HOPF_TC3_NOFENCE_EXPERIMENT
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif

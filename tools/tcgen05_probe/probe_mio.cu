@@ -37,7 +37,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) probe(long l
   }
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&mbar)), "r"(1));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&never)), "r"(1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&never)), "r"(1000000));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(&stopb)), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -112,6 +112,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) probe(long l
           asm volatile("tcgen05.wait::ld.sync.aligned;");
           for (int i = 0; i < 8; i++) acc += __uint_as_float(v[i]);
         }
+        if (mode >= 10) {   // epilogue-like: 3 x tcgen05.ld x8 + wait, st.shared, proxy fence, tcgen05 fence, arrive
+          uint32_t v[8], v2[8], v3[8];
+          const uint32_t b2 = tm + ((uint32_t)(32 * (warp & 3)) << 16) + 128u + (uint32_t)(32 * ((warp >> 2) & 3));
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]) : "r"(b2 + 8 * (k & 3)));
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3]), "=r"(v2[4]), "=r"(v2[5]), "=r"(v2[6]), "=r"(v2[7]) : "r"(b2 + 128 + 8 * (k & 3)));
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v3[0]), "=r"(v3[1]), "=r"(v3[2]), "=r"(v3[3]), "=r"(v3[4]), "=r"(v3[5]), "=r"(v3[6]), "=r"(v3[7]) : "r"(b2 + 256 + 8 * (k & 3)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;");
+          for (int i = 0; i < 8; i++) acc += __uint_as_float(v[i]) + __uint_as_float(v2[i]) + __uint_as_float(v3[i]);
+          const int row = tid & 63, blk = 8 + (k & 7) + 8 * ((it >> 3) % 3);
+          *reinterpret_cast<uint4*>(smem + (row >> 3) * 4096 + blk * 128 + (row & 7) * 16) = make_uint4(0x3c00u, 0, 0, 0);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (mode >= 11) asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (mode >= 12 && lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&never)));
+        }
         if (mode == 4) { uint32_t q; asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(q) : "r"(smem_u32(sbuf + 16 * (k & 15)))); acc += q; }
       }
       __syncwarp();
@@ -127,8 +145,8 @@ int main() {
   long long* d; cudaMalloc(&d, 32 * 8);
   const int smem = 196608 + 16384;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* names[] = {"none", "tcgen05.ld", "st.shared", "try_wait spin", "ld.shared", "ld+sts", "sts A-region", "tcgen05.ld D", "random data", "random, 148 SMs"};
-  for (int mode = 0; mode < 10; mode++) {
+  const char* names[] = {"none", "tcgen05.ld", "st.shared", "try_wait spin", "ld.shared", "ld+sts", "sts A-region", "tcgen05.ld D", "random data", "random, 148 SMs", "epi: ld3+sts+pfence", "epi +tc fence", "epi +arrive"};
+  for (int mode = 0; mode < 13; mode++) {
     cudaMemset(d, 0, 256);
     probe<<<mode == 9 ? 148 : 2, 512, smem>>>(d, mode == 9 ? 8 : mode);
     cudaError_t e = cudaDeviceSynchronize();
