@@ -50,7 +50,11 @@ constexpr int N_DIM = 256;
 constexpr int PTS = 64;                  // point slots per CTA (128 per pair)
 constexpr int EPI_WARPS = 16;
 constexpr int EPI_THREADS = EPI_WARPS * 32;
+#ifdef HOPF_TC3_NO_SETMAXNREG
+constexpr int THREADS = EPI_THREADS + 32;    // + the MMA warp (96 registers for everyone)
+#else
 constexpr int THREADS = EPI_THREADS + 128;   // + one warpgroup whose first warp issues the MMAs
+#endif
 // setmaxnreg moves registers inside the CTA's own allocation (640 threads x 96 at launch):
 // 16 warps x 112 + 4 warps x 32 = 20 warps x 96 (asking for more never returns)
 constexpr int EPI_REGS = 112, MMA_REGS = 32;
@@ -289,7 +293,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   if (warp >= EPI_WARPS) {
     // ================= MMA warpgroup: warp 16 of the leader issues, the others idle =========
+#ifndef HOPF_TC3_NO_SETMAXNREG
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(MMA_REGS));
+#endif
 #ifdef HOPF_TC3_TRACE
     long long *const tr3 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace3 : nullptr;
     long long *const tr4 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace4 : nullptr;
@@ -305,7 +311,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         int any_busy = 1;
 #pragma unroll 1
         for (int s = 0; s < 4; s++) {
+#ifdef HOPF_TC3_EXP_ACQCL
           mbar_wait_cluster(bar_stage0 + 8 * s, r & 1);
+#else
+          // CTA-scope wait, as CUTLASS's MMA warps do for their operand-full barriers (the
+          // remote arrives are default .release.cta; the tensor core reads the peer's shared
+          // memory through the async proxy after the writers' fence.proxy.async)
+          mbar_wait_hint(bar_stage0 + 8 * s, r & 1);
+#endif
 #ifdef HOPF_TC3_TRACE
           if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s] = clock64();
 #endif
@@ -344,20 +357,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     __syncwarp();
   } else {
+#ifndef HOPF_TC3_NO_SETMAXNREG
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(EPI_REGS));
+#endif
     // ================= epilogue warps =======================================================
     const int q = warp & 3, j = warp >> 2;
     const int pl = 32 * (q & 1) + lane;           // local point slot
     const int h = q >> 1;
     const int part = 4 * h + j;                   // which of the 8 partials of the point
-    const bool decider = part == 7;               // warps 14 and 15 (not the issuer warp 0)
+    const bool writer = part == 7;                // the one thread per slot with side effects
     const int cb = 128 * h + 32 * j;              // first coordinate of this thread
     const uint32_t t_lane = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * j);
     const uint32_t t_x = t_lane + 384u;           // x of the slot's point (TMEM columns 384..511)
     const uint32_t busy_addr = (rank == 0) ? smem_u32((const void *)busy) : mapa(smem_u32((const void *)busy), 0);
     const uint32_t stage_remote = mapa(bar_stage0, 0);
-    int4 *ctrl = reinterpret_cast<int4 *>(smem + OFF_CTRL);
-    int *ctrl_n = reinterpret_cast<int *>(smem + OFF_CTRLN);
 
     // u^{k-1} = v^{k-1} + b^{k-2} (the argument of the previous shrink) of this thread's 32
     // coordinates: b^{k-1} = clamp(u, tau), d^{k-1} = u - b^{k-1}.  A slot that starts a point
@@ -366,7 +379,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int i = 0; i < 16; i++) us[i] = splat2(0.f);
 
-    // decider state of the slot (replicated to the other 7 threads through ctrl[pl], ctrl_n[pl])
+    // slot state, kept identically by the 8 threads of the slot: they read the same 8 partial
+    // sums and the same t values, so they take the same decisions without a broadcast
     int dpt = (int)(pair * 2 * PTS) + (int)rank * PTS + pl - (int)stride;
     int dit = 0, dmode = M_EMPTY;
     float dtt = 0.f;
@@ -379,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       while (q < M32) {
         const float tn = (q == cq) ? ct : __ldg(p.t + q);
         if (tn > 0.f && tn <= FLT_MAX) { t_out = tn; break; }
-        fix_list[atomicAdd(fix_count, 1)] = q;
+        if (writer) fix_list[atomicAdd(fix_count, 1)] = q;
         q += S32;
       }
       q_out = q;
@@ -413,58 +427,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #endif
     for (uint32_t r = 0;; r++) {
       tmark(r, 0);
-      // ---- the decider of each slot reads the 8 partial sums of round r-1 and decides --------
-      if (decider) {
-        if (r == 0) {
-          int q; float tq = 0.f;
-          advance(dpt, q, tq);
-          begin(q, tq, M_START_LD);
-        } else {
-          if (lane == 0) mbar_wait_hint(bar_red, (r - 1) & 1);
-          __syncwarp();
-          tmark(r, 12);
-          float s4[4] = {0.f, 0.f, 0.f, 0.f};
-          const float4 *rp = red + (size_t)((r - 1) & 1) * 8 * PTS + pl;
+      // ---- every thread of a slot reads the 8 partial sums of round r-1 and decides ----------
+      if (r == 0) {
+        int q; float tq = 0.f;
+        advance(dpt, q, tq);
+        begin(q, tq, M_START_LD);
+      } else {
+        if (lane == 0) mbar_wait_hint(bar_red, (r - 1) & 1);
+        __syncwarp();
+        tmark(r, 12);
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+        const float4 *rp = red + (size_t)((r - 1) & 1) * 8 * PTS + pl;
 #pragma unroll
-          for (int k = 0; k < 8; k++) {
-            const float4 a = rp[k * PTS];
-            s4[0] += a.x; s4[1] += a.y; s4[2] += a.z; s4[3] += a.w;
+        for (int k = 0; k < 8; k++) {
+          const float4 a = rp[k * PTS];
+          s4[0] += a.x; s4[1] += a.y; s4[2] += a.z; s4[3] += a.w;
+        }
+        if (dmode == M_ACTIVE) {
+          dit += 1;
+          const bool fin = finitef(s4[0] + s4[1] + s4[2]);
+          if (fin && s4[0] <= tol && s4[1] <= tol && s4[2] <= tol) {
+            dmode = M_FINISH;
+            advance(dpt, npt, ntt);   // its x is loaded at the end of the FINISH round
+          } else if (!fin || dit >= p.max_iter) {
+            if (writer) fix_list[atomicAdd(fix_count, 1)] = dpt;
+            int q; float tq = 0.f;
+            advance(dpt, q, tq);
+            begin(q, tq, M_START_LD);
           }
-          if (dmode == M_ACTIVE) {
-            dit += 1;
-            const bool fin = finitef(s4[0] + s4[1] + s4[2]);
-            if (fin && s4[0] <= tol && s4[1] <= tol && s4[2] <= tol) {
-              dmode = M_FINISH;
-              advance(dpt, npt, ntt);   // its x is loaded at the end of the FINISH round
-            } else if (!fin || dit >= p.max_iter) {
-              fix_list[atomicAdd(fix_count, 1)] = dpt;
-              int q; float tq = 0.f;
-              advance(dpt, q, tq);
-              begin(q, tq, M_START_LD);
-            }
-          } else if (dmode == M_FINISH) {
+        } else if (dmode == M_FINISH) {
+          if (writer) {
             p.phi[dpt] = s4[3] + p.gamma;
             p.iters[dpt] = dit;
-            begin(npt, ntt, M_START);
-          } else if (dmode == M_START || dmode == M_START_LD) {
-            dmode = M_ACTIVE;
           }
+          begin(npt, ntt, M_START);
+        } else if (dmode == M_START || dmode == M_START_LD) {
+          dmode = M_ACTIVE;
         }
-        tmark(r, 13);
-        ctrl_n[pl] = npt < M32 ? npt : M32;
-        ctrl[pl] = make_int4(dpt, dit, dmode, __float_as_int(dtt));
-        __syncwarp();
-        if (lane == 0) mbar_arrive_local(bar_dec);
       }
-      if (lane == 0) mbar_wait_hint(bar_dec, r & 1);
-      __syncwarp();
+      tmark(r, 13);
       tmark(r, 1);
-      const int4 cc = ctrl[pl];
-      const int pt = cc.x;
-      const int mode = cc.z, it = cc.y;
-      const float tt = __int_as_float(cc.w);
+      const int pt = dpt;
+      const int mode = dmode, it = dit;
+      const float tt = dtt;
       const bool st = mode == M_START || mode == M_START_LD, fin = mode == M_FINISH;
-      const int nxt = fin ? ctrl_n[pl] : (int)p.M;
+      const int nxt = fin ? (npt < M32 ? npt : M32) : M32;
       if (mode == M_START_LD) {   // new point: x into us
         const float4 *xr = reinterpret_cast<const float4 *>(p.X + pt * (int64_t)N_DIM + cb);
 #pragma unroll
@@ -477,7 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (st) {   // its successor into L2
         if (pt + (int)stride < (int)p.M) {
           asm volatile("prefetch.global.L2 [%0];" :: "l"(p.X + (pt + stride) * (int64_t)N_DIM + cb));
-          if (decider) asm volatile("prefetch.global.L2 [%0];" :: "l"(p.t + pt + stride));
+          if (writer) asm volatile("prefetch.global.L2 [%0];" :: "l"(p.t + pt + stride));
         }
       }
       const bool lane_busy = mode == M_ACTIVE || st || (fin && nxt < (int)p.M);
