@@ -5,28 +5,38 @@
 // M_lambda = (A^{-1} + lambda I)^{-1}; (3.4b) shrink_1
 // (P:239-247); (3.4c); stopping rule P:1595-1601.  n = 256, H in {l1, wl1}.
 //
-// What v4 changes against v3 (dense_tc2.cu), all measured in profiles/r01:
+// What v4 changes against v3 (dense_tc2.cu); every choice below was measured (profiles/r01,
+// tools/tcgen05_probe/*):
 //  * a pair-MMA sequence of one iteration (48 x cta_group::2 kind::f16, M=128, N=256, K=16) runs
-//    at 64 cycles per instruction (tcgen05_v4_probe.txt), i.e. 3072 cycles per round for 128
-//    points; v3 spent ~18000 cycles per round because MMA, epilogue, per-slot finalisation and
-//    the global reload of finished slots ran one after the other.
+//    at 64 cycles per instruction, i.e. 3072 cycles per round for 128 points; v3 spent ~18000
+//    cycles per round because MMA, epilogue, per-slot finalisation and the global reload of
+//    finished slots ran one after the other.
 //  * D is triple-buffered in TMEM (3 x 128 columns): MMA r+1 accumulates into D[(r+1) % 3] while
 //    the epilogue of round r reads v^k from D[r % 3] and v^{k-1} from D[(r-1) % 3] (the previous
-//    accumulator doubles as v_prev, so only x and u stay in registers).
+//    accumulator doubles as v_prev); x sits in the last 128 TMEM columns; only u stays in
+//    registers (b = clamp(u), d = u - b are recomputed).
 //  * The contraction index is permuted (K' = pi(c)) so that stage s (0..3) of every epilogue
-//    thread completes the K-block [64 s, 64 s + 64): the MMA warp issues the 12 MMAs of that block
-//    as soon as all 32 warps of the pair have written it (mbarrier stage_ready[s]), i.e. MMA r+1
-//    chases the epilogue of round r stage by stage.
+//    thread completes the K-block [64 s, 64 s + 64): the MMA thread issues the 12 MMAs of that
+//    block as soon as all 32 epilogue warps of the pair have written it (mbarrier stage_ready[s]),
+//    i.e. MMA r+1 chases the epilogue of round r stage by stage.
+//  * A dedicated MMA warp (one thread issues: a tcgen05.mma issue blocks its thread ~200 cycles,
+//    and an elect.sync issue by a converged warp ran the round skeleton 2.5-4x slower) in a fifth
+//    warpgroup; setmaxnreg gives the epilogue 112 registers and the MMA warpgroup 32.
 //  * Per-slot decisions are taken redundantly by the 8 threads that share a point (they read the
-//    same 8 partial sums), so a round has one CTA barrier; a converged point outputs grad and phi
-//    in the following round (using v^{k+1}, reading R23) while its slot's next point is loaded
-//    with plain loads issued before the MMA wait (prefetched to L2 one lifetime earlier).
+//    same 8 partial sums), so the only per-round CTA-level sync is the partial-sum mbarrier; a
+//    converged point outputs grad and phi in the following round (using v^{k+1}, reading R23)
+//    and its slot's next x is loaded at the end of that round (its t one lifetime earlier).
+//  * Remote mbarrier arrives use the default .release.cta semantics (.release.cluster compiled
+//    to MEMBAR.ALL.GPU + ERRBAR and waited for the warp's global stores on every stage).
 //
-// Thread geometry (16 epilogue warps per CTA, warp 16 issues MMAs in the leader CTA):
+// Thread geometry (16 epilogue warps per CTA; warp 16 of the leader CTA issues the MMAs):
 //   warp w < 16: TMEM lane quarter q = w & 3, column group j = w >> 2; point slot
 //   pl = 32 (q & 1) + lane, coordinates c = 128 (q >> 1) + 32 j + [0, 32) ("2x2" layout of the
 //   M = 128 pair MMA, profiles/r01/tcgen05_2sm_probe.txt); stage s handles c0 + 8 s .. + 8.
 //   pi(c) = 64 s + 32 h + 8 j + i for c = 128 h + 32 j + 8 s + i.
+//
+// HOPF_TC3_TRACE (compile flag) + HOPF_TC3_TRACE=<file> (env) record per-round clock64 stamps of
+// CTAs 0/1 (epilogue warps, MMA thread) for the timeline analysis in DESIGN.md.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -50,11 +60,9 @@ constexpr int N_DIM = 256;
 constexpr int PTS = 64;                  // point slots per CTA (128 per pair)
 constexpr int EPI_WARPS = 16;
 constexpr int EPI_THREADS = EPI_WARPS * 32;
-#ifdef HOPF_TC3_NO_SETMAXNREG
-constexpr int THREADS = EPI_THREADS + 32;    // + the MMA warp (96 registers for everyone)
-#else
-constexpr int THREADS = EPI_THREADS + 128;   // + one warpgroup whose first warp issues the MMAs
-#endif
+// + one warpgroup whose first warp issues the MMAs (a lone 17th warp caps everyone at 96
+// registers and measured 8 % slower than setmaxnreg 112/32)
+constexpr int THREADS = EPI_THREADS + 128;
 // setmaxnreg moves registers inside the CTA's own allocation (640 threads x 96 at launch):
 // 16 warps x 112 + 4 warps x 32 = 20 warps x 96 (asking for more never returns)
 constexpr int EPI_REGS = 112, MMA_REGS = 32;
@@ -65,11 +73,9 @@ constexpr int OFF_BH = 65536;            // M_lambda rows hi: 128 x 256 fp16 (64
 constexpr int OFF_BL = 131072;           // M_lambda rows lo
 constexpr int OFF_RED = 196608;          // [2][8 parts][64 slots] float4 (16 KB)
 constexpr int OFF_W = OFF_RED + 2 * PTS * 8 * 16;   // w[256] (wl1)
-constexpr int OFF_CTRL = OFF_W + N_DIM * 4;          // int4 per slot: pt, it, mode, t
-constexpr int OFF_CTRLN = OFF_CTRL + PTS * 16;      // int per slot: next point (FINISH)
-constexpr int OFF_BAR = OFF_CTRLN + PTS * 4;
+constexpr int OFF_BAR = OFF_W + N_DIM * 4;
 // bars: [0] mma_done, [8] term, [16..48) stage_ready[4], [48] busy[2] (int), [56] tmem base,
-//       [64] red_ready, [72] dec_ready, [80] fin (leader: drain before termination)
+//       [64] red_ready (slots 0-31), [72] red_ready (slots 32-63), [80] fin (leader)
 constexpr int SMEM_BYTES = OFF_BAR + 88;
 static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB dynamic shared memory of a CTA");
 
@@ -185,10 +191,6 @@ __device__ __forceinline__ void commit2_elect(uint32_t bar) {
                :: "r"(bar), "h"((uint16_t)3));
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
-#ifdef HOPF_TC3_EXP_NOLD
-  for (int i = 0; i < 8; i++) v[i] = 0.5f * (taddr & 7);
-  return;
-#endif
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
@@ -198,9 +200,6 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; i++) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
-#ifdef HOPF_TC3_EXP_NOST
-  return;
-#endif
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
                :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])),
                   "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])),
@@ -239,7 +238,6 @@ __device__ __forceinline__ void split2(float2 u, uint32_t &hw, uint32_t &lw) {
 __device__ long long *g_tc3_trace = nullptr;
 __device__ long long *g_tc3_trace2 = nullptr;   // [2 CTAs][16 warps][64 rounds][4]: mma, st0, st3, red
 __device__ long long *g_tc3_trace3 = nullptr;   // MMA warp: [64 rounds][8]: stage s observed, issued
-__device__ long long *g_tc3_trace4 = nullptr;   // MMA warp, stage 0: [64 rounds][16]: after each MMA
 #ifndef HOPF_TC3_TR0
 #define HOPF_TC3_TR0 200
 #endif
@@ -257,7 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   volatile int *busy = reinterpret_cast<volatile int *>(bars + 48);
   volatile uint32_t *tmem_slot = reinterpret_cast<volatile uint32_t *>(bars + 56);
   const uint32_t bar_mma = smem_u32(bars), bar_term = smem_u32(bars + 8);
-  const uint32_t bar_stage0 = smem_u32(bars + 16), bar_red = smem_u32(bars + 64), bar_dec = smem_u32(bars + 72), bar_fin = smem_u32(bars + 80);
+  const uint32_t bar_stage0 = smem_u32(bars + 16), bar_red = smem_u32(bars + 64), bar_fin = smem_u32(bars + 80);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
@@ -278,8 +276,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(bar_mma, 1);
     mbar_init(bar_term, 1);
     for (int s = 0; s < 4; s++) mbar_init(bar_stage0 + 8 * s, 2 * EPI_WARPS);
-    mbar_init(bar_red, EPI_WARPS);
-    mbar_init(bar_dec, 2);
+    mbar_init(bar_red, EPI_WARPS / 2);        // slots 0-31: the 8 warps with (warp & 1) == 0
+    mbar_init(bar_red + 8, EPI_WARPS / 2);    // slots 32-63
     mbar_init(bar_fin, 1);
     busy[0] = busy[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -293,12 +291,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   if (warp >= EPI_WARPS) {
     // ================= MMA warpgroup: warp 16 of the leader issues, the others idle =========
-#ifndef HOPF_TC3_NO_SETMAXNREG
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(MMA_REGS));
-#endif
 #ifdef HOPF_TC3_TRACE
     long long *const tr3 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace3 : nullptr;
-    long long *const tr4 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace4 : nullptr;
 #endif
     if (rank == 0 && warp == EPI_WARPS && lane == 0) {
       // one thread issues (an elect.sync form issued by the converged warp ran the round
@@ -311,14 +306,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         int any_busy = 1;
 #pragma unroll 1
         for (int s = 0; s < 4; s++) {
-#ifdef HOPF_TC3_EXP_ACQCL
-          mbar_wait_cluster(bar_stage0 + 8 * s, r & 1);
-#else
           // CTA-scope wait, as CUTLASS's MMA warps do for their operand-full barriers (the
           // remote arrives are default .release.cta; the tensor core reads the peer's shared
           // memory through the async proxy after the writers' fence.proxy.async)
           mbar_wait_hint(bar_stage0 + 8 * s, r & 1);
-#endif
 #ifdef HOPF_TC3_TRACE
           if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s] = clock64();
 #endif
@@ -357,9 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
     __syncwarp();
   } else {
-#ifndef HOPF_TC3_NO_SETMAXNREG
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(EPI_REGS));
-#endif
     // ================= epilogue warps =======================================================
     const int q = warp & 3, j = warp >> 2;
     const int pl = 32 * (q & 1) + lane;           // local point slot
@@ -433,7 +422,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         advance(dpt, q, tq);
         begin(q, tq, M_START_LD);
       } else {
-        if (lane == 0) mbar_wait_hint(bar_red, (r - 1) & 1);
+        if (lane == 0) mbar_wait_hint(bar_red + 8 * (q & 1), (r - 1) & 1);
         __syncwarp();
         tmark(r, 12);
         float s4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -525,7 +514,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
 #pragma unroll
       for (int s = 0; s < 4; s++) {
-#ifndef HOPF_TC3_EXP_EMPTY
         if (SCALED) {
 #pragma unroll
           for (int e = 0; e < 8; e++) { va[e] *= mscale_inv; vpa[e] *= mscale_inv; }
@@ -604,10 +592,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const uint32_t off = kmaj(pl, 64 * s + 32 * h + 8 * j);
         *reinterpret_cast<uint4 *>(smem + OFF_UH + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         *reinterpret_cast<uint4 *>(smem + OFF_UL + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-#endif
-#ifndef HOPF_TC3_NOFENCE_EXPERIMENT
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
         if (any_st) asm volatile("tcgen05.wait::st.sync.aligned;");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
@@ -626,7 +611,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         *wp = make_float4(asd.x + asd.y, asb.x + asb.y, asv.x + asv.y, aph);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_local(bar_red);
+      if (lane == 0) mbar_arrive_local(bar_red + 8 * (q & 1));
       tmark(r, 7);
       tmark2(r, 3);
       if (fin && nxt < (int)p.M) {   // the next point of a finished slot: x into us now (START next round)
@@ -698,7 +683,7 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
 #else
   const char *trace_path = nullptr;
 #endif
-  long long *dtrace = nullptr, *dtrace2 = nullptr, *dtrace3 = nullptr, *dtrace4 = nullptr;
+  long long *dtrace = nullptr, *dtrace2 = nullptr, *dtrace3 = nullptr;
   if (trace_path) {
     cudaMalloc(&dtrace, 4 * 64 * 16 * sizeof(long long));
     cudaMemset(dtrace, 0, 4 * 64 * 16 * sizeof(long long));
@@ -710,9 +695,6 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
     cudaMalloc(&dtrace3, 64 * 8 * sizeof(long long));
     cudaMemset(dtrace3, 0, 64 * 8 * sizeof(long long));
     cudaMemcpyToSymbol(tc3::g_tc3_trace3, &dtrace3, sizeof(dtrace3));
-    cudaMalloc(&dtrace4, 64 * 16 * sizeof(long long));
-    cudaMemset(dtrace4, 0, 64 * 16 * sizeof(long long));
-    cudaMemcpyToSymbol(tc3::g_tc3_trace4, &dtrace4, sizeof(dtrace4));
 #endif
   }
   fn<<<(unsigned)(2 * pairs), tc3::THREADS, tc3::SMEM_BYTES, stream>>>(
@@ -751,18 +733,6 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
       fclose(f);
     }
     cudaFree(dtrace3);
-    cudaMemcpyToSymbol(tc3::g_tc3_trace4, &z, sizeof(z));
-    std::vector<long long> h4(64 * 16);
-    cudaMemcpy(h4.data(), dtrace4, h4.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-    std::string p4 = std::string(trace_path) + ".mma0";
-    if (FILE *f = fopen(p4.c_str(), "w")) {
-      for (size_t i = 0; i < h4.size(); i += 16) {
-        for (int e = 0; e < 8; e++) fprintf(f, "%lld ", h4[i + e]);
-        fprintf(f, "\n");
-      }
-      fclose(f);
-    }
-    cudaFree(dtrace4);
 #endif
     cudaFree(dtrace);
   }
