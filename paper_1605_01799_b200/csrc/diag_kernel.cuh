@@ -28,6 +28,7 @@
 //   test:  ||v - v_prev||^2, ||d' - d||^2, ||d' - v||^2 = ||b - b'||^2  <= tol
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace hopf {
@@ -294,37 +295,51 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     float2 a0 = splat2(0.f), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0, r0 = a0, r1 = a0;
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
     const float live = waiting ? 0.f : 1.f;
+    // l2: ||d^k - d^{k-1}||^2 and ||d^k - v^k||^2 only matter when ||v^k - v^{k-1}||^2 <= tol
+    // (sv_ok, known before the trip): trips in which no group of the warp has sv_ok skip both
+    // sums (10 instead of 13 packed ops per coordinate pair); the stopping decisions are the
+    // paper's exactly (a group without sv_ok cannot stop at k whatever the other two sums are).
+    const bool full_test = (HK != HK_L2) || __any_sync(0xffffffffu, sv_ok);
+    auto trip = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int q = 0; q < NP; q++) {
-      const float2 kq = KSM ? lds_volatile2(kap_s + q * G + gl) : kap[q];
-      if (HK == HK_L2) {
-        // d[q] = -d_{k-1}, kq = -kappa
-        const float2 dd = fma2(sP, b[q], d[q]);        // d_k - d_{k-1}, d_k = s_k u_k (3.4b)
-        d[q] = fma2(dd, splat2(-live), d[q]);          // -d_k (frozen while waiting)
-        const float2 dmv = add2(d[q], v[q]);           // v^k - d^k
-        b[q] = add2(b[q], d[q]);                       // (3.4c): b_k = u_k - d_k
-        const float2 na = add2(d[q], b[q]);            // -(d_k - b_k)
-        const float2 t = sub2(xh[q], v[q]);
-        const float2 dv = fma2(kq, na, t);             // (3.4a): v_{k+1} - v_k
-        v[q] = add2(v[q], dv);                         // v_{k+1}
-        b[q] = add2(v[q], b[q]);                       // u_{k+1} = v_{k+1} + b_k
-        if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
-        else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
-      } else {
-        const float2 a = sub2(d[q], b[q]);
-        const float2 t = sub2(xh[q], v[q]);
-        const float2 dv = fma2(kq, a, t);              // (3.4a): v^k - v^{k-1}
-        v[q] = add2(v[q], dv);                         // v^k
-        const float2 u = add2(v[q], b[q]);
-        b[q] = clamp2(u, HK == HK_WL1 ? tau[q] : tP);  // projection on [-tau, tau] (Moreau)
-        const float2 dn = sub2(u, b[q]);               // (3.4b) shrink_1; b^k = u - d^k
-        const float2 dd = sub2(dn, d[q]);
-        d[q] = fma2(dd, splat2(live), d[q]);           // d^k (exact zeros kept; frozen while waiting)
-        const float2 dmv = sub2(d[q], v[q]);           // d^k - v^k
-        if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); }
-        else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); }
+      for (int q = 0; q < NP; q++) {
+        const float2 kq = KSM ? lds_volatile2(kap_s + q * G + gl) : kap[q];
+        if (HK == HK_L2) {
+          // d[q] = -d_{k-1}, kq = -kappa
+          const float2 dd = fma2(sP, b[q], d[q]);        // d_k - d_{k-1}, d_k = s_k u_k (3.4b)
+          d[q] = fma2(dd, splat2(-live), d[q]);          // -d_k (frozen while waiting)
+          b[q] = add2(b[q], d[q]);                       // (3.4c): b_k = u_k - d_k
+          const float2 na = add2(d[q], b[q]);            // -(d_k - b_k)
+          const float2 t = sub2(xh[q], v[q]);
+          const float2 dv = fma2(kq, na, t);             // (3.4a): v_{k+1} - v_k
+          if (FULL) {
+            const float2 dmv = add2(d[q], v[q]);         // v^k - d^k
+            if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); }
+            else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); }
+          }
+          v[q] = add2(v[q], dv);                         // v_{k+1}
+          b[q] = add2(v[q], b[q]);                       // u_{k+1} = v_{k+1} + b_k
+          if (q & 1) { c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
+          else       { c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
+        } else {
+          const float2 a = sub2(d[q], b[q]);
+          const float2 t = sub2(xh[q], v[q]);
+          const float2 dv = fma2(kq, a, t);              // (3.4a): v^k - v^{k-1}
+          v[q] = add2(v[q], dv);                         // v^k
+          const float2 u = add2(v[q], b[q]);
+          b[q] = clamp2(u, HK == HK_WL1 ? tau[q] : tP);  // projection on [-tau, tau] (Moreau)
+          const float2 dn = sub2(u, b[q]);               // (3.4b) shrink_1; b^k = u - d^k
+          const float2 dd = sub2(dn, d[q]);
+          d[q] = fma2(dd, splat2(live), d[q]);           // d^k (exact zeros kept; frozen while waiting)
+          const float2 dmv = sub2(d[q], v[q]);           // d^k - v^k
+          if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); }
+          else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); }
+        }
       }
-    }
+    };
+    if (full_test) trip(std::true_type{});
+    else trip(std::false_type{});
     const float psd = (a0.x + a0.y) + (a1.x + a1.y), psb = (b0.x + b0.y) + (b1.x + b1.y);
     const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
     bool conv;
