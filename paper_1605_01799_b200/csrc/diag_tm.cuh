@@ -1,0 +1,324 @@
+// diag_tm.cuh — K1/K2 for wide points (n in (512, 1024], one warp per point) with tensor memory
+// as an extension of the register file.  sm_100a, FP32 SIMT; no MMA is involved.
+//
+// Same method and arithmetic as hopf_diag_kernel<32, 32, HK, false> (diag_kernel.cuh): split
+// Bregman (3.4a)-(3.4c) with the paper's stopping rule, shrink_1
+// / shrink_2, phi = (3.3) at d (reading R2).  Only the storage differs:
+//
+//   registers : d, b (u between l2 trips) — 2 x 32 floats per lane
+//   TMEM      : x_hat (columns 0-31), v (32-63), -kappa / kappa (64-95), tau_i (96-127, wl1)
+//
+// The register kernel keeps x_hat, d, b, v resident (128 of its 168 registers), which limits it
+// to 3 warps per SM sub-partition; with two vectors moved to TMEM this one runs at <= 128
+// registers, i.e. 4 warps per sub-partition (4 CTAs of 128 threads per SM, 128 TMEM columns
+// each = the SM's 512).  Warp w of a CTA owns TMEM lanes 32 (w % 4) + lane, so each thread's
+// 32 slot values of a vector are one 32x32b row of 32 columns, moved in x8 chunks per trip.
+#pragma once
+#include <cfloat>
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+#include "diag_kernel.cuh"
+
+namespace hopf {
+namespace dtm {
+
+constexpr int CPL = 32, NP = 16, THREADS = 128, TMEM_COLS = 128;
+constexpr int DYN_SMEM = 48 * 1024;   // caps residency at 4 CTAs per SM (4 x 128 TMEM columns)
+
+__device__ __forceinline__ void ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; i++) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void st8(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])),
+                  "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])),
+                  "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
+}
+// wait for this thread's outstanding tcgen05.ld, naming the destination registers so the
+// compiler does not read them before the wait
+template <int N>
+__device__ __forceinline__ void wait_ld(float (&a)[N][8]) {
+  static_assert(N >= 2 && N <= 4, "2..4 chunks");
+  if constexpr (N == 2)
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(a[0][0]), "+f"(a[0][1]), "+f"(a[0][2]), "+f"(a[0][3]), "+f"(a[0][4]), "+f"(a[0][5]), "+f"(a[0][6]), "+f"(a[0][7]),
+                   "+f"(a[1][0]), "+f"(a[1][1]), "+f"(a[1][2]), "+f"(a[1][3]), "+f"(a[1][4]), "+f"(a[1][5]), "+f"(a[1][6]), "+f"(a[1][7])
+                 :: "memory");
+  else if constexpr (N == 3)
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(a[0][0]), "+f"(a[0][1]), "+f"(a[0][2]), "+f"(a[0][3]), "+f"(a[0][4]), "+f"(a[0][5]), "+f"(a[0][6]), "+f"(a[0][7]),
+                   "+f"(a[1][0]), "+f"(a[1][1]), "+f"(a[1][2]), "+f"(a[1][3]), "+f"(a[1][4]), "+f"(a[1][5]), "+f"(a[1][6]), "+f"(a[1][7]),
+                   "+f"(a[2][0]), "+f"(a[2][1]), "+f"(a[2][2]), "+f"(a[2][3]), "+f"(a[2][4]), "+f"(a[2][5]), "+f"(a[2][6]), "+f"(a[2][7])
+                 :: "memory");
+  else
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(a[0][0]), "+f"(a[0][1]), "+f"(a[0][2]), "+f"(a[0][3]), "+f"(a[0][4]), "+f"(a[0][5]), "+f"(a[0][6]), "+f"(a[0][7]),
+                   "+f"(a[1][0]), "+f"(a[1][1]), "+f"(a[1][2]), "+f"(a[1][3]), "+f"(a[1][4]), "+f"(a[1][5]), "+f"(a[1][6]), "+f"(a[1][7]),
+                   "+f"(a[2][0]), "+f"(a[2][1]), "+f"(a[2][2]), "+f"(a[2][3]), "+f"(a[2][4]), "+f"(a[2][5]), "+f"(a[2][6]), "+f"(a[2][7]),
+                   "+f"(a[3][0]), "+f"(a[3][1]), "+f"(a[3][2]), "+f"(a[3][3]), "+f"(a[3][4]), "+f"(a[3][5]), "+f"(a[3][6]), "+f"(a[3][7])
+                 :: "memory");
+}
+
+template <int HK>
+__global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagParams p) {
+  extern __shared__ __align__(16) uint8_t dyn_smem[];   // unused: residency cap only
+  __shared__ uint32_t tmem_slot;
+  constexpr int G = 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gl = lane;
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int n = p.n;
+  const float lam = p.lambda, tol = p.tol;
+  const int jmax = (n - gl + G - 1) / G;   // slots j < jmax are real coordinates
+  (void)dyn_smem;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_slot)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tl0 = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16);
+  const uint32_t T_XH = tl0, T_V = tl0 + 32, T_K = tl0 + 64, T_TAU = tl0 + 96;
+
+  // kappa (l2: -kappa) of this lane's slots -> TMEM, once
+  const float ksign = (HK == HK_L2) ? -1.f : 1.f;
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    float kv[8];
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+      const int j = 8 * c + e, i = gl + G * j;
+      kv[e] = (j < jmax) ? ksign * __fdividef(lam, __ldg(p.D + i) + lam) : 0.f;
+    }
+    st8(T_K + 8 * c, kv);
+  }
+
+  float2 d[NP], b[NP];
+  int64_t pt = gid;
+  bool have = pt < p.M;
+  int it = 0;
+  float tt = 0.f, tauS = 0.f;
+  int spec = 0;
+  float s_cur = 1.f;
+  bool sv_ok = false;
+
+  // load the point and set up the solve: x_hat, v -> TMEM; d, b -> registers (reading R5).
+  // All global loads are issued first (x into d, D into b: both are dead at this point), so
+  // their latency overlaps instead of being paid per TMEM chunk.
+  auto start_point = [&](bool active) {
+    bool bad = false;
+    if (active) {
+      tt = __ldg(p.t + pt);
+      bad = !(tt >= 0.f) || !finite_f(tt);
+    }
+    const float *xrow = p.X + (active ? pt : 0) * (int64_t)n;
+#pragma unroll
+    for (int q = 0; q < NP; q++) {
+      const int j0 = 2 * q, j1 = 2 * q + 1;
+      const bool ok0 = active && j0 < jmax, ok1 = active && j1 < jmax;
+      d[q] = make_float2(ok0 ? __ldg(xrow + gl + G * j0) : 0.f, ok1 ? __ldg(xrow + gl + G * j1) : 0.f);
+      b[q] = make_float2(ok0 ? __ldg(p.D + gl + G * j0) : 1.f, ok1 ? __ldg(p.D + gl + G * j1) : 1.f);
+    }
+    if (p.c) {
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const int j0 = 2 * q, j1 = 2 * q + 1;
+        const bool ok0 = active && j0 < jmax, ok1 = active && j1 < jmax;
+        d[q].x -= ok0 ? __ldg(p.c + gl + G * j0) : 0.f;
+        d[q].y -= ok1 ? __ldg(p.c + gl + G * j1) : 0.f;
+      }
+    }
+    const float tl = tt / lam;
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      float xh8[8], v8[8], tau8[8];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const int j = 8 * c + e;
+        const float2 xq = d[4 * c + (e >> 1)], Dq = b[4 * c + (e >> 1)];
+        const float xt = (e & 1) ? xq.y : xq.x;        // x - c (0 on padded slots)
+        const float Dv = (e & 1) ? Dq.y : Dq.x;
+        bad |= !finite_f(xt);
+        const float di = __fdividef(1.f, Dv + lam);
+        xh8[e] = xt * di;
+        v8[e] = xt;                                     // v^0 = x - c
+        if (HK == HK_WL1) tau8[e] = (active && j < jmax) ? tl * __ldg(p.w + gl + G * j) : 0.f;
+      }
+      st8(T_XH + 8 * c, xh8);
+      st8(T_V + 8 * c, v8);
+      if (HK == HK_WL1) st8(T_TAU + 8 * c, tau8);
+    }
+#pragma unroll
+    for (int q = 0; q < NP; q++) {
+      const float2 xt = d[q];
+      if (HK == HK_L2) { d[q] = make_float2(-xt.x, -xt.y); b[q] = xt; }   // -d^0, pending u
+      else { b[q] = splat2(0.f); }                                        // d^0 = x - c, b^0 = 0
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    bad = __any_sync(0xffffffffu, bad);
+    if (active) {
+      spec = bad ? 2 : (tt == 0.f ? 1 : 0);
+      tauS = tt / lam;
+    }
+    it = 0;
+    s_cur = 1.f;
+    sv_ok = false;
+  };
+  start_point(have);
+
+  while (have) {   // one point per warp: `have` is warp-uniform
+    float2 a0 = splat2(0.f), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0, r0 = a0, r1 = a0;
+    const float2 sP = splat2(s_cur), tP = splat2(tauS);
+    const bool full_test = (HK != HK_L2) || sv_ok;   // see hopf_diag_kernel: exact
+    auto trip = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        float ch[(HK == HK_WL1) ? 4 : 3][8];   // kappa, x_hat, v (, tau)
+        ld8(T_K + 8 * c, ch[0]);
+        ld8(T_XH + 8 * c, ch[1]);
+        ld8(T_V + 8 * c, ch[2]);
+        if constexpr (HK == HK_WL1) ld8(T_TAU + 8 * c, ch[3]);
+        wait_ld(ch);
+#pragma unroll
+        for (int e2 = 0; e2 < 4; e2++) {
+          const int q = 4 * c + e2;
+          const float2 kq = make_float2(ch[0][2 * e2], ch[0][2 * e2 + 1]);
+          const float2 xh = make_float2(ch[1][2 * e2], ch[1][2 * e2 + 1]);
+          float2 v = make_float2(ch[2][2 * e2], ch[2][2 * e2 + 1]);
+          if (HK == HK_L2) {
+            // d[q] = -d_{k-1}, kq = -kappa, b[q] = u_k
+            const float2 dd = fma2(sP, b[q], d[q]);                 // d_k - d_{k-1}, d_k = s_k u_k
+            d[q] = sub2(d[q], dd);                                  // -d_k (as the register kernel)
+            b[q] = add2(b[q], d[q]);                                // (3.4c): b_k = u_k - d_k
+            const float2 na = add2(d[q], b[q]);                     // -(d_k - b_k)
+            const float2 t = sub2(xh, v);
+            const float2 dv = fma2(kq, na, t);                      // (3.4a): v_{k+1} - v_k
+            if (FULL) {
+              const float2 dmv = add2(d[q], v);                     // v^k - d^k
+              if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); }
+              else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); }
+            }
+            v = add2(v, dv);                                        // v_{k+1}
+            b[q] = add2(v, b[q]);                                   // u_{k+1} = v_{k+1} + b_k
+            if (q & 1) { c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
+            else       { c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
+          } else {
+            const float2 a = sub2(d[q], b[q]);
+            const float2 t = sub2(xh, v);
+            const float2 dv = fma2(kq, a, t);                       // (3.4a): v^k - v^{k-1}
+            v = add2(v, dv);                                        // v^k
+            const float2 u = add2(v, b[q]);
+            const float2 tq = (HK == HK_WL1) ? make_float2(ch[HK == HK_WL1 ? 3 : 0][2 * e2], ch[HK == HK_WL1 ? 3 : 0][2 * e2 + 1]) : tP;
+            b[q] = clamp2(u, tq);                                   // projection (Moreau)
+            const float2 dn = sub2(u, b[q]);                        // (3.4b) shrink_1
+            const float2 dd = sub2(dn, d[q]);
+            d[q] = add2(d[q], dd);                                  // d^k (as the register kernel)
+            const float2 dmv = sub2(d[q], v);                       // d^k - v^k
+            if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); }
+            else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); }
+          }
+          ch[2][2 * e2] = v.x;
+          ch[2][2 * e2 + 1] = v.y;
+        }
+        st8(T_V + 8 * c, ch[2]);
+      }
+    };
+    if (full_test) trip(std::true_type{});
+    else trip(std::false_type{});
+
+    const float psd = (a0.x + a0.y) + (a1.x + a1.y), psb = (b0.x + b0.y) + (b1.x + b1.y);
+    const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
+    bool conv;
+    int kdone;
+    {
+      float r2;
+      bool ok_sd, ok_sb, ok_sv;
+      group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
+      if (HK == HK_L2) {
+        kdone = it;
+        conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it
+        sv_ok = ok_sv;
+        const float r = sqrtf(r2);
+        s_cur = (r > tauS) ? (r - tauS) / r : 0.f;     // shrink_2 factor of k+1
+        it++;
+      } else {
+        it++;
+        kdone = it;
+        conv = ok_sd && ok_sb && ok_sv;
+      }
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    if (!(spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)))) continue;
+    const int wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -p.max_iter));
+
+    // ---- finalize: phi = <x - c, d> - 1/2 <d, D d> - t H(d) + gamma ((3.3) at d, R2); grad ----
+    // t == 0: phi = J(x), grad = D^{-1}(x - c) (reading R6); invalid input: NaN (R6)
+    float qs = 0.f, hsum = 0.f;
+    float *grow = p.grad + pt * (int64_t)n;
+#pragma unroll
+    for (int q = 0; q < NP; q++) {   // D of this lane's slots into b (dead), loads in flight together
+      const int j0 = 2 * q, j1 = 2 * q + 1;
+      b[q] = make_float2(j0 < jmax ? __ldg(p.D + gl + G * j0) : 1.f, j1 < jmax ? __ldg(p.D + gl + G * j1) : 1.f);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      float xh8[2][8];
+      ld8(T_XH + 8 * c, xh8[0]);
+      ld8(T_XH + 8 * c, xh8[1]);
+      wait_ld(xh8);
+      float g8[8];
+#pragma unroll
+      for (int e = 0; e < 8; e++) {
+        const int j = 8 * c + e, i = gl + G * j;
+        const bool ok = j < jmax;
+        const float2 dqq = d[4 * c + (e >> 1)], Dq = b[4 * c + (e >> 1)];
+        float dq = (e & 1) ? dqq.y : dqq.x;
+        if (HK == HK_L2) dq = 0.f - dq;
+        const float Dv = (e & 1) ? Dq.y : Dq.x;
+        const float xt = xh8[0][e] * (Dv + lam);
+        if (spec == 1) {
+          dq = ok ? __fdividef(xt, Dv) : 0.f;
+          qs = fmaf(0.5f * xt, dq, qs);
+        } else if (ok) {
+          qs = fmaf(xt, dq, qs);
+          qs = fmaf(-0.5f * Dv * dq, dq, qs);
+          if (HK == HK_L2) hsum = fmaf(dq, dq, hsum);
+          else if (HK == HK_WL1) hsum = fmaf(__ldg(p.w + i), fabsf(dq), hsum);
+          else hsum += fabsf(dq);
+        }
+        g8[e] = (spec == 2) ? __int_as_float(0x7fc00000) : dq;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; e++)
+        if (8 * c + e < jmax) grow[gl + G * (8 * c + e)] = g8[e];
+    }
+    qs = group_sum<G>(qs);
+    hsum = group_sum<G>(hsum);
+    float phiv = (spec == 1) ? qs + p.gamma : qs - tt * (HK == HK_L2 ? sqrtf(hsum) : hsum) + p.gamma;
+    if (spec == 2) phiv = __int_as_float(0x7fc00000);
+    if (gl == 0) { p.phi[pt] = phiv; p.iters[pt] = wstatus; }
+    pt += ngroups;
+    have = pt < p.M;
+    if (have) start_point(true);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_slot), "r"(TMEM_COLS));
+}
+
+}  // namespace dtm
+}  // namespace hopf

@@ -13,6 +13,7 @@
 #include "../../include/hopf.h"
 #include "common.cuh"
 #include "diag_kernel.cuh"
+#include "diag_tm.cuh"
 
 namespace hopf {
 
@@ -85,10 +86,35 @@ static const Variant *pick_variant(int n, bool is_union) {
   return nullptr;
 }
 
+// Wide points (the (32, 32) variant, n in (512, 1024]), not union: the kernel that keeps x_hat,
+// v, kappa (and tau) in tensor memory (diag_tm.cuh).  HOPF_DIAG_TM=0 selects the register kernel.
+static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t stream) {
+  using namespace dtm;
+  KernFn fn = h == HOPF_H_L2 ? hopf_diag_tm_kernel<HK_L2>
+              : (h == HOPF_H_WL1 ? hopf_diag_tm_kernel<HK_WL1> : hopf_diag_tm_kernel<HK_L1>);
+  static bool attr_done[3] = {false, false, false};
+  if (!attr_done[(int)h]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_SMEM);
+    attr_done[(int)h] = true;
+  }
+  int64_t blocks = (int64_t)num_sms() * 4;
+  const int64_t need = (p.M + 3) / 4;   // 4 points (warps) per block
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  fn<<<(unsigned)blocks, THREADS, DYN_SMEM, stream>>>(p);
+  g_launches += 1;
+  g_last_threads = THREADS;
+  g_last_blocks = (int)blocks;
+  return check_launch("hopf_diag_tm_kernel");
+}
+
 static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
                             cudaStream_t stream) {
   const Variant *v = pick_variant(p.n, is_union);
   if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
+  static const char *tm_env = getenv("HOPF_DIAG_TM");
+  if (!is_union && v->G == 32 && v->CPL == 32 && !(tm_env && strcmp(tm_env, "0") == 0))
+    return launch_diag_tm(p, h, stream);
   KernFn fn = v->fn[(int)h][is_union ? 1 : 0];
   // Block size: the one that keeps the most warps resident per SM (register-limited kernels
   // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
