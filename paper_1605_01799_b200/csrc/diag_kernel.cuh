@@ -352,8 +352,9 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
         kdone = it;
         conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it
         sv_ok = ok_sv;                                  // ||v^{k+1} - v^k||^2 <= tol, next trip
-        const float r = sqrtf(r2);
-        s_cur = (r > tauS) ? (r - tauS) / r : 0.f;     // shrink_2 factor of k+1
+        // shrink_2 factor of k+1, max(||u|| - tau, 0) / ||u|| = 1 - tau / ||u||,
+        // with the hardware reciprocal square root (reading R20)
+        s_cur = (r2 > tauS * tauS) ? fmaf(-tauS, rsqrtf(r2), 1.f) : 0.f;
         it++;
       } else {
         it++;

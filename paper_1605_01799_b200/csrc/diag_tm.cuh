@@ -251,8 +251,9 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         kdone = it;
         conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it
         sv_ok = ok_sv;
-        const float r = sqrtf(r2);
-        s_cur = (r > tauS) ? (r - tauS) / r : 0.f;     // shrink_2 factor of k+1
+        // shrink_2 factor of k+1, max(||u|| - tau, 0) / ||u|| = 1 - tau / ||u||,
+        // with the hardware reciprocal square root (reading R20)
+        s_cur = (r2 > tauS * tauS) ? fmaf(-tauS, rsqrtf(r2), 1.f) : 0.f;
         it++;
       } else {
         it++;
