@@ -8,6 +8,10 @@
 //   registers : d, b (u between l2 trips) — 2 x 32 floats per lane
 //   TMEM      : x_hat (columns 0-31), v (32-63), -kappa / kappa (64-95), tau_i (96-127, wl1)
 //
+// Because v is reloaded every trip, (3.4a) is formed directly as v^{k+1} = x_hat - kappa (d - b)
+// (one FFMA; the register kernel updates v in place: v + ((x_hat - v) - kappa (d - b))), so an
+// l2 trip far from convergence costs 9 packed FP32 ops per coordinate pair.
+//
 // The register kernel keeps x_hat, d, b, v resident (128 of its 168 registers), which limits it
 // to 3 warps per SM sub-partition; with two vectors moved to TMEM this one runs at <= 128
 // registers, i.e. 4 warps per sub-partition (4 CTAs of 128 threads per SM, 128 TMEM columns
@@ -201,25 +205,25 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
           if (HK == HK_L2) {
             // d[q] = -d_{k-1}, kq = -kappa, b[q] = u_k
             const float2 dd = fma2(sP, b[q], d[q]);                 // d_k - d_{k-1}, d_k = s_k u_k
-            d[q] = sub2(d[q], dd);                                  // -d_k (as the register kernel)
+            d[q] = sub2(d[q], dd);                                  // -d_k
             b[q] = add2(b[q], d[q]);                                // (3.4c): b_k = u_k - d_k
             const float2 na = add2(d[q], b[q]);                     // -(d_k - b_k)
-            const float2 t = sub2(xh, v);
-            const float2 dv = fma2(kq, na, t);                      // (3.4a): v_{k+1} - v_k
+            const float2 vn = fma2(kq, na, xh);                     // (3.4a): v_{k+1}
+            const float2 dv = sub2(vn, v);                          // v_{k+1} - v_k
             if (FULL) {
               const float2 dmv = add2(d[q], v);                     // v^k - d^k
               if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); }
               else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); }
             }
-            v = add2(v, dv);                                        // v_{k+1}
+            v = vn;
             b[q] = add2(v, b[q]);                                   // u_{k+1} = v_{k+1} + b_k
             if (q & 1) { c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
             else       { c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
           } else {
             const float2 a = sub2(d[q], b[q]);
-            const float2 t = sub2(xh, v);
-            const float2 dv = fma2(kq, a, t);                       // (3.4a): v^k - v^{k-1}
-            v = add2(v, dv);                                        // v^k
+            const float2 vn = fma2(kq, a, xh);                      // (3.4a): v^k
+            const float2 dv = sub2(vn, v);                          // v^k - v^{k-1}
+            v = vn;
             const float2 u = add2(v, b[q]);
             const float2 tq = (HK == HK_WL1) ? make_float2(ch[HK == HK_WL1 ? 3 : 0][2 * e2], ch[HK == HK_WL1 ? 3 : 0][2 * e2 + 1]) : tP;
             b[q] = clamp2(u, tq);                                   // projection (Moreau)
