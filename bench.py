@@ -243,6 +243,7 @@ def main():
     torch.cuda.synchronize(dev)
     iters_np = iters.cpu().numpy()
     launches_per_step = hb.last_launch_count()
+    kernel_name = hb.last_kernel()
     import ctypes
     _th, _bl = ctypes.c_int32(0), ctypes.c_int32(0)
     L.hopf_last_launch_config(ctypes.byref(_th), ctypes.byref(_bl))
@@ -274,6 +275,30 @@ def main():
         ms_total = float(tm.item())
     ms_step = ms_total / args.steps
     value = M * ws / (ms_step / 1e3)
+
+    # ---- result gather over NCCL (N > 1): the method's only collective -------------
+    gather = None
+    if ws > 1:
+        def timed(fn, reps=3):
+            fn()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            for _ in range(reps):
+                fn()
+            g1.record(stream)
+            torch.cuda.synchronize(dev)
+            tm = torch.tensor([g0.elapsed_time(g1) / reps], device=dev, dtype=torch.float64)
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            return float(tm.item())
+        ms_small = timed(lambda: shard.gather_results([phi, iters]))
+        ms_grad = timed(lambda: shard.gather_results([grad]))
+        gbytes = grad.numel() * 4 * ws
+        gather = {"what": "all_gather of every rank's results (NCCL), outside the timed step",
+                  "phi_iters_ms": ms_small, "grad_ms": ms_grad,
+                  "grad_bytes_gathered": gbytes,
+                  "grad_GBps_per_rank_in": gbytes * (ws - 1) / ws / (ms_grad / 1e3) / 1e9}
 
     # ---- end to end through the host-buffer entry point (diag path) ----------------------------
     e2e = None
@@ -321,7 +346,8 @@ def main():
         flops = it_sum * n * FLOPS_PER_COORD_ITER[wl.h]
         achieved = flops / (ms_step / 1e3) / 1e12
         peak = sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        roof = {"kernel": kernel_name, "bound": "alu", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": load_traffic(wl.name),
                 "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (guide unit "
                               "counts, max SM clock)",
@@ -342,7 +368,8 @@ def main():
         tc = (n == 256 and wl.h != "l2")
         bf16 = float(peaks.get("bf16_tflops", 1645.3))
         peak = bf16 if tc else sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
-        roof = {"bound": "tensor" if tc else "alu", "achieved": achieved, "peak": peak,
+        roof = {"kernel": kernel_name, "bound": "tensor" if tc else "alu", "achieved": achieved,
+                "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(wl.name),
                 "peak_basis": ("measured dense bf16 cuBLAS burst (MEASURED_PEAKS.json); fp16 "
                                "kind::f16 runs at the bf16 rate") if tc else "FP32 SIMT peak",
@@ -363,7 +390,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded; BASELINE config law)", "config": config_dict(wl, ws),
-            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gather": gather,
             "gpu_launches": launches_per_step * args.steps,
             "launch": launch_cfg if wl.kind != "dense" else None,
             "iters": {"min": int(conv.min()) if conv.size else None,

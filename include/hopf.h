@@ -133,6 +133,10 @@ int32_t hopf_last_launch_count(void);
  * blocks); returns hopf_last_launch_count().  Either pointer may be NULL. */
 int32_t hopf_last_launch_config(int32_t *threads_per_block, int32_t *blocks);
 
+/* Name of the main kernel the most recent successful call launched on this thread (static
+ * string, "" if none), e.g. "hopf_diag_tm_kernel<l2>"; for benchmarks and profiles. */
+const char *hopf_last_kernel(void);
+
 /* Text of the most recent error on this thread ("" if none) and a static string for a code. */
 const char *hopf_last_error(void);
 const char *hopf_strerror(int code);

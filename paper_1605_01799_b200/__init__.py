@@ -53,6 +53,7 @@ def lib():
         L.hopf_strerror.restype = ctypes.c_char_p
         L.hopf_strerror.argtypes = [ctypes.c_int]
         L.hopf_last_launch_count.restype = ctypes.c_int32
+        L.hopf_last_kernel.restype = ctypes.c_char_p
         L.hopf_last_launch_config.restype = ctypes.c_int32
         L.hopf_last_launch_config.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
         L.hopf_version.restype = ctypes.c_int32
@@ -65,6 +66,11 @@ def _check(rc: int, where: str):
         L = lib()
         raise HopfError(rc, where, (L.hopf_last_error() or b"").decode() or
                         L.hopf_strerror(rc).decode())
+
+
+def last_kernel() -> str:
+    """Name of the main kernel the most recent call launched on this thread."""
+    return (lib().hopf_last_kernel() or b"").decode()
 
 
 def last_launch_count() -> int:

@@ -9,6 +9,7 @@
 namespace hopf {
 extern thread_local std::string g_last_error;
 extern thread_local int32_t g_launches;
+extern thread_local const char *g_last_kernel;
 int set_error(int code, const char *fmt, ...);
 int check_launch(const char *what);
 int num_sms();

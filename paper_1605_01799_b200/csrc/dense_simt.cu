@@ -303,6 +303,7 @@ int launch_nw(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream
   if (!p.idx && blocks > need) blocks = need;
   fn<<<(unsigned)blocks, NT, smem, stream>>>(p, plan.Ml, plan.Ainv, plan.A);
   g_launches += 1;
+  g_last_kernel = "hopf_dense_simt_kernel";
   return check_launch("hopf_dense_simt_kernel");
 }
 }  // namespace
@@ -348,7 +349,10 @@ int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t 
   DenseParams q = p;
   q.idx = plan.fix + 1;
   q.idx_count = plan.fix;
-  return launch_simt(q, hk, plan, stream);
+  rc = launch_simt(q, hk, plan, stream);
+  g_last_kernel = (sel && strcmp(sel, "tc1") == 0) ? "hopf_dense_tc_kernel"
+                  : (sel && strcmp(sel, "tc2") == 0) ? "hopf_dense_tc2_kernel" : "hopf_dense_tc3_kernel";
+  return rc;
 }
 
 }  // namespace hopf

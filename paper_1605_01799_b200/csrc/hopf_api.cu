@@ -20,6 +20,7 @@ namespace hopf {
 thread_local std::string g_last_error;
 thread_local int32_t g_launches = 0;
 thread_local int32_t g_last_threads = 0, g_last_blocks = 0;
+thread_local const char *g_last_kernel = "";
 
 int set_error(int code, const char *fmt, ...) {
   char buf[512];
@@ -105,6 +106,8 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
   g_launches += 1;
   g_last_threads = THREADS;
   g_last_blocks = (int)blocks;
+  g_last_kernel = h == HOPF_H_L2 ? "hopf_diag_tm_kernel<l2>"
+                  : (h == HOPF_H_WL1 ? "hopf_diag_tm_kernel<wl1>" : "hopf_diag_tm_kernel<l1>");
   return check_launch("hopf_diag_tm_kernel");
 }
 
@@ -147,6 +150,7 @@ static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
   g_launches += 1;
   g_last_threads = threads;
   g_last_blocks = (int)blocks;
+  g_last_kernel = is_union ? "hopf_diag_kernel<union>" : "hopf_diag_kernel";
   return check_launch("hopf_diag_kernel");
 }
 
@@ -206,6 +210,8 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
 }
 
 int32_t hopf_last_launch_count(void) { return g_launches; }
+
+const char *hopf_last_kernel(void) { return g_last_kernel ? g_last_kernel : ""; }
 
 int32_t hopf_last_launch_config(int32_t *threads_per_block, int32_t *blocks) {
   if (threads_per_block) *threads_per_block = g_last_threads;
