@@ -73,7 +73,9 @@ __device__ __forceinline__ void wait_ld(float (&a)[N][8]) {
 
 template <int HK>
 __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagParams p) {
-  extern __shared__ __align__(16) uint8_t dyn_smem[];   // unused: residency cap only
+  // dynamic shared memory (48 KB, which also caps residency at 4 CTAs per SM): D at [0, 4 KB),
+  // w at [4, 8 KB) (wl1): per-coordinate parameters loaded once per CTA
+  extern __shared__ __align__(16) uint8_t dyn_smem[];
   __shared__ uint32_t tmem_slot;
   constexpr int G = 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -83,7 +85,13 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   const int n = p.n;
   const float lam = p.lambda, tol = p.tol;
   const int jmax = (n - gl + G - 1) / G;   // slots j < jmax are real coordinates
-  (void)dyn_smem;
+  float *const D_s = reinterpret_cast<float *>(dyn_smem);
+  float *const w_s = reinterpret_cast<float *>(dyn_smem + 4096);
+  for (int i = threadIdx.x; i < 1024; i += THREADS) {
+    D_s[i] = i < n ? __ldg(p.D + i) : 1.f;
+    if (HK == HK_WL1) w_s[i] = i < n ? __ldg(p.w + i) : 0.f;
+  }
+  __syncthreads();
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -104,7 +112,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
 #pragma unroll
     for (int e = 0; e < 8; e++) {
       const int j = 8 * c + e, i = gl + G * j;
-      kv[e] = (j < jmax) ? ksign * __fdividef(lam, __ldg(p.D + i) + lam) : 0.f;
+      kv[e] = (j < jmax) ? ksign * __fdividef(lam, D_s[i] + lam) : 0.f;
     }
     st8(T_K + 8 * c, kv);
   }
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       const int j0 = 2 * q, j1 = 2 * q + 1;
       const bool ok0 = active && j0 < jmax, ok1 = active && j1 < jmax;
       d[q] = make_float2(ok0 ? __ldg(xrow + gl + G * j0) : 0.f, ok1 ? __ldg(xrow + gl + G * j1) : 0.f);
-      b[q] = make_float2(ok0 ? __ldg(p.D + gl + G * j0) : 1.f, ok1 ? __ldg(p.D + gl + G * j1) : 1.f);
+      b[q] = make_float2(ok0 ? D_s[gl + G * j0] : 1.f, ok1 ? D_s[gl + G * j1] : 1.f);
     }
     if (p.c) {
 #pragma unroll
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         const float di = __fdividef(1.f, Dv + lam);
         xh8[e] = xt * di;
         v8[e] = xt;                                     // v^0 = x - c
-        if (HK == HK_WL1) tau8[e] = (active && j < jmax) ? tl * __ldg(p.w + gl + G * j) : 0.f;
+        if (HK == HK_WL1) tau8[e] = (active && j < jmax) ? tl * w_s[gl + G * j] : 0.f;
       }
       st8(T_XH + 8 * c, xh8);
       st8(T_V + 8 * c, v8);
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
 #pragma unroll
     for (int q = 0; q < NP; q++) {   // D of this lane's slots into b (dead), loads in flight together
       const int j0 = 2 * q, j1 = 2 * q + 1;
-      b[q] = make_float2(j0 < jmax ? __ldg(p.D + gl + G * j0) : 1.f, j1 < jmax ? __ldg(p.D + gl + G * j1) : 1.f);
+      b[q] = make_float2(j0 < jmax ? D_s[gl + G * j0] : 1.f, j1 < jmax ? D_s[gl + G * j1] : 1.f);
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) {
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
           qs = fmaf(xt, dq, qs);
           qs = fmaf(-0.5f * Dv * dq, dq, qs);
           if (HK == HK_L2) hsum = fmaf(dq, dq, hsum);
-          else if (HK == HK_WL1) hsum = fmaf(__ldg(p.w + i), fabsf(dq), hsum);
+          else if (HK == HK_WL1) hsum = fmaf(w_s[i], fabsf(dq), hsum);
           else hsum += fabsf(dq);
         }
         g8[e] = (spec == 2) ? __int_as_float(0x7fc00000) : dq;
