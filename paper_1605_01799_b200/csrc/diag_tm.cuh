@@ -251,11 +251,26 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     if (full_test) trip(std::true_type{});
     else trip(std::false_type{});
 
-    const float psd = (a0.x + a0.y) + (a1.x + a1.y), psb = (b0.x + b0.y) + (b1.x + b1.y);
-    const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
     bool conv;
     int kdone;
-    {
+    if (HK == HK_L2 && !full_test) {
+      // non-final l2 trip: only ||v^{k+1} - v^k||^2 and ||u_{k+1}||^2 are needed; transposed
+      // 2-value butterfly: lanes 0-15 end with the first total, lanes 16-31 with the second
+      const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
+      const bool hi = lane & 16;
+      float c = (hi ? pr2 : psv) + __shfl_xor_sync(0xffffffffu, hi ? psv : pr2, 16);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      const bool ok_sv = __shfl_sync(0xffffffffu, c, 0) <= tol;
+      const float r2 = __shfl_sync(0xffffffffu, c, 16);
+      kdone = it;
+      conv = false;            // no group had ||v^k - v^{k-1}||^2 <= tol
+      sv_ok = ok_sv;
+      s_cur = (r2 > tauS * tauS) ? fmaf(-tauS, rsqrtf(r2), 1.f) : 0.f;   // P:283-285, R20
+      it++;
+    } else {
+      const float psd = (a0.x + a0.y) + (a1.x + a1.y), psb = (b0.x + b0.y) + (b1.x + b1.y);
+      const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
       float r2;
       bool ok_sd, ok_sb, ok_sv;
       group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
