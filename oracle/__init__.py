@@ -58,7 +58,9 @@ def _load():
                                      dp, dp, ip, i32]
         lib.oracle_union.argtypes = [i64, i32, i32, dp, dp, dp, dp, dp, i32, dp, f64, i32, f64,
                                      dp, dp, ip, dp, ip, dp, i32]
-        for f in (lib.oracle_diag, lib.oracle_dense, lib.oracle_union):
+        lib.oracle_distance_union.argtypes = [i64, i32, i32, dp, dp, dp, dp, f64, i32, f64, i32,
+                                              f64, dp, dp, dp, dp, ip, ip, i32]
+        for f in (lib.oracle_diag, lib.oracle_dense, lib.oracle_union, lib.oracle_distance_union):
             f.restype = ctypes.c_int
         lib.oracle_threads.argtypes = [i32]
         lib.oracle_threads.restype = ctypes.c_int
@@ -168,3 +170,31 @@ def eval_union(X, t, Dk, Ck, gammak, h="l2", w=None, lam=1.0, max_iter=1000, tol
     if rc != 0:
         raise ValueError(f"oracle_union rejected its arguments (rc={rc})")
     return phi, grad, iters, Y, kstar, phik
+
+
+def distance_union(Yq, Dk, Ck, gammak, lam=1.0, max_iter=1000, tol=1e-8, max_newton=50,
+                   stol=1e-6, nthreads=0):
+    """dist, proj, psi, grad, kstar, newton for Omega = union_k {L_k <= 0}: Newton in s on
+    psi(y, s) = 0 with psi = min_k psi_k."""
+    Yq = _f64(Yq)
+    M, n = Yq.shape
+    Dk = _f64(Dk)
+    K = Dk.shape[0]
+    Dk = Dk.reshape(K, n)
+    Ck = _f64(Ck, (K, n))
+    gammak = _f64(gammak, (K,))
+    dist = np.empty(M)
+    proj = np.empty((M, n))
+    psi = np.empty(M)
+    grad = np.empty((M, n))
+    kstar = np.empty(M, dtype=np.int32)
+    newton = np.empty(M, dtype=np.int32)
+    ip = ctypes.POINTER(ctypes.c_int32)
+    rc = _load().oracle_distance_union(M, n, K, _d(Yq), _d(Dk), _d(Ck), _d(gammak), float(lam),
+                                       int(max_iter), float(tol), int(max_newton), float(stol),
+                                       _d(dist), _d(proj), _d(psi), _d(grad),
+                                       kstar.ctypes.data_as(ip), newton.ctypes.data_as(ip),
+                                       int(nthreads))
+    if rc != 0:
+        raise ValueError(f"oracle_distance_union rejected its arguments (rc={rc})")
+    return dist, proj, psi, grad, kstar, newton

@@ -232,3 +232,45 @@ def union_exact(x, t, Dk, Ck, gammak, h="l2", w=None):
     kstar = np.argmin(phik, axis=1)
     grad = np.stack([grads[k][i] for i, k in enumerate(kstar)])
     return phik[np.arange(x.shape[0]), kstar], grad, kstar, phik
+
+
+# --------------------------------------------------------------------------- distance (NEXT-1)
+def ellipsoid_projection(y, c, D, gamma=-0.5, iters=200):
+    """Euclidean projection of y onto E = {z : 1/2 <z-c, D^{-1}(z-c)> + gamma <= 0} (gamma < 0).
+
+    Plain definition, no Hopf formula: minimise 1/2||z - y||^2 subject to
+    sum_i (z_i - c_i)^2 / D_i <= r2, r2 = -2 gamma.  For y outside E the KKT condition
+    z - y + mu D^{-1}(z - c) = 0 gives z_i - c_i = (y_i - c_i) D_i / (D_i + mu), with mu > 0 the
+    root of sum_i (y_i - c_i)^2 D_i / (D_i + mu)^2 = r2 (left side strictly decreasing in mu);
+    bisection to full precision.  Returns (distance, z)."""
+    y = np.asarray(y, np.float64)
+    c = np.asarray(c, np.float64)
+    D = np.asarray(D, np.float64)
+    r2 = -2.0 * gamma
+    yt = y - c
+    if np.sum(yt * yt / D) <= r2:
+        return 0.0, y.copy()
+    f = lambda mu: np.sum(yt * yt * D / (D + mu) ** 2) - r2
+    lo, hi = 0.0, 1.0
+    while f(hi) > 0:
+        hi *= 2.0
+    for _ in range(iters):
+        mid = 0.5 * (lo + hi)
+        if f(mid) > 0:
+            lo = mid
+        else:
+            hi = mid
+    mu = 0.5 * (lo + hi)
+    z = c + yt * D / (D + mu)
+    return float(np.linalg.norm(z - y)), z
+
+
+def union_distance_exact(y, Dk, Ck, gammak):
+    """dist(y, union_k E_k) = min_k dist(y, E_k); the projection and member of the minimiser
+    (lowest k on ties)."""
+    best = (np.inf, None, -1)
+    for k in range(len(gammak)):
+        d, z = ellipsoid_projection(y, Ck[k], Dk[k], gammak[k])
+        if d < best[0]:
+            best = (d, z, k)
+    return best

@@ -22,6 +22,9 @@
  *   Quadratic prox.
  *   Min over initial data (union).
  *   Closest point y = x - t grad/||grad||.
+ *   Distance to a union (NEXT-1): Newton in s on psi(y,s) = 0 (eq. Newton_zero,
+ *   P:1096-1108) with d psi/dt = -||grad psi||, psi = min_k psi_k
+ *   for the union, pi_Omega(y) = y - s grad/||grad||.
  *
  * Readings of the paper: R1 grad := d at stop,
  * R2 phi := Hopf objective at d, R3 tol on squared norms, R5 shifted problems
@@ -341,6 +344,99 @@ int oracle_union(int64_t M, int n, int K, const double *X, const double *t, cons
       }
     }
     free(g);
+    free(ws);
+  }
+  return 0;
+}
+
+/* ---------------- distance / projection to a union (NEXT-1) -------------- */
+/* Evaluates psi(y,s) = min_k psi_k(y,s) and its gradient (the winner's) with the
+ * union routine above (split Bregman per set; s == 0 answered by L(y), R6). */
+static double union_psi(int n, int K, const double *y, double s, const double *Dk,
+                        const double *Ck, const double *gammak, double lambda, int max_iter,
+                        double tol, double *g, double *gk, double *ws, int *kbest) {
+  double best = INFINITY;
+  *kbest = -1;
+  for (int k = 0; k < K; k++) {
+    double ph;
+    int it = solve_diag_point(n, y, s, Dk + (size_t)k * n, Ck + (size_t)k * n, gammak[k],
+                              ORACLE_H_L2, NULL, lambda, max_iter, tol, &ph, gk, ws);
+    if (it == INT32_MIN) { *kbest = -1; return NAN; }
+    if (ph < best) { /* strict: lowest k wins ties (R19) */
+      best = ph;
+      *kbest = k;
+      memcpy(g, gk, sizeof(double) * n);
+    }
+  }
+  return best;
+}
+
+/* Closest point and distance from y to Omega = union_k {L_k <= 0}, L_k(y) =
+ * 1/2 <y-c_k, D_k^{-1}(y-c_k)> + gamma_k, by the paper's procedure:
+ *   s_0 = 0 (psi(y,0) = L(y), grad L(y): reading R24), then
+ *   s_{l+1} = s_l + psi(y,s_l) / ||grad_x psi(y,s_l)||           (eq. Newton_zero)
+ stopping when the Newton correction |s_{l+1} - s_l| <= stol max(1, s_l) or after max_newton
+ * evaluations, the result being the last evaluated s (reading R26); otherwise a step that
+ * leaves the bracket (lo, hi) (psi(lo) > 0 >= psi(hi)) is replaced by bisection (R25):
+ *   dist = s, proj = y - s grad/||grad||, psi = psi(y,s), grad, kstar,
+ *   newton = number of union evaluations at s > 0 (0 for y in Omega: dist 0, proj y).
+ * A point whose psi is non-finite gets NaN outputs and newton = INT32_MIN. */
+int oracle_distance_union(int64_t M, int n, int K, const double *Yq, const double *Dk,
+                          const double *Ck, const double *gammak, double lambda, int max_iter,
+                          double tol, int max_newton, double stol, double *dist, double *proj,
+                          double *psi, double *grad, int32_t *kstar, int32_t *newton,
+                          int nthreads) {
+  if (M < 0 || n < 1 || K < 1 || !Yq || !Dk || !Ck || !gammak || lambda <= 0.0 ||
+      max_iter < 1 || tol < 0.0 || max_newton < 1 || !(stol >= 0.0))
+    return -1;
+  int nt = nthreads_or_default(nthreads);
+#pragma omp parallel num_threads(nt)
+  {
+    double *ws = (double *)malloc(sizeof(double) * 8 * (size_t)n);
+    double *gk = (double *)malloc(sizeof(double) * (size_t)n);
+#pragma omp for schedule(dynamic, 4)
+    for (int64_t p = 0; p < M; p++) {
+      const double *y = Yq + p * n;
+      double *g = grad + p * n;
+      int kb;
+      double s = 0.0;
+      double ps = union_psi(n, K, y, 0.0, Dk, Ck, gammak, lambda, max_iter, tol, g, gk, ws, &kb);
+      int nn = 0, bad = !(ps == ps) || kb < 0;
+      if (!bad && ps > 0.0) {
+        double lo = 0.0, hi = INFINITY;
+        for (int l = 1; l <= max_newton; l++) {
+          double gn = 0.0;
+          for (int i = 0; i < n; i++) gn += g[i] * g[i];
+          gn = sqrt(gn);
+          if (!(gn > 0.0)) break;
+          double sn = s + ps / gn;                       /* eq. Newton_zero */
+          if (fabs(sn - s) <= stol * fmax(1.0, s)) break; /* R26 */
+          /* R25: a step that leaves the open bracket (lo, hi) is replaced by bisection; with
+           * psi(s) > 0 the step is > 0, so this only happens once hi is finite */
+          if (!(sn > lo && sn < hi)) sn = 0.5 * (lo + hi);
+          s = sn;
+          ps = union_psi(n, K, y, s, Dk, Ck, gammak, lambda, max_iter, tol, g, gk, ws, &kb);
+          nn = l;
+          if (!(ps == ps) || kb < 0) { bad = 1; break; }
+          if (ps > 0.0) lo = s; else hi = s;
+        }
+      }
+      if (bad) {
+        dist[p] = NAN; psi[p] = NAN; kstar[p] = -1; newton[p] = INT32_MIN;
+        for (int i = 0; i < n; i++) { g[i] = NAN; proj[p * n + i] = NAN; }
+        continue;
+      }
+      dist[p] = s;
+      psi[p] = ps;
+      kstar[p] = kb;
+      newton[p] = nn;
+      double gn = 0.0;
+      for (int i = 0; i < n; i++) gn += g[i] * g[i];
+      gn = sqrt(gn);
+      for (int i = 0; i < n; i++)
+        proj[p * n + i] = (s > 0.0 && gn > 0.0) ? y[i] - s * g[i] / gn : y[i];
+    }
+    free(gk);
     free(ws);
   }
   return 0;

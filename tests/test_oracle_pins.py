@@ -279,3 +279,52 @@ def test_status_codes_nonconvergence_and_invalid():
     assert it[1] == oracle.INVALID and np.isnan(phi[1])  # t < 0
     assert it[2] == oracle.INVALID and np.all(np.isnan(g[2]))
     assert it[3] == 0 and abs(phi[3] - 0.5 * np.sum(X[3] ** 2 / D)) < 1e-15
+
+
+# ----------------------------------------------------------------- distance mode (NEXT-1)
+def test_distance_sphere_closed_form():
+    """Newton in s on psi(y,s) = 0 for a ball: dist = ||y-c|| - r and
+    pi(y) = c + r (y-c)/||y-c|| exactly (radial symmetry); interior points return 0, y."""
+    rng = np.random.default_rng(11)
+    n = 7
+    r = 1.7
+    c = rng.normal(size=n)
+    Y = c + rng.normal(size=(40, n)) * 3.0
+    Y[0] = c + 0.3 * r * np.eye(n)[0]          # interior
+    D, C, g = np.full((1, n), r * r), c[None], np.array([-0.5])
+    dist, proj, psi, grad, ks, nn = oracle.distance_union(Y, D, C, g, tol=1e-14, stol=1e-12)
+    rho = np.linalg.norm(Y - c, axis=1)
+    out = rho > r
+    np.testing.assert_allclose(dist[out], rho[out] - r, rtol=1e-9, atol=1e-9)
+    exp = c + r * (Y - c) / rho[:, None]
+    np.testing.assert_allclose(proj[out], exp[out], atol=1e-8)
+    assert dist[0] == 0.0 and nn[0] == 0 and np.array_equal(proj[0], Y[0])
+    assert np.all(nn[out] >= 1)
+    # the same on the 2-D unit circle: (3,0) -> (1,0) at 2, (3,4) -> (0.6,0.8) at 4
+    d2, p2, *_ = oracle.distance_union(np.array([[3.0, 0.0], [3.0, 4.0]]), np.ones((1, 2)),
+                                       np.zeros((1, 2)), np.array([-0.5]), tol=1e-14, stol=1e-12)
+    np.testing.assert_allclose(d2, [2.0, 4.0], atol=1e-10)
+    np.testing.assert_allclose(p2, [[1.0, 0.0], [0.6, 0.8]], atol=1e-9)
+
+
+def test_distance_union_matches_exact_projection():
+    """Against the plain definition: projection on each ellipsoid by its KKT secular equation
+    (bisection, no Hopf formula), minimum over the members."""
+    rng = np.random.default_rng(12)
+    n, K = 12, 5
+    Dk = rng.uniform(0.5, 2.0, (K, n)) ** 2
+    Ck = rng.normal(0, 4, (K, n))
+    gk = -0.5 * rng.uniform(0.5, 1.5, K)       # scaled ellipsoids: r^2 = -2 gamma
+    Y = rng.normal(0, 4, (30, n))
+    dist, proj, psi, grad, ks, nn = oracle.distance_union(Y, Dk, Ck, gk, tol=1e-14, stol=1e-12)
+    for i in range(len(Y)):
+        de, z, k = exact.union_distance_exact(Y[i], Dk, Ck, gk)
+        assert abs(dist[i] - de) <= 1e-9 * max(1.0, de)
+        np.testing.assert_allclose(proj[i], z, atol=1e-7 * max(1.0, de))
+        assert ks[i] == k
+        if de > 0:
+            # invariants: ||y - pi|| = dist, pi on the boundary of the winner (L_k(pi) = 0)
+            assert abs(np.linalg.norm(Y[i] - proj[i]) - dist[i]) <= 1e-9 * max(1.0, de)
+            Lk = 0.5 * np.sum((proj[i] - Ck[k]) ** 2 / Dk[k]) + gk[k]
+            assert abs(Lk) <= 1e-7
+            assert abs(psi[i]) <= 1e-8
