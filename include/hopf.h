@@ -93,6 +93,34 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
                     float *grad, int32_t *iters, float *Y, int32_t *kstar, float *phi_k,
                     hopf_stream_t stream);
 
+/* Distance and closest point to a union of ellipsoids (NEXT-1):
+ *   Omega = union_k {y : L_k(y) <= 0},  L_k(y) = 1/2 <y - c_k, diag(Dj_k)^{-1}(y - c_k)> + gamma_k
+ *   (gamma_k < 0; gamma_k = -1/2 is the ellipsoid with semi-axes sqrt(Dj_k)).
+ * psi(y,s) = min_k psi_k(y,s) solves the eikonal problem psi_t + ||grad psi|| = 0, psi(.,0) = L
+ * (H = l2); each evaluation runs split Bregman for the K sets (as hopf_eval_union with t = s).
+ * Newton in s on psi(y,s) = 0 (eq. Newton_zero): s_0 = 0 (psi(y,0) = L(y), R24),
+ *   s_{l+1} = s_l + psi(y,s_l) / ||grad psi(y,s_l)||,
+ * stopping when |s_{l+1} - s_l| <= stol max(1, s_l) or after max_newton evaluations (the
+ * result is the last evaluated s, R26); a step leaving the bracket of the root is replaced by
+ * bisection (R25).
+ *   Y [M*n]      query points (device)
+ *   Dj, C [K*n], gamma [K]   the sets (device)
+ *   lambda, max_iter, tol    the inner split Bregman parameters (as hopf_eval_union)
+ *   max_newton (>= 1), stol (>= 0)   the outer Newton parameters
+ *   dist [M]     s = dist(y, Omega) (0 for y in Omega)
+ *   proj [M*n]   pi_Omega(y) = y - s grad/||grad||; y itself for y in Omega
+ *   psi [M]      psi(y, s) at the returned s (residual of the root)
+ *   grad [M*n]   grad_x psi(y, s)
+ *   kstar [M]    winning set;  newton [M] number of evaluations at s > 0 (0 for y in Omega,
+ *                INT32_MIN for a non-finite point: all outputs NaN)
+ * Constraints: 1 <= K <= 64, n <= 256.  Asynchronous on `stream`; errors as hopf_eval_union. */
+int hopf_distance_union(int64_t M, int32_t n, int32_t K, const float *Y, const float *Dj,
+                        const float *C, const float *gamma, float lambda, int32_t max_iter,
+                        float tol, int32_t max_newton, float stol, float *dist, float *proj,
+                        float *psi, float *grad, int32_t *kstar, int32_t *newton,
+                        hopf_stream_t stream);
+
+
 /* Full SPD initial data J(x) = 1/2 <x, A x> + gamma with A = Q diag(Lambda) Q^T (spectral
  * form as in P:1287-1290).  The plan owns device copies of
  *   M_lambda = (A^{-1} + lambda I)^{-1} = Q diag(Lambda/(1 + lambda Lambda)) Q^T

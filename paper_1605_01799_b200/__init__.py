@@ -46,8 +46,11 @@ def lib():
                                       vp, vp, vp, vp]
         L.hopf_eval_diag_host.argtypes = [i64, i32, vp, vp, vp, vp, f32, ctypes.c_int, vp, f32, i32,
                                           f32, vp, vp, vp]
+        L.hopf_distance_union.argtypes = [i64, i32, i32, vp, vp, vp, vp, f32, i32, f32, i32, f32,
+                                          vp, vp, vp, vp, vp, vp, vp]
         for f in (L.hopf_eval_diag, L.hopf_eval_union, L.hopf_dense_plan_create,
-                  L.hopf_dense_plan_destroy, L.hopf_eval_dense, L.hopf_eval_diag_host):
+                  L.hopf_dense_plan_destroy, L.hopf_eval_dense, L.hopf_eval_diag_host,
+                  L.hopf_distance_union):
             f.restype = ctypes.c_int
         L.hopf_last_error.restype = ctypes.c_char_p
         L.hopf_strerror.restype = ctypes.c_char_p
@@ -149,6 +152,32 @@ def eval_union(X, t, Dk, Ck, gammak, h="l2", w=None, lam=1.0, max_iter=1000, tol
                                _ptr(pk, "f32", M * K, "phik"), _stream(stream))
     _check(rc, "hopf_eval_union")
     return phi, grad, iters, Y, ks, pk
+
+
+def distance_union(Y, Dk, Ck, gammak, lam=1.0, max_iter=1000, tol=1e-8, max_newton=50,
+                   stol=1e-5, stream=None):
+    """hopf_distance_union: distance and closest point to the union of the sets
+    {L_k <= 0} by Newton in s on psi(y,s) = 0.
+    Returns (dist, proj, psi, grad, kstar, newton)."""
+    import torch
+    M, n = Y.shape
+    K = Dk.shape[0]
+    dev = Y.device
+    dist = torch.empty(M, dtype=torch.float32, device=dev)
+    proj = torch.empty((M, n), dtype=torch.float32, device=dev)
+    psi = torch.empty(M, dtype=torch.float32, device=dev)
+    grad = torch.empty((M, n), dtype=torch.float32, device=dev)
+    ks = torch.empty(M, dtype=torch.int32, device=dev)
+    nn = torch.empty(M, dtype=torch.int32, device=dev)
+    rc = lib().hopf_distance_union(M, n, K, _ptr(Y, "f32", M * n, "Y"), _ptr(Dk, "f32", K * n, "Dk"),
+                                   _ptr(Ck, "f32", K * n, "Ck"), _ptr(gammak, "f32", K, "gammak"),
+                                   float(lam), int(max_iter), float(tol), int(max_newton),
+                                   float(stol), _ptr(dist, "f32", M, "dist"),
+                                   _ptr(proj, "f32", M * n, "proj"), _ptr(psi, "f32", M, "psi"),
+                                   _ptr(grad, "f32", M * n, "grad"), _ptr(ks, "i32", M, "kstar"),
+                                   _ptr(nn, "i32", M, "newton"), _stream(stream))
+    _check(rc, "hopf_distance_union")
+    return dist, proj, psi, grad, ks, nn
 
 
 class DensePlan:

@@ -51,6 +51,10 @@ struct DiagParams {
   float *Y;
   int *kstar;
   float *phik;
+  // distance mode (union, H = l2; NEXT-1): non-null dist selects Newton in s on psi(y,s) = 0
+  float *dist = nullptr;
+  int max_newton = 0;
+  float stol = 0.f;
 };
 
 template <int G>
@@ -211,12 +215,16 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
   bool sv_ok = false;   // l2: ||v^k - v^{k-1}||^2 <= tol of the pending iteration
   float best = 0.f;
   int bestk = -1, bestit = 0;
+  // distance mode: Newton evaluations at s > 0 so far, bracket (s_lo, s_hi) of the root
+  int nn = 0;
+  float s_lo = 0.f, s_hi = 0.f;
+  const bool DIST = UNION && p.dist != nullptr;
 
   // ---- load the point (x, t) into registers; detect t == 0 / invalid (collective) -----------
   auto load_point = [&](bool active) {
     bool bad = false;
     if (active) {
-      tt = __ldg(p.t + pt);
+      tt = DIST ? 0.f : __ldg(p.t + pt);   // distance mode starts at s_0 = 0 (reading R24)
       bad = !(tt >= 0.f) || !finite_f(tt);
       const float *xrow = p.X + pt * (int64_t)n;
 #pragma unroll
@@ -415,6 +423,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     if (spec == 2) phiv = __int_as_float(0x7fc00000);
 
     bool point_done = done;
+    bool restart = false;   // distance mode: the same point, the K sets again at a new s
     if (UNION) {
       if (done) {
         if (p.phik && gl == 0) p.phik[pt * p.K + kset] = phiv;
@@ -431,12 +440,42 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       for (int q = 0; q < NP; q++) gn = fmaf(bd[q].x, bd[q].x, fmaf(bd[q].y, bd[q].y, gn));
       gn = sqrtf(group_sum<G>(gn));
       const float ign = (gn > 0.f) ? __fdividef(1.f, gn) : 0.f;
+      if (DIST && point_done && spec != 2 && bestk >= 0) {
+        // distance mode: psi(y,s) = best, grad psi = bd; Newton in s with
+        // d psi/dt = -||grad psi||, same step / stop / safeguard order as the oracle (R24-R26)
+        const float s0 = tt;
+        bool fin = false;
+        if (nn == 0 && s0 == 0.f) {
+          if (!(best > 0.f)) fin = true;                  // y in Omega: dist 0, proj y
+          else { s_lo = 0.f; s_hi = __int_as_float(0x7f800000); }
+        } else if (best > 0.f) {
+          s_lo = s0;
+        } else {
+          s_hi = s0;
+        }
+        if (!fin && (nn >= p.max_newton || !(gn > 0.f))) fin = true;
+        if (!fin) {
+          float sn = s0 + best / gn;                        // eq. Newton_zero
+          if (fabsf(sn - s0) <= p.stol * fmaxf(1.f, s0)) {
+            fin = true;                                     // R26: keep the evaluated s
+          } else {
+            if (!(sn > s_lo && sn < s_hi)) sn = 0.5f * (s_lo + s_hi);   // R25
+            point_done = false;                             // evaluate the K sets at sn
+            restart = true;
+            nn++;
+            tt = sn;
+            tauS = sn / lam;
+            spec = 0;
+          }
+        }
+      }
       if (point_done) {
         const bool nanpt = (spec == 2) || bestk < 0;
         if (gl == 0) {
           p.phi[pt] = nanpt ? __int_as_float(0x7fc00000) : best;
-          p.iters[pt] = nanpt ? INT32_MIN : bestit;
+          p.iters[pt] = nanpt ? INT32_MIN : (DIST ? nn : bestit);
           if (p.kstar) p.kstar[pt] = nanpt ? -1 : bestk;
+          if (DIST) p.dist[pt] = nanpt ? __int_as_float(0x7fc00000) : tt;
         }
         float *grow = p.grad + pt * (int64_t)n;
         float *yrow = p.Y ? p.Y + pt * (int64_t)n : nullptr;
@@ -449,6 +488,8 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
             if (yrow) {
               float y;
               if (nanpt) y = __int_as_float(0x7fc00000);
+              else if (DIST) y = (tt > 0.f && gn > 0.f) ? HOPF_SLOT(xr, j) - tt * (gj * ign)
+                                                          : HOPF_SLOT(xr, j);
               else if (gn > 0.f) y = HOPF_SLOT(xr, j) - tt * (gj * ign);
               else y = __ldg(p.c + (size_t)bestk * n + i);                  // reading R18
               yrow[i] = y;
@@ -473,8 +514,9 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     load_point(point_done && have);   // collective (ballot inside): all lanes call it
     if (done) {
       if (have) {
-        kset = point_done ? 0 : kset + 1;
-        if (UNION && point_done) { best = __int_as_float(0x7f800000); bestk = -1; bestit = 0; }
+        kset = (point_done || restart) ? 0 : kset + 1;
+        if (UNION && (point_done || restart)) { best = __int_as_float(0x7f800000); bestk = -1; bestit = 0; }
+        if (point_done) nn = 0;
         setup_solve();
       } else {
 #pragma unroll

@@ -209,6 +209,33 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
   return launch_diag_like(p, h, true, (cudaStream_t)stream);
 }
 
+int hopf_distance_union(int64_t M, int32_t n, int32_t K, const float *Y, const float *Dj,
+                        const float *C, const float *gamma, float lambda, int32_t max_iter,
+                        float tol, int32_t max_newton, float stol, float *dist, float *proj,
+                        float *psi, float *grad, int32_t *kstar, int32_t *newton,
+                        hopf_stream_t stream) {
+  g_launches = 0;
+  g_last_error.clear();
+  if (M < 0 || n < 1 || K < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d K=%d", (long long)M, n, K);
+  if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
+  if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
+  if (max_newton < 1) return set_error(HOPF_EINVAL, "max_newton must be >= 1");
+  if (!(stol >= 0.f) || !std::isfinite(stol)) return set_error(HOPF_EINVAL, "stol must be >= 0");
+  if (K > 64 || n > 256) return set_error(HOPF_EUNSUPPORTED, "union supports K<=64, n<=256");
+  if (M == 0) return HOPF_OK;
+  if (!Y || !Dj || !C || !gamma || !dist || !proj || !psi || !grad || !kstar || !newton)
+    return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  DiagParams p{};
+  p.M = M; p.n = n; p.X = Y; p.t = nullptr; p.D = Dj; p.c = C; p.w = nullptr; p.gk = gamma;
+  p.gamma = 0.f; p.lambda = lambda; p.max_iter = max_iter; p.tol = tol; p.K = K;
+  p.phi = psi; p.grad = grad; p.iters = newton; p.Y = proj; p.kstar = kstar; p.phik = nullptr;
+  p.dist = dist; p.max_newton = max_newton; p.stol = stol;
+  int rc = launch_diag_like(p, HOPF_H_L2, true, (cudaStream_t)stream);
+  if (rc == HOPF_OK) g_last_kernel = "hopf_diag_kernel<union, distance>";
+  return rc;
+}
+
 int32_t hopf_last_launch_count(void) { return g_launches; }
 
 const char *hopf_last_kernel(void) { return g_last_kernel ? g_last_kernel : ""; }

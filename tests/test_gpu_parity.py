@@ -317,3 +317,63 @@ def test_host_pipeline_matches_device(hb):
     pd, gd, idv = run_diag(hb, wl, X, t)
     torch.cuda.synchronize()
     assert torch.equal(ph, pd.cpu()) and torch.equal(gh, gd.cpu()) and torch.equal(ih, idv.cpu())
+
+
+# ----------------------------------------------------------------- distance mode (NEXT-1)
+DIST_RTOL, PROJ_RTOL = 1e-4, 1e-3
+
+
+def check_distance(g, o, Y, Dk, Ck, gk):
+    """GPU (fp32) vs oracle (fp64) distance mode.  dist within 1e-4 max(1, d); the projection
+    within 1e-3 max(1, d) (the grad-direction bar scaled by s); the winner may differ only at a
+    near tie (the exact per-member distances decide); Newton counts within 2."""
+    from oracle import exact
+    dist, proj, psi, grad, ks, nn = (a.cpu().numpy() for a in g)
+    dist_o, proj_o, psi_o, grad_o, ks_o, nn_o = o
+    ok = nn_o != oracle.INVALID
+    assert np.array_equal(nn[~ok], nn_o[~ok]) and np.all(np.isnan(dist[~ok]))
+    scale = np.maximum(1.0, dist_o[ok])
+    assert np.max(np.abs(dist[ok] - dist_o[ok]) / scale) <= DIST_RTOL
+    same = ks[ok] == ks_o[ok]
+    for i in np.nonzero(ok)[0][~same]:
+        dk = [exact.ellipsoid_projection(Y[i], Ck[k], Dk[k], gk[k])[0] for k in (ks[i], ks_o[i])]
+        assert dk[0] <= dk[1] + DIST_RTOL * max(1.0, dk[1]), f"point {i}: winner {ks[i]} vs {ks_o[i]}"
+    idx = np.nonzero(ok)[0][same]
+    assert np.all(np.abs(proj[idx] - proj_o[idx]) <= PROJ_RTOL * scale[same][:, None])
+    assert np.all(np.abs(nn[ok] - nn_o[ok]) <= 2)
+    inside = ok & (dist_o == 0)
+    assert np.all(dist[inside] == 0) and np.all(nn[inside] == 0)
+    assert np.array_equal(proj[inside], Y[inside])
+
+
+def test_distance_union_c5_geometry(hb):
+    """The C5 sets (K=16 ellipsoids in n=64) and query law; distance and projection per
+    P:1085-1108 against the oracle's Newton on psi, plus invariants at any size."""
+    wl = inputs.config("c5")
+    Y, _ = inputs.points(wl, 0, 300)
+    Y = Y.copy()
+    Y[0] = wl.Ck[3]                      # a centre: inside its ellipsoid
+    Y[1, 5] = np.nan                     # invalid point
+    g = hb.distance_union(dev(Y), dev(wl.Dk), dev(wl.Ck), dev(wl.gammak), stol=1e-5)
+    o = oracle.distance_union(Y, wl.Dk, wl.Ck, wl.gammak, stol=1e-5)
+    check_distance(g, o, Y, wl.Dk, wl.Ck, wl.gammak)
+    dist, proj = g[0].cpu().numpy(), g[1].cpu().numpy()
+    ok = np.isfinite(dist)
+    # ||y - pi(y)|| = dist (P:1091-1095)
+    assert np.allclose(np.linalg.norm(Y[ok] - proj[ok], axis=1), dist[ok], rtol=1e-4, atol=1e-4)
+
+
+def test_distance_sphere_closed_form_gpu(hb):
+    rng = np.random.default_rng(21)
+    n, r = 40, 2.5
+    c = rng.normal(size=n).astype(np.float32)
+    Y = (c + rng.normal(size=(500, n)) * 2.0).astype(np.float32)
+    D = np.full((1, n), r * r, np.float32)
+    dist, proj, psi, grad, ks, nn = (a.cpu().numpy() for a in hb.distance_union(
+        dev(Y), dev(D), dev(c[None]), dev(np.array([-0.5], np.float32)), stol=1e-6))
+    rho = np.linalg.norm(Y.astype(np.float64) - c, axis=1)
+    out = rho > r
+    assert np.max(np.abs(dist[out] - (rho[out] - r)) / np.maximum(1, rho[out] - r)) <= 1e-4
+    exp = c + r * (Y - c) / rho[:, None]
+    assert np.max(np.abs(proj[out] - exp[out])) <= 1e-3
+    assert np.all(dist[~out] == 0) and np.all(nn[~out] == 0)
