@@ -40,7 +40,7 @@ FP32_LANES_PER_SM = 128
 # algorithmic FP32 flops per coordinate-iteration: update + the paper's test
 FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14}
 # per-point HBM bytes: x (4n) + grad (4n) + t, phi, iters (12)
-CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000}
+CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000, "c5d": 2048}
 CPU_MIN_SECONDS = 10.0
 
 
@@ -132,6 +132,9 @@ def _oracle_once(wl, X, t):
     elif wl.kind == "union":
         oracle.eval_union(X, t, wl.Dk, wl.Ck, wl.gammak, wl.h, lam=wl.lam, max_iter=wl.max_iter,
                           tol=wl.tol)
+    elif wl.kind == "distance":
+        oracle.distance_union(X, wl.Dk, wl.Ck, wl.gammak, lam=wl.lam, max_iter=wl.max_iter,
+                              tol=wl.tol, stol=1e-5)
     else:
         oracle.eval_dense(X, t, wl.Q, wl.Lam, wl.gamma, wl.h, lam=wl.lam, max_iter=wl.max_iter,
                           tol=wl.tol)
@@ -151,7 +154,7 @@ def run_reference(args, wl):
         times.append(dt)
     ms = 1e3 * statistics.mean(times)
     value = sample / (ms / 1e3)
-    line = {"metric": METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={wl.n})",
+    line = {"metric": metric_name(wl),
             "value": value, "unit": UNIT, "impl": "reference", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE law)",
@@ -163,13 +166,22 @@ def run_reference(args, wl):
     return 0
 
 
+def metric_name(wl):
+    if wl.kind == "distance":
+        return f"closest-point queries/sec ({wl.name}: union of K={wl.Dk.shape[0]} ellipsoids, n={wl.n})"
+    return METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={wl.n})"
+
+
 def config_dict(wl, ws):
     d = {"workload": f"{wl.name}: n={wl.n}, M={wl.M} points per GPU, H={wl.h}, J={wl.kind}",
          "n": wl.n, "M_per_gpu": wl.M, "global_points": wl.M * ws, "lambda": wl.lam,
          "tol": wl.tol, "max_iter": wl.max_iter, "parallelism": f"dp{ws} (point shards)",
          "l2_flush": "none needed: per-step inputs+outputs exceed the 126 MB L2"}
-    if wl.kind == "union":
-        d["K"] = wl.K
+    if wl.kind in ("union", "distance"):
+        d["K"] = int(wl.Dk.shape[0])
+    if wl.kind == "distance":
+        d["workload"] = (f"{wl.name}: distance/projection to the union of K={d['K']} ellipsoids, "
+                         f"n={wl.n}, M={wl.M} query points per GPU (Newton in s, P:1085-1108)")
     return d
 
 
@@ -233,6 +245,13 @@ def main():
                                    grad.data_ptr(), iters.data_ptr(), Y.data_ptr(),
                                    kst.data_ptr(), None, stream.cuda_stream)
             hb._check(rc, "hopf_eval_union")
+    elif wl.kind == "distance":
+        Dk, Ck, gk = f32(wl.Dk), f32(wl.Ck), f32(wl.gammak)
+        dres = {}
+
+        def step():
+            dres["r"] = hb.distance_union(X, Dk, Ck, gk, wl.lam, wl.max_iter, wl.tol,
+                                          stream=stream)
     else:
         plan = hb.DensePlan(wl.Q, wl.Lam, wl.lam)
         step = lambda: hb.eval_dense(X, t, plan, wl.gamma, wl.h, None, wl.max_iter, wl.tol,
@@ -241,7 +260,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    iters_np = iters.cpu().numpy()
+    iters_np = iters.cpu().numpy() if wl.kind != "distance" else dres["r"][5].cpu().numpy()
     launches_per_step = hb.last_launch_count()
     kernel_name = hb.last_kernel()
     import ctypes
@@ -339,7 +358,11 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     conv = iters_np[iters_np > 0]
     roof = None
-    if wl.kind in ("diag", "union"):
+    if wl.kind == "distance":
+        # iters = Newton evaluations of psi (each: K split Bregman solves); inner counts are not
+        # returned, so no flop roofline is claimed for this mode
+        roof = None
+    elif wl.kind in ("diag", "union"):
         it_sum = float(np.abs(iters_np[iters_np != inputs_invalid()]).sum())
         if wl.kind == "union":
             it_sum = float("nan")  # per-set counts are not returned; see DESIGN.md
@@ -385,7 +408,7 @@ def main():
                "sample": f"first {sample} points of {wl.name} x {reps} passes "
                          f"({dt:.1f} s of the fp64 oracle, OpenMP over points)"}
 
-    line = {"metric": METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={n})",
+    line = {"metric": metric_name(wl),
             "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",

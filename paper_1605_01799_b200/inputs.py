@@ -38,7 +38,7 @@ class Workload:
     n: int
     M: int
     h: str                      # "l1" | "wl1" | "l2"
-    kind: str                   # "diag" | "dense" | "union"
+    kind: str                   # "diag" | "dense" | "union" | "distance"
     seed: int
     x_law: tuple                # ("uniform", lo, hi) | ("normal", std)
     t_law: tuple                # ("uniform", lo, hi)
@@ -142,7 +142,7 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
         Lam = _loguniform(rng, 0.1, 10.0, n)
         return Workload("c4", n, M or 4_000_000, h or "l1", "dense", seed,
                         ("normal", 1.0), ("uniform", 0.1, 1.0), Q=Q, Lam=Lam, gamma=0.0)
-    if name == "c5":
+    if name in ("c5", "c5d"):
         n = n or 64
         K = 16
         seed = seed or SEED_BASE + 5
@@ -151,6 +151,9 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
         a = rng.uniform(0.5, 2.0, (K, n))
         Dk = (a * a).astype(np.float32)
         gk = np.full(K, -0.5, np.float32)
+        if name == "c5d":   # NEXT-1: distance / projection to the C5 union (same sets and y law)
+            return Workload("c5d", n, M or 100_000, "l2", "distance", seed,
+                            ("normal", 5.0), ("uniform", 0.0, 2.0), Dk=Dk, Ck=Ck, gammak=gk)
         return Workload("c5", n, M or 500_000, h or "l2", "union", seed,
                         ("normal", 5.0), ("uniform", 0.0, 2.0), Dk=Dk, Ck=Ck, gammak=gk)
     if name.startswith("p"):
@@ -168,4 +171,4 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d")
