@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   while (have) {   // one point per warp: `have` is warp-uniform
     float2 a0 = splat2(0.f), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0, r0 = a0, r1 = a0;
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
+    const float2 nsP = splat2(-s_cur), omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
     const bool full_test = (HK != HK_L2) || sv_ok;   // see hopf_diag_kernel: exact
     auto trip = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
@@ -212,19 +213,24 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
           float2 v = make_float2(ch[2][2 * e2], ch[2][2 * e2 + 1]);
           if (HK == HK_L2) {
             // d[q] = -d_{k-1}, kq = -kappa, b[q] = u_k
-            const float2 dd = fma2(sP, b[q], d[q]);                 // d_k - d_{k-1}, d_k = s_k u_k
-            d[q] = sub2(d[q], dd);                                  // -d_k
-            b[q] = add2(b[q], d[q]);                                // (3.4c): b_k = u_k - d_k
-            const float2 na = add2(d[q], b[q]);                     // -(d_k - b_k)
-            const float2 vn = fma2(kq, na, xh);                     // (3.4a): v_{k+1}
-            const float2 dv = sub2(vn, v);                          // v_{k+1} - v_k
+            // d_k = s_k u_k, b_k = u_k - d_k = (1 - s_k) u_k, d_k - b_k = (2 s_k - 1) u_k:
+            // three independent scalings of u_k = b[q] ((3.4b), (3.4c))
+            const float2 u = b[q];
             if (FULL) {
+              const float2 dd = fma2(sP, u, d[q]);                  // d_k - d_{k-1}
+              d[q] = sub2(d[q], dd);                                // -d_k
               const float2 dmv = add2(d[q], v);                     // v^k - d^k
               if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); }
               else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); }
+            } else {
+              d[q] = __fmul2_rn(nsP, u);                            // -d_k
             }
+            const float2 bk = __fmul2_rn(omsP, u);                  // b_k
+            const float2 na = __fmul2_rn(na_sP, u);                 // -(d_k - b_k)
+            const float2 vn = fma2(kq, na, xh);                     // (3.4a): v_{k+1}
+            const float2 dv = sub2(vn, v);                          // v_{k+1} - v_k
             v = vn;
-            b[q] = add2(v, b[q]);                                   // u_{k+1} = v_{k+1} + b_k
+            b[q] = add2(v, bk);                                     // u_{k+1} = v_{k+1} + b_k
             if (q & 1) { c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
             else       { c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
           } else {
