@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     //     (s = 1, u = x - c) and its test is skipped.
     float2 a0 = splat2(0.f), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0, r0 = a0, r1 = a0;
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
+    const float2 nsP = splat2(-s_cur), omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
     const float live = waiting ? 0.f : 1.f;
     // l2: ||d^k - d^{k-1}||^2 and ||d^k - v^k||^2 only matter when ||v^k - v^{k-1}||^2 <= tol
     // (sv_ok, known before the trip): trips in which no group of the warp has sv_ok skip both
@@ -314,20 +315,26 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       for (int q = 0; q < NP; q++) {
         const float2 kq = KSM ? lds_volatile2(kap_s + q * G + gl) : kap[q];
         if (HK == HK_L2) {
-          // d[q] = -d_{k-1}, kq = -kappa
-          const float2 dd = fma2(sP, b[q], d[q]);        // d_k - d_{k-1}, d_k = s_k u_k (3.4b)
-          d[q] = fma2(dd, splat2(-live), d[q]);          // -d_k (frozen while waiting)
-          b[q] = add2(b[q], d[q]);                       // (3.4c): b_k = u_k - d_k
-          const float2 na = add2(d[q], b[q]);            // -(d_k - b_k)
-          const float2 t = sub2(xh[q], v[q]);
-          const float2 dv = fma2(kq, na, t);             // (3.4a): v_{k+1} - v_k
+          // d[q] = -d_{k-1}, kq = -kappa, b[q] = u_k.  d_k = s_k u_k, b_k = (1 - s_k) u_k and
+          // d_k - b_k = (2 s_k - 1) u_k are scalings of u_k ((3.4b), (3.4c)); a waiting group
+          // keeps its d (select)
+          const float2 u = b[q];
           if (FULL) {
+            const float2 dd = fma2(sP, u, d[q]);         // d_k - d_{k-1}
+            d[q] = fma2(dd, splat2(-live), d[q]);        // -d_k (frozen while waiting)
             const float2 dmv = add2(d[q], v[q]);         // v^k - d^k
             if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); }
             else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); }
+          } else {
+            const float2 dn = __fmul2_rn(nsP, u);        // -d_k
+            d[q] = waiting ? d[q] : dn;
           }
+          const float2 bk = __fmul2_rn(omsP, u);         // b_k
+          const float2 na = __fmul2_rn(na_sP, u);        // -(d_k - b_k)
+          const float2 t = sub2(xh[q], v[q]);
+          const float2 dv = fma2(kq, na, t);             // (3.4a): v_{k+1} - v_k
           v[q] = add2(v[q], dv);                         // v_{k+1}
-          b[q] = add2(v[q], b[q]);                       // u_{k+1} = v_{k+1} + b_k
+          b[q] = add2(v[q], bk);                         // u_{k+1} = v_{k+1} + b_k
           if (q & 1) { c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
           else       { c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
         } else {
