@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
             const float2 dv = sub2(vn, v);                          // v_{k+1} - v_k
             v = vn;
             b[q] = add2(v, bk);                                     // u_{k+1} = v_{k+1} + b_k
-            if (q & 1) { c1 = fma2(dv, dv, c1); r1 = fma2(b[q], b[q], r1); }
-            else       { c0 = fma2(dv, dv, c0); r0 = fma2(b[q], b[q], r0); }
+            c0 = fma2(dv, dv, c0);          // one packed accumulator per sum: the loop has ample
+            r0 = fma2(b[q], b[q], r0);      // independent work, and the serial tail is shorter
           } else {
             const float2 a = sub2(d[q], b[q]);
             const float2 vn = fma2(kq, a, xh);                      // (3.4a): v^k
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     if (HK == HK_L2 && !full_test) {
       // non-final l2 trip: only ||v^{k+1} - v^k||^2 and ||u_{k+1}||^2 are needed; transposed
       // 2-value butterfly: lanes 0-15 end with the first total, lanes 16-31 with the second
-      const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
+      const float psv = c0.x + c0.y, pr2 = r0.x + r0.y;
       const bool hi = lane & 16;
       float c = (hi ? pr2 : psv) + __shfl_xor_sync(0xffffffffu, hi ? psv : pr2, 16);
 #pragma unroll
