@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   start_point(have);
 
   while (have) {   // one point per warp: `have` is warp-uniform
-    float2 a0 = splat2(0.f), a1 = a0, b0 = a0, b1 = a0, c0 = a0, c1 = a0, r0 = a0, r1 = a0;
+    float2 a0 = splat2(0.f), b0 = a0, c0 = a0, r0 = a0;   // one packed accumulator per sum
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
     const float2 nsP = splat2(-s_cur), omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
     const bool full_test = (HK != HK_L2) || sv_ok;   // see hopf_diag_kernel: exact
@@ -220,8 +220,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
               const float2 dd = fma2(sP, u, d[q]);                  // d_k - d_{k-1}
               d[q] = sub2(d[q], dd);                                // -d_k
               const float2 dmv = add2(d[q], v);                     // v^k - d^k
-              if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); }
-              else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); }
+              a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0);
             } else {
               d[q] = __fmul2_rn(nsP, u);                            // -d_k
             }
@@ -245,8 +244,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
             const float2 dd = sub2(dn, d[q]);
             d[q] = add2(d[q], dd);                                  // d^k (as the register kernel)
             const float2 dmv = sub2(d[q], v);                       // d^k - v^k
-            if (q & 1) { a1 = fma2(dd, dd, a1); b1 = fma2(dmv, dmv, b1); c1 = fma2(dv, dv, c1); }
-            else       { a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0); }
+            a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0);
           }
           ch[2][2 * e2] = v.x;
           ch[2][2 * e2 + 1] = v.y;
@@ -275,8 +273,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       s_cur = (r2 > tauS * tauS) ? fmaf(-tauS, rsqrtf(r2), 1.f) : 0.f;   // P:283-285, R20
       it++;
     } else {
-      const float psd = (a0.x + a0.y) + (a1.x + a1.y), psb = (b0.x + b0.y) + (b1.x + b1.y);
-      const float psv = (c0.x + c0.y) + (c1.x + c1.y), pr2 = (r0.x + r0.y) + (r1.x + r1.y);
+      const float psd = a0.x + a0.y, psb = b0.x + b0.y;
+      const float psv = c0.x + c0.y, pr2 = r0.x + r0.y;
       float r2;
       bool ok_sd, ok_sb, ok_sv;
       group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
