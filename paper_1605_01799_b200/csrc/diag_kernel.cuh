@@ -345,8 +345,8 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
           const float2 dn = sub2(u, b[q]);               // (3.4b) shrink_1; b^k = u - d^k
           const float2 dd = sub2(dn, d[q]);
           d[q] = fma2(dd, splat2(live), d[q]);           // d^k (exact zeros kept; frozen while waiting)
-          const float2 dmv = sub2(d[q], v[q]);           // d^k - v^k
-          a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0); c0 = fma2(dv, dv, c0);
+          // ||d^k - v^k||^2 is formed after the trip only for groups whose other two sums pass
+          a0 = fma2(dd, dd, a0); c0 = fma2(dv, dv, c0);
         }
       }
     };
@@ -371,7 +371,22 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       } else {
         it++;
         kdone = it;
-        conv = ok_sd && ok_sb && ok_sv;
+        // P:1597-1601.  The trip accumulated ||d^k - d^{k-1}||^2 and ||v^k - v^{k-1}||^2 only;
+        // where both pass, ||d^k - v^k||^2 is summed now from the registers (d = d^k, v = v^k),
+        // so the decision is the paper's at every iteration (the third sum is rarely needed)
+        const bool need = ok_sd && ok_sv;
+        conv = false;
+        if (__any_sync(0xffffffffu, need)) {
+          float sb = 0.f;
+#pragma unroll
+          for (int q = 0; q < NP; q++) {
+            const float2 dmv = sub2(d[q], v[q]);
+            sb = fmaf(dmv.x, dmv.x, fmaf(dmv.y, dmv.y, sb));
+          }
+          sb = group_sum<G>(sb);
+          conv = need && sb <= tol;
+        }
+        (void)ok_sb;
       }
     }
     if (have && !waiting && (spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)))) {
