@@ -263,6 +263,16 @@ def main():
     iters_np = iters.cpu().numpy() if wl.kind != "distance" else dres["r"][5].cpu().numpy()
     launches_per_step = hb.last_launch_count()
     kernel_name = hb.last_kernel()
+    # total split Bregman iterations of one step (all solves: union sets, Newton evaluations),
+    # from the library's instrumentation counter in one extra untimed step
+    inner_iters = None
+    if wl.kind in ("diag", "union", "distance"):
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        hb.set_iteration_counter(cnt)
+        step()
+        torch.cuda.synchronize(dev)
+        hb.set_iteration_counter(None)
+        inner_iters = int(cnt.item())
     import ctypes
     _th, _bl = ctypes.c_int32(0), ctypes.c_int32(0)
     L.hopf_last_launch_config(ctypes.byref(_th), ctypes.byref(_bl))
@@ -358,14 +368,11 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     conv = iters_np[iters_np > 0]
     roof = None
-    if wl.kind == "distance":
-        # iters = Newton evaluations of psi (each: K split Bregman solves); inner counts are not
-        # returned, so no flop roofline is claimed for this mode
-        roof = None
-    elif wl.kind in ("diag", "union"):
-        it_sum = float(np.abs(iters_np[iters_np != inputs_invalid()]).sum())
-        if wl.kind == "union":
-            it_sum = float("nan")  # per-set counts are not returned; see DESIGN.md
+    if wl.kind in ("diag", "union", "distance"):
+        it_sum = float(inner_iters)
+        # algorithmic HBM bytes per point: diag x in, grad out (4n each) + t, phi, iters;
+        # union / distance also write y (closest point / projection) and k*
+        hbm_per_point = (8 * n + 12) if wl.kind == "diag" else (12 * n + 16)
         flops = it_sum * n * FLOPS_PER_COORD_ITER[wl.h]
         achieved = flops / (ms_step / 1e3) / 1e12
         peak = sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
@@ -375,10 +382,11 @@ def main():
                 "peak_basis": f"{sms} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz (guide unit "
                               "counts, max SM clock)",
                 "algorithmic_flops_per_launch": flops,
+                "inner_iterations_per_launch": inner_iters,
                 "flops_per_coord_iter": FLOPS_PER_COORD_ITER[wl.h],
                 "mean_iters": float(conv.mean()) if conv.size else None,
-                "hbm_bytes_per_launch": M * (8 * n + 12),
-                "hbm_GBps": M * (8 * n + 12) / (ms_step / 1e3) / 1e9}
+                "hbm_bytes_per_launch": M * hbm_per_point,
+                "hbm_GBps": M * hbm_per_point / (ms_step / 1e3) / 1e9}
         if clocks:
             roof["frac_at_measured_clock"] = achieved / (sms * FP32_LANES_PER_SM * 2 *
                                                          clocks["sm_mhz"] * 1e6 / 1e12)

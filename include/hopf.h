@@ -154,6 +154,13 @@ int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host, const float *
                         const float *w, float lambda, int32_t max_iter, float tol,
                         float *phi_host, float *grad_host, int32_t *iters_host);
 
+/* Instrumentation (benchmarks): while `counter` (a DEVICE pointer to one unsigned 64-bit
+ * integer, or NULL to switch off) is set on this thread, hopf_eval_diag / hopf_eval_union /
+ * hopf_distance_union atomically add the split Bregman iterations of every solve they run
+ * (t > 0 solves; the union's K solves per point, every Newton evaluation) to *counter.  The
+ * caller zeroes and reads it.  Not used by the dense path.  Returns HOPF_OK. */
+int hopf_set_iteration_counter(unsigned long long *counter);
+
 /* Number of kernel launches the most recent successful call made on this thread. */
 int32_t hopf_last_launch_count(void);
 

@@ -56,6 +56,8 @@ def lib():
         L.hopf_strerror.restype = ctypes.c_char_p
         L.hopf_strerror.argtypes = [ctypes.c_int]
         L.hopf_last_launch_count.restype = ctypes.c_int32
+        L.hopf_set_iteration_counter.argtypes = [vp]
+        L.hopf_set_iteration_counter.restype = ctypes.c_int
         L.hopf_last_kernel.restype = ctypes.c_char_p
         L.hopf_last_launch_config.restype = ctypes.c_int32
         L.hopf_last_launch_config.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
@@ -69,6 +71,12 @@ def _check(rc: int, where: str):
         L = lib()
         raise HopfError(rc, where, (L.hopf_last_error() or b"").decode() or
                         L.hopf_strerror(rc).decode())
+
+
+def set_iteration_counter(counter) -> None:
+    """Point the library's solve-iteration counter at a device int64 tensor (or None)."""
+    _check(lib().hopf_set_iteration_counter(None if counter is None else counter.data_ptr()),
+           "hopf_set_iteration_counter")
 
 
 def last_kernel() -> str:

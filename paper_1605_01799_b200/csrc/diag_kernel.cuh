@@ -51,6 +51,8 @@ struct DiagParams {
   float *Y;
   int *kstar;
   float *phik;
+  // optional instrumentation: total split Bregman iterations of all solves (bench roofline)
+  unsigned long long *iter_total = nullptr;
   // distance mode (union, H = l2; NEXT-1): non-null dist selects Newton in s on psi(y,s) = 0
   float *dist = nullptr;
   int max_newton = 0;
@@ -290,6 +292,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     }
   }
 
+  unsigned my_iters = 0;   // this lane's share of p.iter_total (group lane 0 counts)
   while (__any_sync(0xffffffffu, have)) {
     // ================= one loop trip (all lanes, branch-free) ===============================
     // l1/wl1: the full iteration k = it+1, one reduction of (sd, sb, sv).
@@ -392,6 +395,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     if (have && !waiting && (spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)))) {
       waiting = true;
       wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -p.max_iter));
+      if (spec == 0) my_iters += (unsigned)kdone;
     }
     {
       const unsigned gbit = (gl == 0) ? 1u : 0u;
@@ -545,6 +549,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       }
     }
   }
+  if (p.iter_total && gl == 0 && my_iters) atomicAdd(p.iter_total, (unsigned long long)my_iters);
 }
 
 }  // namespace hopf

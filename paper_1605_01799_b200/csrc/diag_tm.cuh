@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   };
   start_point(have);
 
+  unsigned my_iters = 0;   // this warp's share of p.iter_total (lane 0 counts)
   while (have) {   // one point per warp: `have` is warp-uniform
     float2 a0 = splat2(0.f), b0 = a0, c0 = a0, r0 = a0;   // one packed accumulator per sum
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     asm volatile("tcgen05.wait::st.sync.aligned;");
     if (!(spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)))) continue;
     const int wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -p.max_iter));
+    if (spec == 0) my_iters += (unsigned)kdone;
 
     // ---- finalize: phi = <x - c, d> - 1/2 <d, D d> - t H(d) + gamma ((3.3) at d, R2); grad ----
     // t == 0: phi = J(x), grad = D^{-1}(x - c) (reading R6); invalid input: NaN (R6)
@@ -346,6 +348,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     have = pt < p.M;
     if (have) start_point(true);
   }
+  if (p.iter_total && lane == 0 && my_iters) atomicAdd(p.iter_total, (unsigned long long)my_iters);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)

@@ -21,6 +21,7 @@ thread_local std::string g_last_error;
 thread_local int32_t g_launches = 0;
 thread_local int32_t g_last_threads = 0, g_last_blocks = 0;
 thread_local const char *g_last_kernel = "";
+thread_local unsigned long long *g_iter_counter = nullptr;
 
 int set_error(int code, const char *fmt, ...) {
   char buf[512];
@@ -111,8 +112,10 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
   return check_launch("hopf_diag_tm_kernel");
 }
 
-static int launch_diag_like(const DiagParams &p, hopf_h_kind h, bool is_union,
+static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union,
                             cudaStream_t stream) {
+  DiagParams p = p_in;
+  p.iter_total = g_iter_counter;
   const Variant *v = pick_variant(p.n, is_union);
   if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
   static const char *tm_env = getenv("HOPF_DIAG_TM");
@@ -234,6 +237,11 @@ int hopf_distance_union(int64_t M, int32_t n, int32_t K, const float *Y, const f
   int rc = launch_diag_like(p, HOPF_H_L2, true, (cudaStream_t)stream);
   if (rc == HOPF_OK) g_last_kernel = "hopf_diag_kernel<union, distance>";
   return rc;
+}
+
+int hopf_set_iteration_counter(unsigned long long *counter) {
+  g_iter_counter = counter;
+  return HOPF_OK;
 }
 
 int32_t hopf_last_launch_count(void) { return g_launches; }
