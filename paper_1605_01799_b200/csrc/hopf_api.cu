@@ -80,6 +80,14 @@ static const Variant kVariants[] = {
     HOPF_VARIANT(16, 32), HOPF_VARIANT(32, 32)};
 
 static const Variant *pick_variant(int n, bool is_union) {
+  // HOPF_DIAG_VARIANT=G,CPL forces a variant (experiments)
+  static const char *force = getenv("HOPF_DIAG_VARIANT");
+  if (force) {
+    int fg = 0, fc = 0;
+    if (sscanf(force, "%d,%d", &fg, &fc) == 2)
+      for (const Variant &v : kVariants)
+        if (v.G == fg && v.CPL == fc && v.G * v.CPL >= n && (!is_union || v.fn[0][1])) return &v;
+  }
   for (const Variant &v : kVariants) {
     if (v.G * v.CPL < n) continue;
     if (is_union && v.fn[0][1] == nullptr) continue;

@@ -377,3 +377,32 @@ def test_distance_sphere_closed_form_gpu(hb):
     exp = c + r * (Y - c) / rho[:, None]
     assert np.max(np.abs(proj[out] - exp[out])) <= 1e-3
     assert np.all(dist[~out] == 0) and np.all(nn[~out] == 0)
+
+
+def test_iteration_counter_matches_iters(hb):
+    """hopf_set_iteration_counter: the device counter equals the sum of the returned iteration
+    counts (diag: both kernels), and for the union K solves per point (per-set counts from
+    K single-set evaluations)."""
+    import torch
+    wl = inputs.config("c3")
+    X, t = inputs.points(wl, 0, 2000)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    hb.set_iteration_counter(cnt)
+    phi, grad, it = run_diag(hb, wl, X, t)
+    torch.cuda.synchronize()
+    hb.set_iteration_counter(None)
+    itn = it.cpu().numpy()
+    assert int(cnt.item()) == int(np.abs(itn[itn != oracle.INVALID]).sum())
+    wu = inputs.config("c5")
+    Xu, tu = inputs.points(wu, 0, 300)
+    cnt.zero_()
+    hb.set_iteration_counter(cnt)
+    hb.eval_union(dev(Xu), dev(tu), dev(wu.Dk), dev(wu.Ck), dev(wu.gammak), "l2")
+    torch.cuda.synchronize()
+    hb.set_iteration_counter(None)
+    total = 0
+    for k in range(wu.Dk.shape[0]):
+        _, _, itk = hb.eval_diag(dev(Xu), dev(tu), dev(wu.Dk[k]), dev(wu.Ck[k]), float(wu.gammak[k]), "l2")
+        ik = itk.cpu().numpy()
+        total += int(np.abs(ik[ik != oracle.INVALID]).sum())
+    assert int(cnt.item()) == total
