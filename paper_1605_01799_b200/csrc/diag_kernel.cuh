@@ -191,6 +191,9 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
 
   // -kappa_i (l2) or kappa_i (l1) = lambda/(D_i+lambda), layout [pair][G] of float2
   __shared__ __align__(16) float2 kap_s[KSM ? NP * G : 1];
+  // non-union: D_i, 1/(D_i + lambda) and w_i by coordinate, staged once per CTA for the
+  // per-point setup and finalize (they were re-fetched from global per point)
+  __shared__ float D_s[KSM ? G * CPL : 1], di_s[KSM ? G * CPL : 1], w_s[(KSM && HK == HK_WL1) ? G * CPL : 1];
   const float ksign = (HK == HK_L2) ? -1.f : 1.f;
   if (KSM) {
     for (int e = threadIdx.x; e < NP * G; e += blockDim.x) {
@@ -200,6 +203,12 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       kv.x = (2 * pp < CPL && i0 < n) ? ksign * __fdividef(lam, __ldg(p.D + i0) + lam) : 0.f;
       kv.y = (2 * pp + 1 < CPL && i1 < n) ? ksign * __fdividef(lam, __ldg(p.D + i1) + lam) : 0.f;
       kap_s[e] = kv;
+    }
+    for (int i = threadIdx.x; i < G * CPL; i += blockDim.x) {
+      const float Dv = i < n ? __ldg(p.D + i) : 1.f;
+      D_s[i] = Dv;
+      di_s[i] = __fdividef(1.f, Dv + lam);
+      if (HK == HK_WL1) w_s[i] = i < n ? __ldg(p.w + i) : 0.f;
     }
     __syncthreads();
   }
@@ -255,14 +264,22 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       const int j0 = 2 * q, j1 = 2 * q + 1;
       const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
       const int i0 = gl + G * j0, i1 = gl + G * j1;
-      const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
       const float c0 = (cp && ok0) ? __ldg(cp + i0) : 0.f, c1 = (cp && ok1) ? __ldg(cp + i1) : 0.f;
       const float2 xv = UNION ? xr[q] : xh[q];
       const float xt0 = ok0 ? xv.x - c0 : 0.f, xt1 = ok1 ? xv.y - c1 : 0.f;
-      const float di0 = __fdividef(1.f, D0 + lam), di1 = __fdividef(1.f, D1 + lam);
+      float di0, di1;
+      if (KSM) {
+        di0 = ok0 ? di_s[i0] : 1.f;
+        di1 = ok1 ? di_s[i1] : 1.f;
+      } else {
+        const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
+        di0 = __fdividef(1.f, D0 + lam);
+        di1 = __fdividef(1.f, D1 + lam);
+      }
       if (!KSM) kap[q] = make_float2(ok0 ? ksign * lam * di0 : 0.f, ok1 ? ksign * lam * di1 : 0.f);
       if (HK == HK_WL1)
-        tau[q] = make_float2(ok0 ? tl * __ldg(p.w + i0) : 0.f, ok1 ? tl * __ldg(p.w + i1) : 0.f);
+        tau[q] = KSM ? make_float2(ok0 ? tl * w_s[i0] : 0.f, ok1 ? tl * w_s[i1] : 0.f)
+                     : make_float2(ok0 ? tl * __ldg(p.w + i0) : 0.f, ok1 ? tl * __ldg(p.w + i1) : 0.f);
       const float2 xt = make_float2(xt0, xt1);
       xh[q] = make_float2(xt0 * di0, xt1 * di1);
       if (HK == HK_L2) {
@@ -417,7 +434,8 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
         const int j0 = 2 * q, j1 = 2 * q + 1;
         const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
         const int i0 = gl + G * j0, i1 = gl + G * j1;
-        const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
+        const float D0 = ok0 ? (KSM ? D_s[i0] : __ldg(Dp + i0)) : 1.f;
+        const float D1 = ok1 ? (KSM ? D_s[i1] : __ldg(Dp + i1)) : 1.f;
         const float xt0 = xh[q].x * (D0 + lam), xt1 = xh[q].y * (D1 + lam);
         float2 dq = (HK == HK_L2) ? make_float2(0.f - d[q].x, 0.f - d[q].y) : d[q];
         if (spec == 1) {
@@ -430,8 +448,8 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
           qs = fmaf(-0.5f * D1 * dq.y, dq.y, qs);
           if (HK == HK_L2) hsum = fmaf(dq.x, dq.x, fmaf(dq.y, dq.y, hsum));
           else if (HK == HK_WL1)
-            hsum = fmaf(ok0 ? __ldg(p.w + i0) : 0.f, fabsf(dq.x),
-                        fmaf(ok1 ? __ldg(p.w + i1) : 0.f, fabsf(dq.y), hsum));
+            hsum = fmaf(ok0 ? (KSM ? w_s[i0] : __ldg(p.w + i0)) : 0.f, fabsf(dq.x),
+                        fmaf(ok1 ? (KSM ? w_s[i1] : __ldg(p.w + i1)) : 0.f, fabsf(dq.y), hsum));
           else hsum += fabsf(dq.x) + fabsf(dq.y);
         }
         d[q] = dq;   // from here on d holds the solve's gradient (+d)
