@@ -60,7 +60,10 @@ def _load():
                                      dp, dp, ip, dp, ip, dp, i32]
         lib.oracle_distance_union.argtypes = [i64, i32, i32, dp, dp, dp, dp, f64, i32, f64, i32,
                                               f64, dp, dp, dp, dp, ip, ip, i32]
-        for f in (lib.oracle_diag, lib.oracle_dense, lib.oracle_union, lib.oracle_distance_union):
+        lib.oracle_maxh.argtypes = [i64, i32, dp, dp, dp, dp, f64, i32, ip, dp, dp, f64, i32, f64,
+                                    dp, dp, ip, ip, i32]
+        for f in (lib.oracle_diag, lib.oracle_dense, lib.oracle_union, lib.oracle_distance_union,
+                  lib.oracle_maxh):
             f.restype = ctypes.c_int
         lib.oracle_threads.argtypes = [i32]
         lib.oracle_threads.restype = ctypes.c_int
@@ -198,3 +201,28 @@ def distance_union(Yq, Dk, Ck, gammak, lam=1.0, max_iter=1000, tol=1e-8, max_new
     if rc != 0:
         raise ValueError(f"oracle_distance_union rejected its arguments (rc={rc})")
     return dist, proj, psi, grad, kstar, newton
+
+
+def eval_maxh(X, t, D, c, gamma, kinds, a, W=None, lam=1.0, max_iter=1000, tol=1e-8, nthreads=0):
+    """phi = max_i phi_i for H = min_i a_i H_{kind_i}; returns phi, grad, iters, istar."""
+    X = _f64(X)
+    M, n = X.shape
+    D = _f64(D, (n,))
+    c = _f64(c, (n,)) if c is not None else None
+    t = _f64(t, (M,))
+    K = len(kinds)
+    kinds = np.ascontiguousarray([_hk(k) for k in kinds], dtype=np.int32)
+    a = _f64(a, (K,))
+    W = _f64(W, (K, n)) if W is not None else None
+    phi = np.empty(M)
+    grad = np.empty((M, n))
+    iters = np.empty(M, dtype=np.int32)
+    istar = np.empty(M, dtype=np.int32)
+    ip = ctypes.POINTER(ctypes.c_int32)
+    rc = _load().oracle_maxh(M, n, _d(X), _d(t), _d(D), _d(c), float(gamma), K,
+                             kinds.ctypes.data_as(ip), _d(W), _d(a), float(lam), int(max_iter),
+                             float(tol), _d(phi), _d(grad), iters.ctypes.data_as(ip),
+                             istar.ctypes.data_as(ip), int(nthreads))
+    if rc != 0:
+        raise ValueError(f"oracle_maxh rejected its arguments (rc={rc})")
+    return phi, grad, iters, istar

@@ -441,3 +441,69 @@ int oracle_distance_union(int64_t M, int n, int K, const double *Yq, const doubl
   }
   return 0;
 }
+
+/* ---------------- max over a min of Hamiltonians (NEXT-4) --------- */
+/* H = min_i a_i H_{kind_i}(.; w_i) with one diagonal J: phi = max_i phi_i, each phi_i
+ * the split Bregman solve with H_i (its prox threshold t a_i w_ij / lambda, its t H_i(d) term in
+ * (3.3)); grad = grad of the winner; the lowest i wins ties (as R19).  kinds[K], a[K] host
+ * arrays, W [K*n] weights (rows used for ORACLE_H_WL1 only). */
+int oracle_maxh(int64_t M, int n, const double *X, const double *t, const double *D,
+                const double *c, double gamma, int K, const int32_t *kinds, const double *W,
+                const double *a, double lambda, int max_iter, double tol, double *phi,
+                double *grad, int32_t *iters, int32_t *istar, int nthreads) {
+  if (M < 0 || n < 1 || K < 1 || !D || !kinds || !a || lambda <= 0.0 || max_iter < 1 || tol < 0.0)
+    return -1;
+  for (int i = 0; i < K; i++) {
+    if (kinds[i] < 0 || kinds[i] > 2 || !(a[i] > 0.0)) return -1;
+    if (kinds[i] == ORACLE_H_WL1 && !W) return -1;
+  }
+  int nt = nthreads_or_default(nthreads);
+#pragma omp parallel num_threads(nt)
+  {
+    double *ws = (double *)malloc(sizeof(double) * 8 * (size_t)n);
+    double *g = (double *)malloc(sizeof(double) * (size_t)n);
+    double *wa = (double *)malloc(sizeof(double) * (size_t)n);
+#pragma omp for schedule(dynamic, 16)
+    for (int64_t p = 0; p < M; p++) {
+      const double *x = X + p * n;
+      double best = -INFINITY;
+      int besti = -1, bestit = 0;
+      for (int i = 0; i < K; i++) {
+        /* H_i = a_i H_kind(.; w_i): an l1 / weighted l1 with weights a_i w_ij, or a_i ||.||_2
+         * (the l2 solve with t H_i = (a_i t) ||.||_2) */
+        double ph, ti = t[p];
+        const double *wi = NULL;
+        int h = kinds[i];
+        if (h == ORACLE_H_L2) {
+          ti = t[p] * a[i];
+        } else {
+          for (int j = 0; j < n; j++) wa[j] = a[i] * (h == ORACLE_H_WL1 ? W[(size_t)i * n + j] : 1.0);
+          wi = wa;
+          h = ORACLE_H_WL1;
+        }
+        int it = solve_diag_point(n, x, ti, D, c, gamma, h, wi, lambda, max_iter, tol, &ph, g, ws);
+        if (it == INT32_MIN) { besti = -1; bestit = INT32_MIN; break; }
+        if (ph > best) { /* strict: lowest i wins ties */
+          best = ph;
+          besti = i;
+          bestit = it;
+          memcpy(grad + p * n, g, sizeof(double) * n);
+        }
+      }
+      if (besti < 0) {
+        phi[p] = NAN;
+        for (int j = 0; j < n; j++) grad[p * n + j] = NAN;
+        iters[p] = INT32_MIN;
+        if (istar) istar[p] = -1;
+        continue;
+      }
+      phi[p] = best;
+      iters[p] = bestit;
+      if (istar) istar[p] = besti;
+    }
+    free(wa);
+    free(g);
+    free(ws);
+  }
+  return 0;
+}

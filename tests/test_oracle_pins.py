@@ -328,3 +328,50 @@ def test_distance_union_matches_exact_projection():
             Lk = 0.5 * np.sum((proj[i] - Ck[k]) ** 2 / Dk[k]) + gk[k]
             assert abs(Lk) <= 1e-7
             assert abs(psi[i]) <= 1e-8
+
+
+# ----------------------------------------------------------------- max over min of H (NEXT-4)
+def test_maxh_closed_form_mixed_kinds():
+    """J = 1/2||x||^2, H = min(||.||_1, c ||.||_2) (P:683-738): phi = max(phi_1, phi_2) with the
+    closed forms phi_1 = 1/2 sum max(|x_j| - t, 0)^2 (P:248-263 with a = 1) and
+    phi_2 = 1/2 max(||x|| - c t, 0)^2; grad = the winner's."""
+    rng = np.random.default_rng(31)
+    n, M, cc = 6, 400, 1.7
+    X = rng.uniform(-3, 3, (M, n))
+    t = rng.uniform(0.1, 1.5, M)
+    phi, grad, it, ist = oracle.eval_maxh(X, t, np.ones(n), None, 0.0, ["l1", "l2"], [1.0, cc],
+                                          tol=1e-14, max_iter=5000)
+    s1 = np.maximum(np.abs(X) - t[:, None], 0.0)
+    p1 = 0.5 * np.sum(s1 * s1, axis=1)
+    g1 = np.sign(X) * s1
+    r = np.linalg.norm(X, axis=1)
+    m2 = np.maximum(r - cc * t, 0.0)
+    p2 = 0.5 * m2 * m2
+    g2 = X * (m2 / r)[:, None]
+    exp = np.maximum(p1, p2)
+    np.testing.assert_allclose(phi, exp, rtol=1e-9, atol=1e-9)
+    win2 = p2 > p1 + 1e-9
+    win1 = p1 > p2 + 1e-9
+    assert np.all(ist[win2] == 1) and np.all(ist[win1] == 0)
+    np.testing.assert_allclose(grad[win1], g1[win1], atol=1e-6)
+    np.testing.assert_allclose(grad[win2], g2[win2], atol=1e-6)
+
+
+def test_maxh_matches_hopf_formula_with_min_hamiltonian_2d():
+    """n = 2: the Hopf formula with the nonconvex H = min_i H_i minimised by exhaustive search
+    (no split Bregman, no max identity) equals the oracle's max_i phi_i."""
+    D = np.array([0.7, 1.6])
+    w = np.array([[1.0, 1.0], [0.4, 1.8]])
+    kinds, a = ["wl1", "wl1", "l2"], [1.0, 1.0, 1.3]
+    W = np.stack([w[0], w[1], np.ones(2)])
+    Jstar = lambda V: 0.5 * (V * V) @ D
+    Hmin = lambda V: np.minimum(np.minimum(np.abs(V) @ w[0], np.abs(V) @ w[1]),
+                                1.3 * np.linalg.norm(V, axis=1))
+    rng = np.random.default_rng(32)
+    X = rng.uniform(-3, 3, (6, 2))
+    t = rng.uniform(0.2, 1.2, 6)
+    phi, grad, it, ist = oracle.eval_maxh(X, t, D, None, 0.0, kinds, a, W, tol=1e-14, max_iter=5000)
+    for i in range(len(X)):
+        ref, vbest = exact.hopf_dual_grid_2d(X[i], t[i], Jstar, Hmin, 8.0)
+        assert abs(phi[i] - ref) <= 1e-6 * max(1.0, abs(ref)), (i, phi[i], ref)
+        np.testing.assert_allclose(grad[i], vbest, atol=1e-3)
