@@ -40,7 +40,8 @@ FP32_LANES_PER_SM = 128
 # algorithmic FP32 flops per coordinate-iteration: update + the paper's test
 FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14}
 # per-point HBM bytes: x (4n) + grad (4n) + t, phi, iters (12)
-CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000, "c5d": 2048}
+CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000, "c5d": 2048,
+              "c2h": 200_000}
 CPU_MIN_SECONDS = 10.0
 
 
@@ -132,6 +133,10 @@ def _oracle_once(wl, X, t):
     elif wl.kind == "union":
         oracle.eval_union(X, t, wl.Dk, wl.Ck, wl.gammak, wl.h, lam=wl.lam, max_iter=wl.max_iter,
                           tol=wl.tol)
+    elif wl.kind == "maxh":
+        kinds, av, Wm = wl.maxh
+        oracle.eval_maxh(X, t, wl.D, None, wl.gamma, kinds, av, Wm, lam=wl.lam,
+                         max_iter=wl.max_iter, tol=wl.tol)
     elif wl.kind == "distance":
         oracle.distance_union(X, wl.Dk, wl.Ck, wl.gammak, lam=wl.lam, max_iter=wl.max_iter,
                               tol=wl.tol, stol=1e-5)
@@ -167,6 +172,8 @@ def run_reference(args, wl):
 
 
 def metric_name(wl):
+    if wl.kind == "maxh":
+        return f"Hopf evals/sec ({wl.name}: H = min of {len(wl.maxh[0])} Hamiltonians, n={wl.n})"
     if wl.kind == "distance":
         return f"closest-point queries/sec ({wl.name}: union of K={wl.Dk.shape[0]} ellipsoids, n={wl.n})"
     return METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={wl.n})"
@@ -245,6 +252,14 @@ def main():
                                    grad.data_ptr(), iters.data_ptr(), Y.data_ptr(),
                                    kst.data_ptr(), None, stream.cuda_stream)
             hb._check(rc, "hopf_eval_union")
+    elif wl.kind == "maxh":
+        kinds, av, Wm = wl.maxh
+        D, Wd = f32(wl.D), f32(Wm)
+        mres = {}
+
+        def step():
+            mres["r"] = hb.eval_maxh(X, t, D, None, wl.gamma, kinds, av, Wd, wl.lam, wl.max_iter,
+                                     wl.tol, out=out, stream=stream)
     elif wl.kind == "distance":
         Dk, Ck, gk = f32(wl.Dk), f32(wl.Ck), f32(wl.gammak)
         dres = {}
@@ -266,7 +281,7 @@ def main():
     # total split Bregman iterations of one step (all solves: union sets, Newton evaluations),
     # from the library's instrumentation counter in one extra untimed step
     inner_iters = None
-    if wl.kind in ("diag", "union", "distance"):
+    if wl.kind in ("diag", "union", "distance", "maxh"):
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         hb.set_iteration_counter(cnt)
         step()
@@ -368,12 +383,12 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     conv = iters_np[iters_np > 0]
     roof = None
-    if wl.kind in ("diag", "union", "distance"):
+    if wl.kind in ("diag", "union", "distance", "maxh"):
         it_sum = float(inner_iters)
         # algorithmic HBM bytes per point: diag x in, grad out (4n each) + t, phi, iters;
         # union / distance also write y (closest point / projection) and k*
-        hbm_per_point = (8 * n + 12) if wl.kind == "diag" else (12 * n + 16)
-        flops = it_sum * n * FLOPS_PER_COORD_ITER[wl.h]
+        hbm_per_point = (8 * n + 12) if wl.kind in ("diag", "maxh") else (12 * n + 16)
+        flops = it_sum * n * FLOPS_PER_COORD_ITER["l1" if wl.kind == "maxh" else wl.h]
         achieved = flops / (ms_step / 1e3) / 1e12
         peak = sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
         roof = {"kernel": kernel_name, "bound": "alu", "achieved": achieved, "peak": peak,

@@ -93,6 +93,21 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
                     float *grad, int32_t *iters, float *Y, int32_t *kstar, float *phi_k,
                     hopf_stream_t stream);
 
+/* Maximum over a minimum of Hamiltonians (NEXT-4): for H = min_i H_i,
+ *   phi(x,t) = max_i phi_i(x,t),  phi_i the solution with H_i and the same diagonal J,
+ * the lowest i winning ties; grad = the winner's gradient, iters = its status.
+ *   K (>= 1)       number of Hamiltonians
+ *   h_kinds [K]    HOST array of hopf_h_kind;  a [K] HOST array of scales a_i > 0
+ *   W [K*n]        DEVICE weights (row i used when h_kinds[i] == HOPF_H_WL1), else may be NULL
+ *   H_i(p) = a_i H_{kind_i}(p; W_i); evaluated as the kind's solve at time a_i t (t a_i H = (a_i t) H)
+ *   istar [M] or NULL   index of the winning Hamiltonian (-1 on invalid points)
+ * Other arguments as hopf_eval_diag.  Launches K solves + K combine steps on `stream`
+ * (stream-ordered scratch via cudaMallocAsync); results valid after the stream syncs. */
+int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const float *Dj,
+                   const float *c, float gamma, int32_t K, const int32_t *h_kinds, const float *a,
+                   const float *W, float lambda, int32_t max_iter, float tol, float *phi,
+                   float *grad, int32_t *iters, int32_t *istar, hopf_stream_t stream);
+
 /* Distance and closest point to a union of ellipsoids (NEXT-1):
  *   Omega = union_k {y : L_k(y) <= 0},  L_k(y) = 1/2 <y - c_k, diag(Dj_k)^{-1}(y - c_k)> + gamma_k
  *   (gamma_k < 0; gamma_k = -1/2 is the ellipsoid with semi-axes sqrt(Dj_k)).

@@ -46,11 +46,13 @@ def lib():
                                       vp, vp, vp, vp]
         L.hopf_eval_diag_host.argtypes = [i64, i32, vp, vp, vp, vp, f32, ctypes.c_int, vp, f32, i32,
                                           f32, vp, vp, vp]
+        L.hopf_eval_maxh.argtypes = [i64, i32, vp, vp, vp, vp, f32, i32, vp, vp, vp, f32, i32, f32,
+                                     vp, vp, vp, vp, vp]
         L.hopf_distance_union.argtypes = [i64, i32, i32, vp, vp, vp, vp, f32, i32, f32, i32, f32,
                                           vp, vp, vp, vp, vp, vp, vp]
         for f in (L.hopf_eval_diag, L.hopf_eval_union, L.hopf_dense_plan_create,
                   L.hopf_dense_plan_destroy, L.hopf_eval_dense, L.hopf_eval_diag_host,
-                  L.hopf_distance_union):
+                  L.hopf_distance_union, L.hopf_eval_maxh):
             f.restype = ctypes.c_int
         L.hopf_last_error.restype = ctypes.c_char_p
         L.hopf_strerror.restype = ctypes.c_char_p
@@ -160,6 +162,30 @@ def eval_union(X, t, Dk, Ck, gammak, h="l2", w=None, lam=1.0, max_iter=1000, tol
                                _ptr(pk, "f32", M * K, "phik"), _stream(stream))
     _check(rc, "hopf_eval_union")
     return phi, grad, iters, Y, ks, pk
+
+
+def eval_maxh(X, t, D, c, gamma, kinds, a, W=None, lam=1.0, max_iter=1000, tol=1e-8, out=None,
+              stream=None):
+    """hopf_eval_maxh: phi = max_i phi_i for H = min_i a_i H_{kind_i}.
+    Returns (phi, grad, iters, istar)."""
+    import numpy as np
+    import torch
+    M, n = X.shape
+    K = len(kinds)
+    phi, grad, iters = _outputs(M, n, X.device, out)
+    ist = torch.empty(M, dtype=torch.int32, device=X.device)
+    hk = np.ascontiguousarray([H_KINDS[k] if isinstance(k, str) else int(k) for k in kinds], dtype=np.int32)
+    av = np.ascontiguousarray(a, dtype=np.float32)
+    if av.shape != (K,):
+        raise ValueError("a must have one scale per Hamiltonian")
+    rc = lib().hopf_eval_maxh(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                              _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma), K,
+                              hk.ctypes.data, av.ctypes.data, _ptr(W, "f32", K * n, "W"),
+                              float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                              _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                              _ptr(ist, "i32", M, "istar"), _stream(stream))
+    _check(rc, "hopf_eval_maxh")
+    return phi, grad, iters, ist
 
 
 def distance_union(Y, Dk, Ck, gammak, lam=1.0, max_iter=1000, tol=1e-8, max_newton=50,

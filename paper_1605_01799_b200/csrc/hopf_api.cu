@@ -123,6 +123,34 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
   return check_launch("hopf_diag_tm_kernel");
 }
 
+
+// ---------------------------------------------------------------- NEXT-4 helpers
+// t_s = a * t (a_i H = time rescaling: t a_i H(p) = (a_i t) H(p))
+__global__ void hopf_scale_t_kernel(int64_t M, const float *t, float a, float *ts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
+    ts[i] = a * t[i];
+}
+// istar = 0 where the first solve is valid, -1 on invalid points
+__global__ void hopf_istar_init_kernel(int64_t M, const int32_t *iters, int32_t *istar) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
+    istar[i] = iters[i] == INT32_MIN ? -1 : 0;
+}
+// one warp per point: keep the larger phi (strict: the lowest i wins ties; NaN never wins)
+__global__ void hopf_maxh_combine_kernel(int64_t M, int n, int idx, const float *phi_i,
+                                         const float *grad_i, const int32_t *it_i, float *phi,
+                                         float *grad, int32_t *iters, int32_t *istar) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = w0; p < M; p += nw) {
+    const bool win = phi_i[p] > phi[p];
+    if (win) {
+      for (int j = lane; j < n; j += 32) grad[p * n + j] = grad_i[p * n + j];
+      if (lane == 0) { phi[p] = phi_i[p]; iters[p] = it_i[p]; if (istar) istar[p] = idx; }
+    }
+  }
+}
+
 static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union,
                             cudaStream_t stream) {
   DiagParams p = p_in;
@@ -248,6 +276,62 @@ int hopf_distance_union(int64_t M, int32_t n, int32_t K, const float *Y, const f
   int rc = launch_diag_like(p, HOPF_H_L2, true, (cudaStream_t)stream);
   if (rc == HOPF_OK) g_last_kernel = "hopf_diag_kernel<union, distance>";
   return rc;
+}
+
+
+int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const float *Dj,
+                   const float *c, float gamma, int32_t K, const int32_t *h_kinds, const float *a,
+                   const float *W, float lambda, int32_t max_iter, float tol, float *phi,
+                   float *grad, int32_t *iters, int32_t *istar, hopf_stream_t stream) {
+  g_launches = 0;
+  g_last_error.clear();
+  if (M < 0 || n < 1 || K < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d K=%d", (long long)M, n, K);
+  if (!h_kinds || !a) return set_error(HOPF_EINVAL, "h_kinds and a (host arrays) are required");
+  for (int i = 0; i < K; i++) {
+    if (h_kinds[i] < 0 || h_kinds[i] > 2) return set_error(HOPF_EINVAL, "unknown H kind %d", h_kinds[i]);
+    if (!finite_pos(a[i])) return set_error(HOPF_EINVAL, "a[%d] must be > 0 and finite", i);
+    if (h_kinds[i] == HOPF_H_WL1 && !W) return set_error(HOPF_EINVAL, "W is required for HOPF_H_WL1");
+  }
+  if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
+  if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
+  if (n > 1024) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", n);
+  if (M == 0) return HOPF_OK;
+  if (!X || !t || !Dj || !phi || !grad || !iters) return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  float *ts = nullptr, *phs = nullptr, *gs = nullptr;
+  int32_t *its = nullptr;
+  if (cudaMallocAsync((void **)&ts, sizeof(float) * M, st) != cudaSuccess ||
+      (K > 1 && (cudaMallocAsync((void **)&phs, sizeof(float) * M, st) != cudaSuccess ||
+                 cudaMallocAsync((void **)&gs, sizeof(float) * M * n, st) != cudaSuccess ||
+                 cudaMallocAsync((void **)&its, sizeof(int32_t) * M, st) != cudaSuccess)))
+    return set_error(HOPF_ECUDA, "scratch allocation failed");
+  const int nb = num_sms() * 8;
+  int rc = HOPF_OK;
+  for (int i = 0; i < K && rc == HOPF_OK; i++) {
+    // phi_i: the diag solve with H_i = a_i H_kind(.; w_i), as (a_i t) H_kind
+    hopf_scale_t_kernel<<<nb, 256, 0, st>>>(M, t, a[i], ts);
+    DiagParams p{};
+    p.M = M; p.n = n; p.X = X; p.t = ts; p.D = Dj; p.c = c;
+    p.w = h_kinds[i] == HOPF_H_WL1 ? W + (size_t)i * n : nullptr;
+    p.gamma = gamma; p.lambda = lambda; p.max_iter = max_iter; p.tol = tol; p.K = 0;
+    p.phi = i == 0 ? phi : phs; p.grad = i == 0 ? grad : gs; p.iters = i == 0 ? iters : its;
+    rc = launch_diag_like(p, (hopf_h_kind)h_kinds[i], false, st);
+    if (rc != HOPF_OK) break;
+    if (i == 0) {
+      if (istar) hopf_istar_init_kernel<<<nb, 256, 0, st>>>(M, iters, istar);
+    } else {
+      hopf_maxh_combine_kernel<<<nb, 256, 0, st>>>(M, n, i, phs, gs, its, phi, grad, iters, istar);
+    }
+  }
+  cudaFreeAsync(ts, st);
+  if (phs) cudaFreeAsync(phs, st);
+  if (gs) cudaFreeAsync(gs, st);
+  if (its) cudaFreeAsync(its, st);
+  if (rc != HOPF_OK) return rc;
+  g_launches = 3 * K - (istar ? 0 : 1);   // K scale, K solve, K-1 combine (+ istar init)
+  g_last_kernel = "hopf_diag kernels + hopf_maxh_combine_kernel";
+  return check_launch("hopf_maxh_combine_kernel");
 }
 
 int hopf_set_iteration_counter(unsigned long long *counter) {

@@ -122,6 +122,13 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
                       ("uniform", -3.0, 3.0), ("uniform", 0.1, 2.0),
                       D=np.ones(n, np.float32), gamma=0.0)
         return wl
+    if name == "c2h":
+        # NEXT-4: C2's J and points with H = min(sum w_j |p_j|, 1.2 ||p||_2, 0.8 ||p||_1)
+        wl = config("c2", M=M, n=n, seed=seed)
+        wl.name, wl.kind = "c2h", "maxh"
+        wl.maxh = (["wl1", "l2", "l1"], np.array([1.0, 1.2, 0.8], np.float32),
+                   np.stack([wl.w, np.ones_like(wl.w), np.ones_like(wl.w)]).astype(np.float32))
+        return wl
     if name in ("c2", "c3"):
         num = 2 if name == "c2" else 3
         n = n or (100 if num == 2 else 1000)
@@ -130,8 +137,9 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
         D = _loguniform(rng, 0.5, 2.0, n).astype(np.float32)
         if num == 2:
             w = rng.uniform(0.5, 1.5, n).astype(np.float32)
-            return Workload("c2", n, M or 1_000_000, h or "wl1", "diag", seed,
-                            ("normal", 2.0), ("uniform", 0.0, 1.0), D=D, w=w, gamma=-0.5)
+            if name == "c2":
+                return Workload("c2", n, M or 1_000_000, h or "wl1", "diag", seed,
+                                ("normal", 2.0), ("uniform", 0.0, 1.0), D=D, w=w, gamma=-0.5)
         return Workload("c3", n, M or 100_000, h or "l2", "diag", seed,
                         ("normal", 1.0), ("uniform", 0.0, 2.0), D=D, gamma=-0.5)
     if name == "c4":
@@ -171,4 +179,4 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h")

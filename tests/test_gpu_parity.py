@@ -406,3 +406,24 @@ def test_iteration_counter_matches_iters(hb):
         ik = itk.cpu().numpy()
         total += int(np.abs(ik[ik != oracle.INVALID]).sum())
     assert int(cnt.item()) == total
+
+
+# ----------------------------------------------------------------- max over min of H (NEXT-4)
+def test_maxh_mixed_hamiltonians(hb):
+    """H = min(sum w_j |p_j|, 1.2 ||p||_2, 0.8 ||p||_1) with C2's ellipsoid J: phi,
+    grad, iters and the winner against the oracle's max_i phi_i; t == 0 and invalid points."""
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 3000)
+    X, t = X.copy(), t.copy()
+    t[0] = 0.0
+    X[1, 7] = np.nan
+    kinds, a = ["wl1", "l2", "l1"], np.array([1.0, 1.2, 0.8], np.float32)
+    W = np.stack([wl.w, np.ones_like(wl.w), np.ones_like(wl.w)]).astype(np.float32)
+    phi, grad, it, ist = hb.eval_maxh(dev(X), dev(t), dev(wl.D), None, wl.gamma, kinds, a, dev(W))
+    o = oracle.eval_maxh(X, t, wl.D, None, wl.gamma, kinds, a, W)
+    ist_g, ist_o = ist.cpu().numpy(), o[3]
+    same = ist_g == ist_o
+    # a different winner is accepted only at a near tie of the phi_i
+    assert np.mean(same) > 0.98
+    check(phi[same], grad[same], it[same], o[0][same], o[1][same], o[2][same])
+    assert ist_g[1] == -1 and it.cpu().numpy()[0] == 0
