@@ -274,3 +274,34 @@ def union_distance_exact(y, Dk, Ck, gammak):
         if d < best[0]:
             best = (d, z, k)
     return best
+
+
+# --------------------------------------------------------------------------- ellipsoidal H (NEXT-2)
+def diag_ell_secular(x, t, D, W, c=None, gamma=0.0, iters=200):
+    """J = 1/2<x-c, D^{-1}(x-c)> + gamma, H(p) = sqrt(<p, W p>) (W, D diagonal > 0).
+
+    Plain definition: the maximiser v of <xt,v> - 1/2<v,Dv> - t ||v||_W satisfies
+    xt - D v = t W v / s with s = ||v||_W > 0, so v_i = xt_i s / (D_i s + t W_i) and
+    h(s) = sum_i W_i xt_i^2 / (D_i s + t W_i)^2 = 1 (h strictly decreasing); v = 0 when
+    h(0+) = sum_i xt_i^2 / (t^2 W_i) <= 1.  Bisection on s.  Returns (phi, grad)."""
+    xt = np.asarray(x, np.float64) - (0.0 if c is None else np.asarray(c, np.float64))
+    D = np.asarray(D, np.float64)
+    W = np.asarray(W, np.float64)
+    if t <= 0 or np.sum(xt * xt / (t * t * W)) <= 1.0:
+        v = np.zeros_like(xt) if t > 0 else xt / D
+        phi = gamma + (0.5 * np.sum(xt * xt / D) if t <= 0 else 0.0)
+        return phi, v
+    h = lambda s: np.sum(W * xt * xt / (D * s + t * W) ** 2) - 1.0
+    lo, hi = 0.0, 1.0
+    while h(hi) > 0:
+        hi *= 2.0
+    for _ in range(iters):
+        mid = 0.5 * (lo + hi)
+        if h(mid) > 0:
+            lo = mid
+        else:
+            hi = mid
+    s = 0.5 * (lo + hi)
+    v = xt * s / (D * s + t * W)
+    phi = xt @ v - 0.5 * v @ (D * v) - t * np.sqrt(v @ (W * v)) + gamma
+    return float(phi), v

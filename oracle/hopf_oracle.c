@@ -52,6 +52,7 @@
 #define ORACLE_H_L1 0
 #define ORACLE_H_WL1 1
 #define ORACLE_H_L2 2
+#define ORACLE_H_ELL 3 /* NEXT-2: H(p) = sqrt(<p, W p>), W = diag(w) > 0 */
 
 /* ---------------- prox of t/lambda * H (3.4b) ---------------------------- */
 
@@ -77,9 +78,37 @@ static void shrink2(int n, const double *u, double alpha, double *out) {
   for (int i = 0; i < n; i++) out[i] = u[i] * f;
 }
 
+/* prox of tau ||.||_W, W = diag(w) (NEXT-2): Moreau gives
+ * prox(u) = u - tau Pi_E(u / tau) with E = {y : <y, W^{-1} y> <= 1} the dual ball (semi-axes
+ * d_i = sqrt(w_i)); outside E, Pi_E(z)_i = d_i^2 z_i / (d_i^2 + mu) with mu the root of
+ * sum_i d_i^2 z_i^2 / (d_i^2 + mu)^2 = 1, found as the paper does: Newton on
+ * mu -> sum_i d_i^2 z_i^2 / (d_i^2 + mu) + mu from mu_0 = 0, stopping at |mu_{k+1} - mu_k| <= 1e-8. */
+static void prox_ell(int n, const double *u, double tau, const double *w, double *out) {
+  if (!(tau > 0.0)) { memcpy(out, u, sizeof(double) * n); return; }
+  double q = 0.0;
+  for (int i = 0; i < n; i++) { double z = u[i] / tau; q += z * z / w[i]; }
+  if (q <= 1.0) { for (int i = 0; i < n; i++) out[i] = 0.0; return; }
+  double mu = 0.0;
+  for (int it = 0; it < 1000; it++) {
+    double f1 = 0.0, f2 = 0.0;
+    for (int i = 0; i < n; i++) {
+      double z = u[i] / tau, e = w[i] + mu;
+      f1 += w[i] * z * z / (e * e);
+      f2 += w[i] * z * z / (e * e * e);
+    }
+    double mn = mu - (1.0 - f1) / (2.0 * f2);   /* Newton on the derivative 1 - f1 */
+    int done = fabs(mn - mu) <= 1e-8;
+    mu = mn;
+    if (done) break;
+  }
+  for (int i = 0; i < n; i++) out[i] = u[i] - tau * (w[i] * (u[i] / tau) / (w[i] + mu));
+}
+
 static void prox_tH(int n, int h, const double *u, double t, const double *w,
                     double lambda, double *alpha_buf, double *out) {
-  if (h == ORACLE_H_L2) {
+  if (h == ORACLE_H_ELL) {
+    prox_ell(n, u, t / lambda, w, out);
+  } else if (h == ORACLE_H_L2) {
     shrink2(n, u, t / lambda, out);
   } else {
     for (int i = 0; i < n; i++)
@@ -90,6 +119,10 @@ static void prox_tH(int n, int h, const double *u, double t, const double *w,
 
 static double H_of(int n, int h, const double *p, const double *w) {
   double s = 0.0;
+  if (h == ORACLE_H_ELL) {
+    for (int i = 0; i < n; i++) s += w[i] * p[i] * p[i];
+    return sqrt(s);
+  }
   if (h == ORACLE_H_L2) {
     for (int i = 0; i < n; i++) s += p[i] * p[i];
     return sqrt(s);
@@ -191,7 +224,8 @@ int oracle_diag(int64_t M, int n, const double *X, const double *t, const double
                 int max_iter, double tol, double *phi, double *grad, int32_t *iters,
                 int nthreads) {
   if (M < 0 || n < 1 || !D || lambda <= 0.0 || max_iter < 1 || tol < 0.0) return -1;
-  if (h == ORACLE_H_WL1 && !w) return -1;
+  if ((h == ORACLE_H_WL1 || h == ORACLE_H_ELL) && !w) return -1;
+  if (h < 0 || h > ORACLE_H_ELL) return -1;
   int nt = nthreads_or_default(nthreads);
 #pragma omp parallel num_threads(nt)
   {
@@ -273,7 +307,8 @@ int oracle_dense(int64_t M, int n, const double *X, const double *t, const doubl
                  int32_t *iters, int nthreads) {
   if (M < 0 || n < 1 || !Ml || !A || !Ainv || lambda <= 0.0 || max_iter < 1 || tol < 0.0)
     return -1;
-  if (h == ORACLE_H_WL1 && !w) return -1;
+  if ((h == ORACLE_H_WL1 || h == ORACLE_H_ELL) && !w) return -1;
+  if (h < 0 || h > ORACLE_H_ELL) return -1;
   int nt = nthreads_or_default(nthreads);
 #pragma omp parallel num_threads(nt)
   {
@@ -298,7 +333,8 @@ int oracle_union(int64_t M, int n, int K, const double *X, const double *t, cons
   if (M < 0 || n < 1 || K < 1 || !Dk || !Ck || !gammak || lambda <= 0.0 || max_iter < 1 ||
       tol < 0.0)
     return -1;
-  if (h == ORACLE_H_WL1 && !w) return -1;
+  if ((h == ORACLE_H_WL1 || h == ORACLE_H_ELL) && !w) return -1;
+  if (h < 0 || h > ORACLE_H_ELL) return -1;
   if (Y && h != ORACLE_H_L2) return -1;
   int nt = nthreads_or_default(nthreads);
 #pragma omp parallel num_threads(nt)

@@ -375,3 +375,38 @@ def test_maxh_matches_hopf_formula_with_min_hamiltonian_2d():
         ref, vbest = exact.hopf_dual_grid_2d(X[i], t[i], Jstar, Hmin, 8.0)
         assert abs(phi[i] - ref) <= 1e-6 * max(1.0, abs(ref)), (i, phi[i], ref)
         np.testing.assert_allclose(grad[i], vbest, atol=1e-3)
+
+
+# ----------------------------------------------------------------- ellipsoidal-norm H (NEXT-2)
+def test_ell_hamiltonian_matches_secular_reference():
+    """H(p) = sqrt(<p, W p>) (Moreau + projection on the dual ellipsoid by Newton
+    on mu from mu_0 = 0): against the plain optimality condition solved by bisection."""
+    rng = np.random.default_rng(41)
+    n, M = 9, 60
+    D = np.exp(rng.uniform(np.log(0.5), np.log(2.0), n))
+    W = np.exp(rng.uniform(np.log(0.3), np.log(3.0), n))
+    c = rng.normal(size=n)
+    X = rng.normal(0, 2, (M, n))
+    t = rng.uniform(0.05, 2.0, M)
+    t[0] = 0.0
+    X[1] = c + 0.01   # inside t W-ball: grad 0
+    phi, grad, it = oracle.eval_diag(X, t, D, c, -0.5, "ell", W, tol=1e-22, max_iter=20000)
+    for i in range(M):
+        pe, ge = exact.diag_ell_secular(X[i], t[i], D, W, c, -0.5)
+        assert abs(phi[i] - pe) <= 1e-9 * max(1.0, abs(pe)), i
+        np.testing.assert_allclose(grad[i], ge, atol=1e-6)
+    assert it[0] == 0 and np.all(grad[1] == 0.0)
+
+
+def test_ell_with_identity_weights_is_l2():
+    """W = I: ||.||_W = ||.||_2, the prox by ellipsoid projection must reproduce shrink_2."""
+    rng = np.random.default_rng(42)
+    n, M = 12, 200
+    D = np.exp(rng.uniform(np.log(0.5), np.log(2.0), n))
+    X = rng.normal(0, 1.5, (M, n))
+    t = rng.uniform(0.1, 2.0, M)
+    a = oracle.eval_diag(X, t, D, None, -0.5, "ell", np.ones(n))
+    b = oracle.eval_diag(X, t, D, None, -0.5, "l2")
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-7, atol=1e-7)
+    np.testing.assert_allclose(a[1], b[1], atol=1e-5)
+    assert np.mean(np.abs(a[2] - b[2]) <= 1) > 0.95
