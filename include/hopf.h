@@ -55,11 +55,14 @@ enum {
   HOPF_ECUDA = -3
 };
 
-/* Hamiltonians (support functions of a box / a ball):
+/* Hamiltonians (support functions of a box / a ball / an ellipsoid):
  *   HOPF_H_L1  : H(p) = sum_i |p_i|        (shrink_1, threshold t/lambda)
  *   HOPF_H_WL1 : H(p) = sum_i w_i |p_i|    (shrink_1, threshold t w_i/lambda), w_i > 0
- *   HOPF_H_L2  : H(p) = ||p||_2            (shrink_2, threshold t/lambda)              */
-typedef enum { HOPF_H_L1 = 0, HOPF_H_WL1 = 1, HOPF_H_L2 = 2 } hopf_h_kind;
+ *   HOPF_H_L2  : H(p) = ||p||_2            (shrink_2, threshold t/lambda)
+ *   HOPF_H_ELL : H(p) = sqrt(<p, diag(w) p>), w_i > 0  (NEXT-2: prox by projection on the dual
+ *                ellipsoid, Newton on its multiplier); hopf_eval_diag and
+ *                hopf_eval_maxh only (hopf_eval_union returns HOPF_EUNSUPPORTED)            */
+typedef enum { HOPF_H_L1 = 0, HOPF_H_WL1 = 1, HOPF_H_L2 = 2, HOPF_H_ELL = 3 } hopf_h_kind;
 
 /* Diagonal (ellipsoidal) initial data:
  *   J(x) = 1/2 <x - c, diag(Dj)^{-1} (x - c)> + gamma,  J*(v) = 1/2 <v, Dj v> + <c, v> - gamma
@@ -68,7 +71,7 @@ typedef enum { HOPF_H_L1 = 0, HOPF_H_WL1 = 1, HOPF_H_L2 = 2 } hopf_h_kind;
  *   X [M*n]   query points;  t [M] times (t >= 0)
  *   Dj [n]    diagonal of J's curvature inverse (> 0);  c [n] centre or NULL (= 0)
  *   gamma     additive constant of J
- *   h, w      Hamiltonian kind and weights w [n] (HOPF_H_WL1 only, else ignored / may be NULL)
+ *   h, w      Hamiltonian kind and weights w [n] (HOPF_H_WL1 / HOPF_H_ELL, else may be NULL)
  *   lambda    split Bregman penalty (> 0; the paper uses 1)
  *   max_iter  iteration cap (>= 1); tol squared-norm stopping threshold (>= 0, paper 1e-8)
  *   phi [M], grad [M*n], iters [M]   outputs                                               */
@@ -98,7 +101,7 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
  * the lowest i winning ties; grad = the winner's gradient, iters = its status.
  *   K (>= 1)       number of Hamiltonians
  *   h_kinds [K]    HOST array of hopf_h_kind;  a [K] HOST array of scales a_i > 0
- *   W [K*n]        DEVICE weights (row i used when h_kinds[i] == HOPF_H_WL1), else may be NULL
+ *   W [K*n]        DEVICE weights (row i used when h_kinds[i] is HOPF_H_WL1 / HOPF_H_ELL), else may be NULL
  *   H_i(p) = a_i H_{kind_i}(p; W_i); evaluated as the kind's solve at time a_i t (t a_i H = (a_i t) H)
  *   istar [M] or NULL   index of the winning Hamiltonian (-1 on invalid points)
  * Other arguments as hopf_eval_diag.  Launches K solves + K combine steps on `stream`

@@ -482,7 +482,7 @@ int oracle_distance_union(int64_t M, int n, int K, const double *Yq, const doubl
 /* H = min_i a_i H_{kind_i}(.; w_i) with one diagonal J: phi = max_i phi_i, each phi_i
  * the split Bregman solve with H_i (its prox threshold t a_i w_ij / lambda, its t H_i(d) term in
  * (3.3)); grad = grad of the winner; the lowest i wins ties (as R19).  kinds[K], a[K] host
- * arrays, W [K*n] weights (rows used for ORACLE_H_WL1 only). */
+ * arrays, W [K*n] weights (rows used for ORACLE_H_WL1 / ORACLE_H_ELL only). */
 int oracle_maxh(int64_t M, int n, const double *X, const double *t, const double *D,
                 const double *c, double gamma, int K, const int32_t *kinds, const double *W,
                 const double *a, double lambda, int max_iter, double tol, double *phi,
@@ -490,8 +490,8 @@ int oracle_maxh(int64_t M, int n, const double *X, const double *t, const double
   if (M < 0 || n < 1 || K < 1 || !D || !kinds || !a || lambda <= 0.0 || max_iter < 1 || tol < 0.0)
     return -1;
   for (int i = 0; i < K; i++) {
-    if (kinds[i] < 0 || kinds[i] > 2 || !(a[i] > 0.0)) return -1;
-    if (kinds[i] == ORACLE_H_WL1 && !W) return -1;
+    if (kinds[i] < 0 || kinds[i] > ORACLE_H_ELL || !(a[i] > 0.0)) return -1;
+    if ((kinds[i] == ORACLE_H_WL1 || kinds[i] == ORACLE_H_ELL) && !W) return -1;
   }
   int nt = nthreads_or_default(nthreads);
 #pragma omp parallel num_threads(nt)
@@ -506,12 +506,16 @@ int oracle_maxh(int64_t M, int n, const double *X, const double *t, const double
       int besti = -1, bestit = 0;
       for (int i = 0; i < K; i++) {
         /* H_i = a_i H_kind(.; w_i): an l1 / weighted l1 with weights a_i w_ij, or a_i ||.||_2
-         * (the l2 solve with t H_i = (a_i t) ||.||_2) */
+         * (the l2 solve with t H_i = (a_i t) ||.||_2), or a_i ||.||_{W_i} (the ellipsoidal solve
+         * at time a_i t) */
         double ph, ti = t[p];
         const double *wi = NULL;
         int h = kinds[i];
         if (h == ORACLE_H_L2) {
           ti = t[p] * a[i];
+        } else if (h == ORACLE_H_ELL) {
+          ti = t[p] * a[i];
+          wi = W + (size_t)i * n;
         } else {
           for (int j = 0; j < n; j++) wa[j] = a[i] * (h == ORACLE_H_WL1 ? W[(size_t)i * n + j] : 1.0);
           wi = wa;

@@ -33,7 +33,10 @@
 
 namespace hopf {
 
-enum { HK_L1 = 0, HK_WL1 = 1, HK_L2 = 2 };
+// HK_ELL (NEXT-2): H(p) = sqrt(<p, W p>), W = diag(w) > 0.  (3.4b) is prox_{tau ||.||_W}(u) =
+// u - tau P(u / tau), P the projection on the dual ellipsoid {z : <z, W^-1 z> <= 1}, computed by
+// Newton on its multiplier mu; see the ELL branch of the trip below.
+enum { HK_L1 = 0, HK_WL1 = 1, HK_L2 = 2, HK_ELL = 3 };
 
 struct DiagParams {
   int64_t M;
@@ -193,7 +196,12 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
   __shared__ __align__(16) float2 kap_s[KSM ? NP * G : 1];
   // non-union: D_i, 1/(D_i + lambda) and w_i by coordinate, staged once per CTA for the
   // per-point setup and finalize (they were re-fetched from global per point)
-  __shared__ float D_s[KSM ? G * CPL : 1], di_s[KSM ? G * CPL : 1], w_s[(KSM && HK == HK_WL1) ? G * CPL : 1];
+  constexpr bool WSM = KSM && (HK == HK_WL1 || HK == HK_ELL);
+  __shared__ float D_s[KSM ? G * CPL : 1], di_s[KSM ? G * CPL : 1], w_s[WSM ? G * CPL : 1];
+  // ELL: (w_i, 1/w_i) pairs in the kappa layout; padded slots hold w = 1 (their u is 0)
+  constexpr bool ELL = HK == HK_ELL;
+  static_assert(!(ELL && UNION), "the ellipsoidal Hamiltonian is instantiated for hopf_eval_diag only");
+  __shared__ __align__(16) float2 w2_s[ELL ? NP * G : 1], wi2_s[ELL ? NP * G : 1];
   const float ksign = (HK == HK_L2) ? -1.f : 1.f;
   if (KSM) {
     for (int e = threadIdx.x; e < NP * G; e += blockDim.x) {
@@ -208,9 +216,25 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       const float Dv = i < n ? __ldg(p.D + i) : 1.f;
       D_s[i] = Dv;
       di_s[i] = __fdividef(1.f, Dv + lam);
-      if (HK == HK_WL1) w_s[i] = i < n ? __ldg(p.w + i) : 0.f;
+      if (WSM) w_s[i] = i < n ? __ldg(p.w + i) : 0.f;
+    }
+    if (ELL) {
+      for (int e = threadIdx.x; e < NP * G; e += blockDim.x) {
+        const int pp = e / G, l = e % G;
+        const int i0 = l + G * (2 * pp), i1 = l + G * (2 * pp + 1);
+        const float w0 = (2 * pp < CPL && i0 < n) ? __ldg(p.w + i0) : 1.f;
+        const float w1 = (2 * pp + 1 < CPL && i1 < n) ? __ldg(p.w + i1) : 1.f;
+        w2_s[e] = make_float2(w0, w1);
+        wi2_s[e] = make_float2(1.f / w0, 1.f / w1);
+      }
     }
     __syncthreads();
+  }
+  // ELL: min_i w_i, the scale of the Newton stopping test on mu
+  float wmin = 1.f;
+  if (ELL) {
+    wmin = __int_as_float(0x7f800000);
+    for (int i = 0; i < n; i++) wmin = fminf(wmin, w_s[i]);
   }
 
   int64_t pt = gid;
@@ -223,6 +247,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
   float tauS = 0.f;     // scalar threshold t/lambda
   int spec = 0;         // 0 normal, 1 t == 0, 2 invalid
   float s_cur = 1.f;    // l2: shrink factor of the pending (3.4b)
+  float mu = 0.f;       // ELL: multiplier of the last projection (warm start of the next)
   bool sv_ok = false;   // l2: ||v^k - v^{k-1}||^2 <= tol of the pending iteration
   float best = 0.f;
   int bestk = -1, bestit = 0;
@@ -293,6 +318,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     }
     it = 0;
     s_cur = 1.f;
+    mu = 0.f;
     sv_ok = false;
     waiting = false;
   };
@@ -370,8 +396,72 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
         }
       }
     };
-    if (full_test) trip(std::true_type{});
-    else trip(std::false_type{});
+    if constexpr (ELL) {
+      // (3.4a) and u = v + b for every coordinate; b holds u until the projection is known
+      float2 qacc = splat2(0.f);
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const float2 kq = lds_volatile2(kap_s + q * G + gl);
+        const float2 a = sub2(d[q], b[q]);
+        const float2 t = sub2(xh[q], v[q]);
+        const float2 dv = fma2(kq, a, t);
+        v[q] = add2(v[q], dv);
+        const float2 u = add2(v[q], b[q]);
+        b[q] = u;
+        c0 = fma2(dv, dv, c0);
+        qacc = fma2(__fmul2_rn(u, lds_volatile2(wi2_s + q * G + gl)), u, qacc);
+      }
+      // u / tau inside the dual ellipsoid <z, W^-1 z> <= 1  <=>  sum u_i^2 / w_i <= tau^2:
+      // prox = 0 (mu = 0 below gives d' = 0 exactly).  Otherwise the projection of z = u / tau
+      // is w z / (w + mu) with mu > 0 the root of F(mu) = sum w u^2 / (w + mu)^2 - tau^2; Newton
+      // mu <- mu + (S1 - tau^2) / (2 S2), S2 = sum w u^2 / (w + mu)^3, warm-started at the previous
+      // iteration's mu and clamped at 0 (F convex decreasing: from the right of the root one step
+      // lands left of it, from the left Newton is monotone), stopped when the step is below
+      // 1e-6 (mu + min w) (the oracle starts at 0 and stops at |step| <= 1e-8; reading R27)
+      const float qn = group_sum<G>(qacc.x + qacc.y);
+      const float tau2 = tauS * tauS;
+      const bool outside = qn > tau2;
+      bool act = have && !waiting && spec == 0 && outside;
+      int nit = 0;
+      while (__any_sync(0xffffffffu, act)) {
+        float2 s1 = splat2(0.f), s2 = splat2(0.f);
+        const float2 muP = splat2(mu);
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          const float2 w = lds_volatile2(w2_s + q * G + gl);
+          const float2 e = add2(w, muP);
+          const float2 r = make_float2(__frcp_rn(e.x), __frcp_rn(e.y));
+          const float2 h = __fmul2_rn(b[q], r);           // u / (w + mu)
+          const float2 wh2 = __fmul2_rn(__fmul2_rn(w, h), h);
+          s1 = add2(s1, wh2);
+          s2 = fma2(wh2, r, s2);
+        }
+        const float S1 = group_sum<G>(s1.x + s1.y), S2 = group_sum<G>(s2.x + s2.y);
+        if (act) {
+          const float mun = fmaxf(fmaf(S1 - tau2, __frcp_rn(2.f * S2), mu), 0.f);
+          act = !(fabsf(mun - mu) <= 1e-6f * (mun + wmin)) && ++nit < 40;
+          mu = mun;
+        }
+      }
+      // (3.4b): d' = u - w u / (w + mu) = mu u / (w + mu);  (3.4c): b' = u - d'
+      const float2 muP = splat2(outside ? mu : 0.f);
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const float2 w = lds_volatile2(w2_s + q * G + gl);
+        const float2 e = add2(w, muP);
+        const float2 r = make_float2(__frcp_rn(e.x), __frcp_rn(e.y));
+        const float2 u = b[q];
+        const float2 dn = __fmul2_rn(__fmul2_rn(muP, u), r);
+        b[q] = sub2(u, dn);
+        const float2 dd = sub2(dn, d[q]);
+        d[q] = fma2(dd, splat2(live), d[q]);
+        a0 = fma2(dd, dd, a0);
+      }
+    } else if (full_test) {
+      trip(std::true_type{});
+    } else {
+      trip(std::false_type{});
+    }
     const float psd = a0.x + a0.y, psb = b0.x + b0.y;
     const float psv = c0.x + c0.y, pr2 = r0.x + r0.y;
     bool conv;
@@ -447,6 +537,8 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
           qs = fmaf(xt1, dq.y, qs);
           qs = fmaf(-0.5f * D1 * dq.y, dq.y, qs);
           if (HK == HK_L2) hsum = fmaf(dq.x, dq.x, fmaf(dq.y, dq.y, hsum));
+          else if (ELL)
+            hsum = fmaf((ok0 ? w_s[i0] : 0.f) * dq.x, dq.x, fmaf((ok1 ? w_s[i1] : 0.f) * dq.y, dq.y, hsum));
           else if (HK == HK_WL1)
             hsum = fmaf(ok0 ? (KSM ? w_s[i0] : __ldg(p.w + i0)) : 0.f, fabsf(dq.x),
                         fmaf(ok1 ? (KSM ? w_s[i1] : __ldg(p.w + i1)) : 0.f, fabsf(dq.y), hsum));
@@ -460,7 +552,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     const float gam = UNION ? __ldg(p.gk + kset) : p.gamma;
     float phiv;
     if (spec == 1) phiv = qs + gam;
-    else phiv = qs - tt * (HK == HK_L2 ? sqrtf(hsum) : hsum) + gam;
+    else phiv = qs - tt * ((HK == HK_L2 || ELL) ? sqrtf(hsum) : hsum) + gam;
     if (spec == 2) phiv = __int_as_float(0x7fc00000);
 
     bool point_done = done;

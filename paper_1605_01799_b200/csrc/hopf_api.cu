@@ -58,6 +58,7 @@ using KernFn = void (*)(const DiagParams);
 struct Variant {
   int G, CPL;
   KernFn fn[3][2];  // [h kind][union]
+  KernFn ell;       // HOPF_H_ELL, hopf_eval_diag only
 };
 
 // union kernels keep x and the best grad resident too: only CPL <= 16 is instantiated
@@ -70,7 +71,8 @@ constexpr KernFn union_fn() {
   {G_, C_,                                                                                   \
    {{hopf_diag_kernel<G_, C_, HK_L1, false>, union_fn<G_, C_, HK_L1>()},                     \
     {hopf_diag_kernel<G_, C_, HK_WL1, false>, union_fn<G_, C_, HK_WL1>()},                   \
-    {hopf_diag_kernel<G_, C_, HK_L2, false>, union_fn<G_, C_, HK_L2>()}}}
+    {hopf_diag_kernel<G_, C_, HK_L2, false>, union_fn<G_, C_, HK_L2>()}},                    \
+   hopf_diag_kernel<G_, C_, HK_ELL, false>}
 
 // Ordered by padded width G*CPL (roughly), then G: the first variant with G*CPL >= n is used.
 // (8, 13) precedes (4, 25): for C2 (n = 100) its 127 registers give 4 warps per SMSP instead of 3
@@ -158,9 +160,11 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   const Variant *v = pick_variant(p.n, is_union);
   if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
   static const char *tm_env = getenv("HOPF_DIAG_TM");
-  if (!is_union && v->G == 32 && v->CPL == 32 && !(tm_env && strcmp(tm_env, "0") == 0))
+  const bool ell = h == HOPF_H_ELL;
+  if (ell && is_union) return set_error(HOPF_EUNSUPPORTED, "HOPF_H_ELL is supported by hopf_eval_diag only");
+  if (!ell && !is_union && v->G == 32 && v->CPL == 32 && !(tm_env && strcmp(tm_env, "0") == 0))
     return launch_diag_tm(p, h, stream);
-  KernFn fn = v->fn[(int)h][is_union ? 1 : 0];
+  KernFn fn = ell ? v->ell : v->fn[(int)h][is_union ? 1 : 0];
   // Block size: the one that keeps the most warps resident per SM (register-limited kernels
   // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
   struct Occ { int threads, per_sm; };
@@ -192,7 +196,7 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   g_launches += 1;
   g_last_threads = threads;
   g_last_blocks = (int)blocks;
-  g_last_kernel = is_union ? "hopf_diag_kernel<union>" : "hopf_diag_kernel";
+  g_last_kernel = is_union ? "hopf_diag_kernel<union>" : (ell ? "hopf_diag_kernel<ell>" : "hopf_diag_kernel");
   return check_launch("hopf_diag_kernel");
 }
 
@@ -211,11 +215,11 @@ int hopf_eval_diag(int64_t M, int32_t n, const float *X, const float *t, const f
   g_launches = 0;
   g_last_error.clear();
   if (M < 0 || n < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d", (long long)M, n);
-  if ((int)h < 0 || (int)h > 2) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
+  if ((int)h < 0 || (int)h > 3) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
   if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
   if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
-  if (h == HOPF_H_WL1 && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1");
+  if ((h == HOPF_H_WL1 || h == HOPF_H_ELL) && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1 / HOPF_H_ELL");
   if (M == 0) return HOPF_OK;
   if (!X || !t || !Dj || !phi || !grad || !iters)
     return set_error(HOPF_EINVAL, "a required pointer is NULL");
@@ -234,11 +238,11 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
   g_launches = 0;
   g_last_error.clear();
   if (M < 0 || n < 1 || K < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d K=%d", (long long)M, n, K);
-  if ((int)h < 0 || (int)h > 2) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
+  if ((int)h < 0 || (int)h > 3) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
   if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
   if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
-  if (h == HOPF_H_WL1 && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1");
+  if ((h == HOPF_H_WL1 || h == HOPF_H_ELL) && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1 / HOPF_H_ELL");
   if (Y && h != HOPF_H_L2) return set_error(HOPF_EINVAL, "Y (closest point) requires HOPF_H_L2");
   if (K > 64 || n > 256) return set_error(HOPF_EUNSUPPORTED, "union supports K<=64, n<=256");
   if (M == 0) return HOPF_OK;
@@ -288,9 +292,10 @@ int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const f
   if (M < 0 || n < 1 || K < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d K=%d", (long long)M, n, K);
   if (!h_kinds || !a) return set_error(HOPF_EINVAL, "h_kinds and a (host arrays) are required");
   for (int i = 0; i < K; i++) {
-    if (h_kinds[i] < 0 || h_kinds[i] > 2) return set_error(HOPF_EINVAL, "unknown H kind %d", h_kinds[i]);
+    if (h_kinds[i] < 0 || h_kinds[i] > 3) return set_error(HOPF_EINVAL, "unknown H kind %d", h_kinds[i]);
     if (!finite_pos(a[i])) return set_error(HOPF_EINVAL, "a[%d] must be > 0 and finite", i);
-    if (h_kinds[i] == HOPF_H_WL1 && !W) return set_error(HOPF_EINVAL, "W is required for HOPF_H_WL1");
+    if ((h_kinds[i] == HOPF_H_WL1 || h_kinds[i] == HOPF_H_ELL) && !W)
+      return set_error(HOPF_EINVAL, "W is required for HOPF_H_WL1 / HOPF_H_ELL");
   }
   if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
@@ -313,7 +318,7 @@ int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const f
     hopf_scale_t_kernel<<<nb, 256, 0, st>>>(M, t, a[i], ts);
     DiagParams p{};
     p.M = M; p.n = n; p.X = X; p.t = ts; p.D = Dj; p.c = c;
-    p.w = h_kinds[i] == HOPF_H_WL1 ? W + (size_t)i * n : nullptr;
+    p.w = (h_kinds[i] == HOPF_H_WL1 || h_kinds[i] == HOPF_H_ELL) ? W + (size_t)i * n : nullptr;
     p.gamma = gamma; p.lambda = lambda; p.max_iter = max_iter; p.tol = tol; p.K = 0;
     p.phi = i == 0 ? phi : phs; p.grad = i == 0 ? grad : gs; p.iters = i == 0 ? iters : its;
     rc = launch_diag_like(p, (hopf_h_kind)h_kinds[i], false, st);

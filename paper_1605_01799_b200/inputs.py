@@ -129,6 +129,11 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
         wl.maxh = (["wl1", "l2", "l1"], np.array([1.0, 1.2, 0.8], np.float32),
                    np.stack([wl.w, np.ones_like(wl.w), np.ones_like(wl.w)]).astype(np.float32))
         return wl
+    if name == "c2e":
+        # NEXT-2: C2's J and points with H(p) = sqrt(<p, diag(w) p>), w = C2's weights
+        wl = config("c2", M=M, n=n, seed=seed, h="ell")
+        wl.name = "c2e"
+        return wl
     if name in ("c2", "c3"):
         num = 2 if name == "c2" else 3
         n = n or (100 if num == 2 else 1000)
@@ -179,4 +184,4 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h", "c2e")

@@ -80,7 +80,7 @@ def test_diag_configs_subset(hb, name, M):
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13, 16, 17, 31, 33, 64, 100, 127, 200, 255, 256,
                                300, 511, 777, 1000, 1024])
-@pytest.mark.parametrize("h", ["l1", "wl1", "l2"])
+@pytest.mark.parametrize("h", ["l1", "wl1", "l2", "ell"])
 def test_diag_ragged_dimensions(hb, n, h):
     """Every compiled lane-group variant, ragged tails, shifted centre c and lambda != 1."""
     rng = np.random.default_rng(n * 7 + len(h))
@@ -427,3 +427,52 @@ def test_maxh_mixed_hamiltonians(hb):
     assert np.mean(same) > 0.98
     check(phi[same], grad[same], it[same], o[0][same], o[1][same], o[2][same])
     assert ist_g[1] == -1 and it.cpu().numpy()[0] == 0
+
+
+# ----------------------------------------------------------------- ellipsoidal-norm H (NEXT-2)
+def test_ell_c2e_subset_and_edges(hb):
+    """H(p) = sqrt(<p, diag(w) p>) on C2's J and points, with t == 0, invalid
+    points, a point inside the t-ellipsoid (grad = 0) and max_iter exhaustion."""
+    wl = inputs.config("c2e")
+    X, t = inputs.points(wl, 0, 20000)
+    X, t = X.copy(), t.copy()
+    t[0] = 0.0
+    X[1, 3] = np.nan
+    t[2] = -1.0
+    X[4] = 0.0
+    t[5] = 1e4
+    g = run_diag(hb, wl, X, t)
+    o = oracle_diag(wl, X, t)
+    check(*g, *o)
+    assert np.all(g[1][5].cpu().numpy() == 0) and abs(g[0][5].item() - wl.gamma) < 1e-6
+    g2 = run_diag(hb, wl, X, t, max_iter=4)
+    o2 = oracle_diag(wl, X, t, max_iter=4)
+    ok = o2[2] != oracle.INVALID
+    np.testing.assert_allclose(g2[1].cpu().numpy()[ok], o2[1][ok], atol=1e-4)
+    with pytest.raises(hb.HopfError):
+        hb.eval_union(dev(X[:8, :64]), dev(t[:8]), dev(np.ones((2, 64), np.float32)),
+                      dev(np.zeros((2, 64), np.float32)), dev(np.zeros(2, np.float32)), "ell",
+                      dev(np.ones(64, np.float32)))
+
+
+def test_ell_identity_weights_match_l2_gpu(hb):
+    """W = I: the ellipsoid projection must give the l2 kernel's results."""
+    wl = inputs.config("c3", n=300)
+    X, t = inputs.points(wl, 0, 2000)
+    a = hb.eval_diag(dev(X), dev(t), dev(wl.D), None, wl.gamma, "ell", dev(np.ones(300, np.float32)))
+    b = hb.eval_diag(dev(X), dev(t), dev(wl.D), None, wl.gamma, "l2")
+    np.testing.assert_allclose(a[0].cpu().numpy(), b[0].cpu().numpy(), rtol=1e-4, atol=1e-4)
+    assert np.abs(a[1].cpu().numpy() - b[1].cpu().numpy()).max() <= 1e-3
+
+
+def test_maxh_with_ellipsoidal_member(hb):
+    """NEXT-4 with an NEXT-2 member: H = min(sqrt(<p, W p>), 0.9 ||p||_1)."""
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 3000)
+    kinds, a = ["ell", "l1"], np.array([1.0, 0.9], np.float32)
+    W = np.stack([wl.w, np.ones_like(wl.w)]).astype(np.float32)
+    phi, grad, it, ist = hb.eval_maxh(dev(X), dev(t), dev(wl.D), None, wl.gamma, kinds, a, dev(W))
+    o = oracle.eval_maxh(X, t, wl.D, None, wl.gamma, kinds, a, W)
+    same = ist.cpu().numpy() == o[3]
+    assert np.mean(same) > 0.98
+    check(phi[same], grad[same], it[same], o[0][same], o[1][same], o[2][same])

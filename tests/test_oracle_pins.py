@@ -410,3 +410,18 @@ def test_ell_with_identity_weights_is_l2():
     np.testing.assert_allclose(a[0], b[0], rtol=1e-7, atol=1e-7)
     np.testing.assert_allclose(a[1], b[1], atol=1e-5)
     assert np.mean(np.abs(a[2] - b[2]) <= 1) > 0.95
+
+
+def test_maxh_ell_member_is_time_scaled_ell_solve():
+    """a ||p||_W with a single Hamiltonian: the ellipsoidal solve at time a t (t a H = (a t) H)."""
+    rng = np.random.default_rng(43)
+    n, M = 7, 40
+    D = rng.uniform(0.5, 2.0, n)
+    W = rng.uniform(0.5, 1.5, (1, n))
+    X = rng.normal(0, 2, (M, n))
+    t = rng.uniform(0.1, 1.0, M)
+    m = oracle.eval_maxh(X, t, D, None, 0.3, ["ell"], np.array([1.7]), W)
+    d = oracle.eval_diag(X, 1.7 * t, D, None, 0.3, "ell", W[0])
+    np.testing.assert_array_equal(m[0], d[0])
+    np.testing.assert_array_equal(m[1], d[1])
+    assert np.all(m[3] == 0)
