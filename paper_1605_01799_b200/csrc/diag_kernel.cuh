@@ -128,6 +128,24 @@ __device__ __forceinline__ void group_reduce4(float v0, float v1, float v2, floa
   }
 }
 
+// Group totals of (S1, S2, sv): S1 and S2 broadcast to every lane of the group, ok_sv = (sv <= tol).
+template <int G>
+__device__ __forceinline__ void group_reduce3(float s1, float s2, float sv, float tol, float &S1,
+                                              float &S2, bool &ok_sv) {
+  const int lane = threadIdx.x & 31;
+  const int base = lane & ~(G - 1);
+  if constexpr (G >= 4) {
+    const float c = group_sum4_transposed<G>(sv, 0.f, s1, s2);
+    ok_sv = (__ballot_sync(0xffffffffu, c <= tol) >> base) & 1u;
+    S1 = __shfl_sync(0xffffffffu, c, base + 2 * (G / 4));
+    S2 = __shfl_sync(0xffffffffu, c, base + 3 * (G / 4));
+  } else {
+    S1 = group_sum<G>(s1);
+    S2 = group_sum<G>(s2);
+    ok_sv = group_sum<G>(sv) <= tol;
+  }
+}
+
 // ---- packed fp32x2 helpers (sm_100 FADD2 / FFMA2: two slots of FP32 work per issue) --------
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 // a - b as one FFMA2 with a broadcast -1 (exact: b * -1 is exact, one rounding of the sum);
@@ -137,6 +155,13 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __
 __device__ __forceinline__ float2 splat2(float s) { return make_float2(s, s); }
 __device__ __forceinline__ float2 clamp2(float2 u, float2 t) {
   return make_float2(fminf(fmaxf(u.x, -t.x), t.x), fminf(fmaxf(u.y, -t.y), t.y));
+}
+
+// MUFU reciprocal (rcp.approx.ftz: ~1 ulp; __frcp_rn adds an IEEE fix-up with a slow path)
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 #define HOPF_SLOT(arr, j) (((j) & 1) ? (arr)[(j) >> 1].y : (arr)[(j) >> 1].x)
@@ -201,7 +226,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
   // ELL: (w_i, 1/w_i) pairs in the kappa layout; padded slots hold w = 1 (their u is 0)
   constexpr bool ELL = HK == HK_ELL;
   static_assert(!(ELL && UNION), "the ellipsoidal Hamiltonian is instantiated for hopf_eval_diag only");
-  __shared__ __align__(16) float2 w2_s[ELL ? NP * G : 1], wi2_s[ELL ? NP * G : 1];
+  __shared__ __align__(16) float2 w2_s[ELL ? NP * G : 1];
   const float ksign = (HK == HK_L2) ? -1.f : 1.f;
   if (KSM) {
     for (int e = threadIdx.x; e < NP * G; e += blockDim.x) {
@@ -225,7 +250,6 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
         const float w0 = (2 * pp < CPL && i0 < n) ? __ldg(p.w + i0) : 1.f;
         const float w1 = (2 * pp + 1 < CPL && i1 < n) ? __ldg(p.w + i1) : 1.f;
         w2_s[e] = make_float2(w0, w1);
-        wi2_s[e] = make_float2(1.f / w0, 1.f / w1);
       }
     }
     __syncthreads();
@@ -396,60 +420,98 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
         }
       }
     };
+    bool ell_ok_sv = false;
     if constexpr (ELL) {
-      // (3.4a) and u = v + b for every coordinate; b holds u until the projection is known
-      float2 qacc = splat2(0.f);
-#pragma unroll
-      for (int q = 0; q < NP; q++) {
-        const float2 kq = lds_volatile2(kap_s + q * G + gl);
-        const float2 a = sub2(d[q], b[q]);
-        const float2 t = sub2(xh[q], v[q]);
-        const float2 dv = fma2(kq, a, t);
-        v[q] = add2(v[q], dv);
-        const float2 u = add2(v[q], b[q]);
-        b[q] = u;
-        c0 = fma2(dv, dv, c0);
-        qacc = fma2(__fmul2_rn(u, lds_volatile2(wi2_s + q * G + gl)), u, qacc);
-      }
-      // u / tau inside the dual ellipsoid <z, W^-1 z> <= 1  <=>  sum u_i^2 / w_i <= tau^2:
-      // prox = 0 (mu = 0 below gives d' = 0 exactly).  Otherwise the projection of z = u / tau
-      // is w z / (w + mu) with mu > 0 the root of F(mu) = sum w u^2 / (w + mu)^2 - tau^2; Newton
-      // mu <- mu + (S1 - tau^2) / (2 S2), S2 = sum w u^2 / (w + mu)^3, warm-started at the previous
-      // iteration's mu and clamped at 0 (F convex decreasing: from the right of the root one step
-      // lands left of it, from the left Newton is monotone), stopped when the step is below
-      // 1e-6 (mu + min w) (the oracle starts at 0 and stops at |step| <= 1e-8; reading R27)
-      const float qn = group_sum<G>(qacc.x + qacc.y);
-      const float tau2 = tauS * tauS;
-      const bool outside = qn > tau2;
-      bool act = have && !waiting && spec == 0 && outside;
-      int nit = 0;
-      while (__any_sync(0xffffffffu, act)) {
-        float2 s1 = splat2(0.f), s2 = splat2(0.f);
+      // (3.4a) and u = v + b for every coordinate (b holds u until the projection is known),
+      // fused with the first Newton evaluation at the warm-start mu (below)
+      float2 s1 = splat2(0.f), s2 = s1;
+      // 1 / (w + mu_e) at the last evaluated mu_e, reused by (3.4b) below when it fits in
+      // registers (CPL <= 16); wider variants recompute it (MUFU)
+      constexpr bool RR = NP <= 8;
+      float2 rr[RR ? NP : 1];
+      float mu_e = mu;
+      {
         const float2 muP = splat2(mu);
 #pragma unroll
         for (int q = 0; q < NP; q++) {
+          const float2 kq = lds_volatile2(kap_s + q * G + gl);
+          const float2 a = sub2(d[q], b[q]);
+          const float2 t = sub2(xh[q], v[q]);
+          const float2 dv = fma2(kq, a, t);
+          v[q] = add2(v[q], dv);
+          const float2 u = add2(v[q], b[q]);
+          b[q] = u;
+          c0 = fma2(dv, dv, c0);
           const float2 w = lds_volatile2(w2_s + q * G + gl);
           const float2 e = add2(w, muP);
-          const float2 r = make_float2(__frcp_rn(e.x), __frcp_rn(e.y));
-          const float2 h = __fmul2_rn(b[q], r);           // u / (w + mu)
+          const float2 r = make_float2(rcp_approx(e.x), rcp_approx(e.y));
+          if (RR) rr[q] = r;
+          const float2 h = __fmul2_rn(u, r);             // u / (w + mu)
           const float2 wh2 = __fmul2_rn(__fmul2_rn(w, h), h);
           s1 = add2(s1, wh2);
           s2 = fma2(wh2, r, s2);
         }
-        const float S1 = group_sum<G>(s1.x + s1.y), S2 = group_sum<G>(s2.x + s2.y);
+      }
+      // (3.4b) = prox_{tau ||.||_W}(u) = u - tau P(u / tau), P the projection on the dual
+      // ellipsoid {z : <z, W^-1 z> <= 1} (Moreau): P(z) = w z / (w + mu), mu >= 0,
+      // mu = 0 iff u / tau is inside (sum u^2 / w <= tau^2), else the root of
+      // S1(mu) = sum w u^2 / (w + mu)^2 = tau^2.  Newton on psi(mu) = 1 / sqrt(S1) - 1 / tau
+      // (the trust-region secular form: psi is concave and nearly linear, so from either side a
+      // step lands at or left of the root, then the iteration is monotone):
+      //   mu <- max(0, mu + (S1 / S2) (sqrt(S1) / tau - 1)),   S2 = sum w u^2 / (w + mu)^3,
+      // warm-started at the previous iteration's mu.  The clamp at 0 is the inside case: the
+      // root is then negative, the iterates stop at 0 and d' = 0 * u / w = 0 exactly.  Newton's
+      // error after a step h is O(h^2 / (w + mu)) (psi'' / psi' ~ 1 / (w + mu)), so a step below
+      // 3e-4 (mu + min w) leaves ~1e-7 (mu + min w): the iterate after that step is accepted
+      // without another evaluation (mostly one evaluation per split Bregman iteration).
+      // The paper runs Newton on the same root from mu_0 = 0 on sum w u^2/(w+mu) + mu tau^2 and
+      // stops at |step| <= 1e-8, after testing inside-ness (the oracle does; reading R27)
+      float S1, S2;
+      group_reduce3<G>(s1.x + s1.y, s2.x + s2.y, c0.x + c0.y, tol, S1, S2, ell_ok_sv);
+      const float itau = rcp_approx(tauS);
+      bool act = have && !waiting && spec == 0;
+      int nit = 0;
+      for (;;) {
         if (act) {
-          const float mun = fmaxf(fmaf(S1 - tau2, __frcp_rn(2.f * S2), mu), 0.f);
-          act = !(fabsf(mun - mu) <= 1e-6f * (mun + wmin)) && ++nit < 40;
+          const float mun = S2 > 0.f ? fmaxf(fmaf(S1 * rcp_approx(S2), fmaf(sqrtf(S1), itau, -1.f), mu), 0.f)
+                                     : 0.f;   // u = 0: d' = 0
+          act = !(fabsf(mun - mu) <= 3e-4f * (mun + wmin)) && ++nit < 30;
           mu = mun;
         }
+        if (!__any_sync(0xffffffffu, act)) break;
+        float2 t1 = splat2(0.f), t2 = splat2(0.f);
+        const float2 muP = splat2(mu);
+        mu_e = mu;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          const float2 w = lds_volatile2(w2_s + q * G + gl);
+          const float2 e = add2(w, muP);
+          const float2 r = make_float2(rcp_approx(e.x), rcp_approx(e.y));
+          if (RR) rr[q] = r;
+          const float2 h = __fmul2_rn(b[q], r);
+          const float2 wh2 = __fmul2_rn(__fmul2_rn(w, h), h);
+          t1 = add2(t1, wh2);
+          t2 = fma2(wh2, r, t2);
+        }
+        S1 = group_sum<G>(t1.x + t1.y);
+        S2 = group_sum<G>(t2.x + t2.y);
       }
-      // (3.4b): d' = u - w u / (w + mu) = mu u / (w + mu);  (3.4c): b' = u - d'
-      const float2 muP = splat2(outside ? mu : 0.f);
+      // (3.4b): d' = u - w u / (w + mu) = mu u / (w + mu);  (3.4c): b' = u - d'.
+      // 1 / (w + mu) from the last evaluation at mu_e: mu - mu_e is the final Newton step
+      // (<= 3e-4 (mu + min w) unless the cap stopped it), corrected to first order,
+      // r (1 - (mu - mu_e) r), i.e. to ~1e-7 relative
+      const float mf = mu;
+      const float2 muP = splat2(mf);
+      const float2 ndel = splat2(mu_e - mf);
 #pragma unroll
       for (int q = 0; q < NP; q++) {
-        const float2 w = lds_volatile2(w2_s + q * G + gl);
-        const float2 e = add2(w, muP);
-        const float2 r = make_float2(__frcp_rn(e.x), __frcp_rn(e.y));
+        float2 r;
+        if constexpr (RR) {
+          r = __fmul2_rn(rr[q], fma2(ndel, rr[q], splat2(1.f)));
+        } else {
+          const float2 e = add2(lds_volatile2(w2_s + q * G + gl), muP);
+          r = make_float2(rcp_approx(e.x), rcp_approx(e.y));
+        }
         const float2 u = b[q];
         const float2 dn = __fmul2_rn(__fmul2_rn(muP, u), r);
         b[q] = sub2(u, dn);
@@ -469,7 +531,14 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
     {
       float r2;
       bool ok_sd, ok_sb, ok_sv;
-      group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
+      if constexpr (ELL) {   // sv was reduced with the Newton sums
+        ok_sd = group_sum<G>(psd) <= tol;
+        ok_sv = ell_ok_sv;
+        ok_sb = false;
+        r2 = 0.f;
+      } else {
+        group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
+      }
       if (HK == HK_L2) {
         kdone = it;
         conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it

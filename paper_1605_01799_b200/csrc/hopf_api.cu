@@ -58,7 +58,6 @@ using KernFn = void (*)(const DiagParams);
 struct Variant {
   int G, CPL;
   KernFn fn[3][2];  // [h kind][union]
-  KernFn ell;       // HOPF_H_ELL, hopf_eval_diag only
 };
 
 // union kernels keep x and the best grad resident too: only CPL <= 16 is instantiated
@@ -71,8 +70,7 @@ constexpr KernFn union_fn() {
   {G_, C_,                                                                                   \
    {{hopf_diag_kernel<G_, C_, HK_L1, false>, union_fn<G_, C_, HK_L1>()},                     \
     {hopf_diag_kernel<G_, C_, HK_WL1, false>, union_fn<G_, C_, HK_WL1>()},                   \
-    {hopf_diag_kernel<G_, C_, HK_L2, false>, union_fn<G_, C_, HK_L2>()}},                    \
-   hopf_diag_kernel<G_, C_, HK_ELL, false>}
+    {hopf_diag_kernel<G_, C_, HK_L2, false>, union_fn<G_, C_, HK_L2>()}}}
 
 // Ordered by padded width G*CPL (roughly), then G: the first variant with G*CPL >= n is used.
 // (8, 13) precedes (4, 25): for C2 (n = 100) its 127 registers give 4 warps per SMSP instead of 3
@@ -84,7 +82,29 @@ static const Variant kVariants[] = {
     HOPF_VARIANT(8, 32),
     HOPF_VARIANT(16, 32), HOPF_VARIANT(32, 32)};
 
-static const Variant *pick_variant(int n, bool is_union) {
+// HOPF_H_ELL (hopf_eval_diag only): its own list.  The projection adds per-point scalar work and
+// group reductions (Newton on mu); measured on C2e (n = 100): (8, 13) 5.3 ms, (16, 7) 6.5 ms,
+// (32, 4) 8.2 ms, so narrow groups first, as in the main list.
+#define HOPF_ELL_VARIANT(G_, C_) {G_, C_, {{hopf_diag_kernel<G_, C_, HK_ELL, false>, nullptr}}}
+static const Variant kEllVariants[] = {
+    HOPF_ELL_VARIANT(1, 4),  HOPF_ELL_VARIANT(2, 4),  HOPF_ELL_VARIANT(4, 4),
+    HOPF_ELL_VARIANT(8, 4),  HOPF_ELL_VARIANT(16, 4), HOPF_ELL_VARIANT(8, 13),
+    HOPF_ELL_VARIANT(16, 7), HOPF_ELL_VARIANT(32, 4), HOPF_ELL_VARIANT(32, 8),
+    HOPF_ELL_VARIANT(32, 16), HOPF_ELL_VARIANT(32, 32)};
+
+static const Variant *pick_variant(int n, bool is_union, bool ell = false) {
+  if (ell) {
+    static const char *force = getenv("HOPF_DIAG_VARIANT");
+    if (force) {
+      int fg = 0, fc = 0;
+      if (sscanf(force, "%d,%d", &fg, &fc) == 2)
+        for (const Variant &v : kEllVariants)
+          if (v.G == fg && v.CPL == fc && v.G * v.CPL >= n) return &v;
+    }
+    for (const Variant &v : kEllVariants)
+      if (v.G * v.CPL >= n) return &v;
+    return nullptr;
+  }
   // HOPF_DIAG_VARIANT=G,CPL forces a variant (experiments)
   static const char *force = getenv("HOPF_DIAG_VARIANT");
   if (force) {
@@ -157,14 +177,14 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
                             cudaStream_t stream) {
   DiagParams p = p_in;
   p.iter_total = g_iter_counter;
-  const Variant *v = pick_variant(p.n, is_union);
-  if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
-  static const char *tm_env = getenv("HOPF_DIAG_TM");
   const bool ell = h == HOPF_H_ELL;
   if (ell && is_union) return set_error(HOPF_EUNSUPPORTED, "HOPF_H_ELL is supported by hopf_eval_diag only");
+  const Variant *v = pick_variant(p.n, is_union, ell);
+  if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
+  static const char *tm_env = getenv("HOPF_DIAG_TM");
   if (!ell && !is_union && v->G == 32 && v->CPL == 32 && !(tm_env && strcmp(tm_env, "0") == 0))
     return launch_diag_tm(p, h, stream);
-  KernFn fn = ell ? v->ell : v->fn[(int)h][is_union ? 1 : 0];
+  KernFn fn = ell ? v->fn[0][0] : v->fn[(int)h][is_union ? 1 : 0];
   // Block size: the one that keeps the most warps resident per SM (register-limited kernels
   // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
   struct Occ { int threads, per_sm; };
