@@ -196,7 +196,7 @@ __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
 // SMSP has a 16K-register file); the widest variants otherwise take ~195 registers and only
 // 2 warps per SMSP, which leaves the dependent FP32x2 chains exposed.
 template <int G, int CPL, int HK, bool UNION>
-__global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
+__global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag_kernel(const DiagParams p) {
   constexpr bool KSM = !UNION;            // -kappa in shared memory
   constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
   constexpr int GPW = 32 / G;             // groups per warp
@@ -462,8 +462,8 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       // warm-started at the previous iteration's mu.  The clamp at 0 is the inside case: the
       // root is then negative, the iterates stop at 0 and d' = 0 * u / w = 0 exactly.  Newton's
       // error after a step h is O(h^2 / (w + mu)) (psi'' / psi' ~ 1 / (w + mu)), so a step below
-      // 3e-4 (mu + min w) leaves ~1e-7 (mu + min w): the iterate after that step is accepted
-      // without another evaluation (mostly one evaluation per split Bregman iteration).
+      // 1e-3 (mu + min w) leaves ~1e-6 (mu + min w): the iterate after that step is accepted
+      // without another evaluation (on C2e 1.7 evaluations per split Bregman iteration).
       // The paper runs Newton on the same root from mu_0 = 0 on sum w u^2/(w+mu) + mu tau^2 and
       // stops at |step| <= 1e-8, after testing inside-ness (the oracle does; reading R27)
       float S1, S2;
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
         if (act) {
           const float mun = S2 > 0.f ? fmaxf(fmaf(S1 * rcp_approx(S2), fmaf(sqrtf(S1), itau, -1.f), mu), 0.f)
                                      : 0.f;   // u = 0: d' = 0
-          act = !(fabsf(mun - mu) <= 3e-4f * (mun + wmin)) && ++nit < 30;
+          act = !(fabsf(mun - mu) <= 1e-3f * (mun + wmin)) && ++nit < 30;
           mu = mun;
         }
         if (!__any_sync(0xffffffffu, act)) break;
@@ -498,8 +498,8 @@ __global__ void __launch_bounds__(128, 3) hopf_diag_kernel(const DiagParams p) {
       }
       // (3.4b): d' = u - w u / (w + mu) = mu u / (w + mu);  (3.4c): b' = u - d'.
       // 1 / (w + mu) from the last evaluation at mu_e: mu - mu_e is the final Newton step
-      // (<= 3e-4 (mu + min w) unless the cap stopped it), corrected to first order,
-      // r (1 - (mu - mu_e) r), i.e. to ~1e-7 relative
+      // (<= 1e-3 (mu + min w) unless the cap stopped it), corrected to first order,
+      // r (1 - (mu - mu_e) r), i.e. to ~1e-6 relative
       const float mf = mu;
       const float2 muP = splat2(mf);
       const float2 ndel = splat2(mu_e - mf);
