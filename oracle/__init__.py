@@ -26,8 +26,8 @@ _SRC = _HERE / "hopf_oracle.c"
 _BUILD = _HERE / "_build"
 _LIB_PATH = _BUILD / "libhopf_oracle.so"
 
-H_L1, H_WL1, H_L2, H_ELL = 0, 1, 2, 3
-H_KINDS = {"l1": H_L1, "wl1": H_WL1, "l2": H_L2, "ell": H_ELL}
+H_L1, H_WL1, H_L2, H_ELL, H_LINF = 0, 1, 2, 3, 4
+H_KINDS = {"l1": H_L1, "wl1": H_WL1, "l2": H_L2, "ell": H_ELL, "linf": H_LINF}
 INVALID = np.iinfo(np.int32).min
 
 _lib = None

@@ -305,3 +305,34 @@ def diag_ell_secular(x, t, D, W, c=None, gamma=0.0, iters=200):
     v = xt * s / (D * s + t * W)
     phi = xt @ v - 0.5 * v @ (D * v) - t * np.sqrt(v @ (W * v)) + gamma
     return float(phi), v
+
+
+# --------------------------------------------------------------------------- l_inf H (NEXT-2)
+def diag_linf_bisection(x, t, D, c=None, gamma=0.0, iters=200):
+    """J = 1/2<x-c, D^{-1}(x-c)> + gamma, H = ||.||_inf.
+
+    Plain definition: phi = max_v <xt,v> - 1/2<v,Dv> - t max_i |v_i|.  For a fixed level
+    s = max_i |v_i| the maximiser is v_i = clamp(xt_i / D_i, -s, s); the remaining objective
+    g(s) = sum_i [1/2 D_i v_i^2 - xt_i v_i] + t s is convex in s >= 0 with derivative
+    g'(s) = t - sum_{|xt_i|/D_i > s} (|xt_i| - D_i s), increasing: s* = 0 if g'(0) >= 0, else
+    the root of g' by bisection.  Returns (phi, grad = v*)."""
+    xt = np.asarray(x, np.float64) - (0.0 if c is None else np.asarray(c, np.float64))
+    D = np.asarray(D, np.float64)
+    if t <= 0:
+        return 0.5 * np.sum(xt * xt / D) + gamma, xt / D
+    a = np.abs(xt) / D
+    gp = lambda s: t - np.sum(np.where(a > s, np.abs(xt) - D * s, 0.0))
+    if gp(0.0) >= 0:
+        s = 0.0
+    else:
+        lo, hi = 0.0, float(a.max())
+        for _ in range(iters):
+            mid = 0.5 * (lo + hi)
+            if gp(mid) < 0:
+                lo = mid
+            else:
+                hi = mid
+        s = 0.5 * (lo + hi)
+    v = np.clip(xt / D, -s, s)
+    phi = xt @ v - 0.5 * v @ (D * v) - t * (np.abs(v).max() if v.size else 0.0) + gamma
+    return float(phi), v

@@ -53,6 +53,7 @@
 #define ORACLE_H_WL1 1
 #define ORACLE_H_L2 2
 #define ORACLE_H_ELL 3 /* NEXT-2: H(p) = sqrt(<p, W p>), W = diag(w) > 0 */
+#define ORACLE_H_LINF 4 /* NEXT-2: H(p) = ||p||_inf */
 
 /* ---------------- prox of t/lambda * H (3.4b) ---------------------------- */
 
@@ -104,10 +105,52 @@ static void prox_ell(int n, const double *u, double tau, const double *w, double
   for (int i = 0; i < n; i++) out[i] = u[i] - tau * (w[i] * (u[i] / tau) / (w[i] + mu));
 }
 
+static int cmp_double(const void *a, const void *b) {
+  const double x = *(const double *)a, y = *(const double *)b;
+  return (x > y) - (x < y);
+}
+/* ||shrink_1(z, mu)||_1 = sum_i max(|z_i| - mu, 0)   (h of P:1410-1413) */
+static double h_linf(int n, const double *z, double mu) {
+  double s = 0.0;
+  for (int i = 0; i < n; i++) s += fmax(fabs(z[i]) - mu, 0.0);
+  return s;
+}
+/* prox of tau ||.||_inf: Moreau, prox(u) = u - tau pi_C(u / tau), C the unit l1
+ * ball (the dual ball of l_inf).  For z = u / tau outside C: pi_C(z) = shrink_1(z, mu) with
+ * ||shrink_1(z, mu)||_1 = 1 (eq. condition_mu_linfty); h(mu) = ||shrink_1(z, mu)||_1 is piecewise
+ * affine and decreasing with breakpoints B = {0} U {|z_i|}: sort them increasingly (l_0 = 0 <=
+ * l_1 <= ... <= l_n), search j with h(l_j) >= 1 > h(l_{j+1}) (binary search), and interpolate
+ * on the affine piece.  sort_buf: n doubles. */
+static void prox_linf(int n, const double *u, double tau, double *sort_buf, double *out) {
+  if (!(tau > 0.0)) { memcpy(out, u, sizeof(double) * n); return; }
+  double l1 = 0.0;
+  for (int i = 0; i < n; i++) l1 += fabs(u[i] / tau);
+  if (l1 <= 1.0) { for (int i = 0; i < n; i++) out[i] = 0.0; return; }   /* z in C: pi = z */
+  double *z = out;   /* out holds z = u / tau until the end */
+  for (int i = 0; i < n; i++) { z[i] = u[i] / tau; sort_buf[i] = fabs(z[i]); }
+  qsort(sort_buf, (size_t)n, sizeof(double), cmp_double);
+  /* breakpoint k: l_0 = 0, l_k = sort_buf[k-1]; h(l_0) = ||z||_1 > 1, h(l_n) = 0 < 1 */
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (h_linf(n, z, sort_buf[mid - 1]) >= 1.0) lo = mid; else hi = mid;
+  }
+  const double la = lo == 0 ? 0.0 : sort_buf[lo - 1], lb = sort_buf[hi - 1];
+  const double ha = h_linf(n, z, la), hb = h_linf(n, z, lb);
+  const double mu = la + (ha - 1.0) * (lb - la) / (ha - hb);
+  for (int i = 0; i < n; i++) {
+    const double a = fabs(z[i]) - mu;
+    const double pi = a > 0.0 ? (z[i] >= 0.0 ? a : -a) : 0.0;   /* shrink_1(z, mu) */
+    out[i] = u[i] - tau * pi;
+  }
+}
+
 static void prox_tH(int n, int h, const double *u, double t, const double *w,
                     double lambda, double *alpha_buf, double *out) {
   if (h == ORACLE_H_ELL) {
     prox_ell(n, u, t / lambda, w, out);
+  } else if (h == ORACLE_H_LINF) {
+    prox_linf(n, u, t / lambda, alpha_buf, out);
   } else if (h == ORACLE_H_L2) {
     shrink2(n, u, t / lambda, out);
   } else {
@@ -126,6 +169,10 @@ static double H_of(int n, int h, const double *p, const double *w) {
   if (h == ORACLE_H_L2) {
     for (int i = 0; i < n; i++) s += p[i] * p[i];
     return sqrt(s);
+  }
+  if (h == ORACLE_H_LINF) {
+    for (int i = 0; i < n; i++) s = fmax(s, fabs(p[i]));
+    return s;
   }
   for (int i = 0; i < n; i++) s += (h == ORACLE_H_WL1 ? w[i] : 1.0) * fabs(p[i]);
   return s;
@@ -225,7 +272,7 @@ int oracle_diag(int64_t M, int n, const double *X, const double *t, const double
                 int nthreads) {
   if (M < 0 || n < 1 || !D || lambda <= 0.0 || max_iter < 1 || tol < 0.0) return -1;
   if ((h == ORACLE_H_WL1 || h == ORACLE_H_ELL) && !w) return -1;
-  if (h < 0 || h > ORACLE_H_ELL) return -1;
+  if (h < 0 || h > ORACLE_H_LINF) return -1;
   int nt = nthreads_or_default(nthreads);
 #pragma omp parallel num_threads(nt)
   {
@@ -308,7 +355,7 @@ int oracle_dense(int64_t M, int n, const double *X, const double *t, const doubl
   if (M < 0 || n < 1 || !Ml || !A || !Ainv || lambda <= 0.0 || max_iter < 1 || tol < 0.0)
     return -1;
   if ((h == ORACLE_H_WL1 || h == ORACLE_H_ELL) && !w) return -1;
-  if (h < 0 || h > ORACLE_H_ELL) return -1;
+  if (h < 0 || h > ORACLE_H_LINF) return -1;
   int nt = nthreads_or_default(nthreads);
 #pragma omp parallel num_threads(nt)
   {
@@ -334,7 +381,7 @@ int oracle_union(int64_t M, int n, int K, const double *X, const double *t, cons
       tol < 0.0)
     return -1;
   if ((h == ORACLE_H_WL1 || h == ORACLE_H_ELL) && !w) return -1;
-  if (h < 0 || h > ORACLE_H_ELL) return -1;
+  if (h < 0 || h > ORACLE_H_LINF) return -1;
   if (Y && h != ORACLE_H_L2) return -1;
   int nt = nthreads_or_default(nthreads);
 #pragma omp parallel num_threads(nt)
@@ -490,7 +537,7 @@ int oracle_maxh(int64_t M, int n, const double *X, const double *t, const double
   if (M < 0 || n < 1 || K < 1 || !D || !kinds || !a || lambda <= 0.0 || max_iter < 1 || tol < 0.0)
     return -1;
   for (int i = 0; i < K; i++) {
-    if (kinds[i] < 0 || kinds[i] > ORACLE_H_ELL || !(a[i] > 0.0)) return -1;
+    if (kinds[i] < 0 || kinds[i] > ORACLE_H_LINF || !(a[i] > 0.0)) return -1;
     if ((kinds[i] == ORACLE_H_WL1 || kinds[i] == ORACLE_H_ELL) && !W) return -1;
   }
   int nt = nthreads_or_default(nthreads);
@@ -516,6 +563,8 @@ int oracle_maxh(int64_t M, int n, const double *X, const double *t, const double
         } else if (h == ORACLE_H_ELL) {
           ti = t[p] * a[i];
           wi = W + (size_t)i * n;
+        } else if (h == ORACLE_H_LINF) {
+          ti = t[p] * a[i];
         } else {
           for (int j = 0; j < n; j++) wa[j] = a[i] * (h == ORACLE_H_WL1 ? W[(size_t)i * n + j] : 1.0);
           wi = wa;

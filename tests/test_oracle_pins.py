@@ -425,3 +425,62 @@ def test_maxh_ell_member_is_time_scaled_ell_solve():
     np.testing.assert_array_equal(m[0], d[0])
     np.testing.assert_array_equal(m[1], d[1])
     assert np.all(m[3] == 0)
+
+
+# ----------------------------------------------------------------- l_inf H (NEXT-2)
+def test_linf_hamiltonian_matches_bisection_reference():
+    """H = ||.||_inf (Moreau + projection on the l1 ball by sorted breakpoints and
+    interpolation): against the plain level-set maximisation solved by bisection."""
+    rng = np.random.default_rng(51)
+    n, M = 10, 80
+    D = np.exp(rng.uniform(np.log(0.5), np.log(2.0), n))
+    c = rng.normal(size=n)
+    X = rng.normal(0, 3, (M, n))
+    t = rng.uniform(0.05, 4.0, M)
+    t[0] = 0.0
+    X[1] = c + 0.01          # ||x - c||_1 small: grad 0
+    X[2, 3] = X[2, 4]        # duplicate breakpoints
+    phi, grad, it = oracle.eval_diag(X, t, D, c, 0.25, "linf", None, tol=1e-22, max_iter=20000)
+    for i in range(M):
+        pe, ge = exact.diag_linf_bisection(X[i], t[i], D, c, 0.25)
+        assert abs(phi[i] - pe) <= 1e-9 * max(1.0, abs(pe)), i
+        np.testing.assert_allclose(grad[i], ge, atol=1e-6)
+    assert it[0] == 0 and np.all(grad[1] == 0.0)
+
+
+def test_linf_in_one_dimension_is_l1():
+    """n = 1: ||.||_inf = ||.||_1 = |.|; the l1-ball projection must reproduce shrink_1."""
+    rng = np.random.default_rng(52)
+    X = rng.normal(0, 3, (300, 1))
+    t = rng.uniform(0.0, 3.0, 300)
+    a = oracle.eval_diag(X, t, np.array([0.7]), None, 0.0, "linf")
+    b = oracle.eval_diag(X, t, np.array([0.7]), None, 0.0, "l1")
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(a[1], b[1], atol=1e-12)
+    np.testing.assert_array_equal(a[2], b[2])
+
+
+def test_linf_isotropic_hopf_lax_closed_form():
+    """J = 1/2||.||^2, H = ||.||_inf: Hopf-Lax with L = H* = indicator of the unit l1 ball gives
+    phi(x,t) = 1/2 min_{||x - y||_1 <= t} ||y||^2, i.e. y = x - pi_{tB1}(x) with pi the Euclidean
+    projection on the l1 ball of radius t, here found by sorting (Duchi et al.'s formula: the
+    largest k with |x|_(k) > (sum_{j<=k} |x|_(j) - t)/k), not the oracle's breakpoint search."""
+    rng = np.random.default_rng(53)
+    n, M = 6, 100
+    X = rng.normal(0, 3, (M, n))
+    t = rng.uniform(0.1, 8.0, M)
+    phi, grad, _ = oracle.eval_diag(X, t, np.ones(n), None, 0.0, "linf", None, tol=1e-24,
+                                    max_iter=20000)
+    for i in range(M):
+        x, tt = X[i], t[i]
+        if np.abs(x).sum() <= tt:
+            y = np.zeros(n)
+        else:
+            a = np.sort(np.abs(x))[::-1]
+            cs = np.cumsum(a)
+            k = max(j for j in range(1, n + 1) if a[j - 1] > (cs[j - 1] - tt) / j)
+            theta = (cs[k - 1] - tt) / k
+            p = np.sign(x) * np.maximum(np.abs(x) - theta, 0.0)
+            y = x - p
+        assert abs(phi[i] - 0.5 * y @ y) <= 1e-9 * max(1.0, phi[i])
+        np.testing.assert_allclose(grad[i], y, atol=1e-6)   # grad phi = grad J(y) = y
