@@ -40,10 +40,13 @@ FP32_LANES_PER_SM = 128
 # algorithmic FP32 flops per coordinate-iteration: update + the paper's test
 # ell (NEXT-2): (3.4a) + u 6, inside test 3, one Newton step on mu 8 (the warm-started steady
 # state), d' and b' 5, the test sums 5
-FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14, "ell": 27}
+# linf (NEXT-2): (3.4a) + u 6, one evaluation of the l1-ball sums 2, d' = clamp 2, b' 1, the
+# test sums 5 (min / max / compare-select counted as one flop)
+FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14, "ell": 27, "linf": 16}
 # per-point HBM bytes: x (4n) + grad (4n) + t, phi, iters (12)
 CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000, "c5d": 2048,
-              "c2h": 200_000, "c2e": 200_000}
+              "c2h": 200_000, "c2e": 200_000,
+              "c2i": 200_000}
 CPU_MIN_SECONDS = 10.0
 
 

@@ -60,9 +60,11 @@ enum {
  *   HOPF_H_WL1 : H(p) = sum_i w_i |p_i|    (shrink_1, threshold t w_i/lambda), w_i > 0
  *   HOPF_H_L2  : H(p) = ||p||_2            (shrink_2, threshold t/lambda)
  *   HOPF_H_ELL : H(p) = sqrt(<p, diag(w) p>), w_i > 0  (NEXT-2: prox by projection on the dual
- *                ellipsoid, Newton on its multiplier); hopf_eval_diag and
- *                hopf_eval_maxh only (hopf_eval_union returns HOPF_EUNSUPPORTED)            */
-typedef enum { HOPF_H_L1 = 0, HOPF_H_WL1 = 1, HOPF_H_L2 = 2, HOPF_H_ELL = 3 } hopf_h_kind;
+ *                ellipsoid, Newton on its multiplier)
+ *   HOPF_H_LINF: H(p) = max_i |p_i|         (NEXT-2: prox by projection on the l1 ball,
+ *                P:1348-1428)
+ *   ELL and LINF: hopf_eval_diag and hopf_eval_maxh only (hopf_eval_union: HOPF_EUNSUPPORTED) */
+typedef enum { HOPF_H_L1 = 0, HOPF_H_WL1 = 1, HOPF_H_L2 = 2, HOPF_H_ELL = 3, HOPF_H_LINF = 4 } hopf_h_kind;
 
 /* Diagonal (ellipsoidal) initial data:
  *   J(x) = 1/2 <x - c, diag(Dj)^{-1} (x - c)> + gamma,  J*(v) = 1/2 <v, Dj v> + <c, v> - gamma

@@ -15,7 +15,7 @@ __all__ = ["lib", "eval_diag", "eval_union", "eval_dense", "DensePlan", "eval_di
 
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libhopf.so"
-H_KINDS = {"l1": 0, "wl1": 1, "l2": 2, "ell": 3}
+H_KINDS = {"l1": 0, "wl1": 1, "l2": 2, "ell": 3, "linf": 4}
 INVALID = -(2 ** 31)
 _lib = None
 

@@ -36,7 +36,9 @@ namespace hopf {
 // HK_ELL (NEXT-2): H(p) = sqrt(<p, W p>), W = diag(w) > 0.  (3.4b) is prox_{tau ||.||_W}(u) =
 // u - tau P(u / tau), P the projection on the dual ellipsoid {z : <z, W^-1 z> <= 1}, computed by
 // Newton on its multiplier mu; see the ELL branch of the trip below.
-enum { HK_L1 = 0, HK_WL1 = 1, HK_L2 = 2, HK_ELL = 3 };
+// HK_LINF (NEXT-2): H(p) = ||p||_inf.  (3.4b) is u - pi_{tau B1}(u) (Moreau; B1 the unit l1 ball,
+// P:1348-1428) = clamp(u, -mu, mu) with mu the l1-ball multiplier; see the LINF branch.
+enum { HK_L1 = 0, HK_WL1 = 1, HK_L2 = 2, HK_ELL = 3, HK_LINF = 4 };
 
 struct DiagParams {
   int64_t M;
@@ -66,6 +68,13 @@ template <int G>
 __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int G>
+__device__ __forceinline__ float group_max(float v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
@@ -196,7 +205,7 @@ __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
 // SMSP has a 16K-register file); the widest variants otherwise take ~195 registers and only
 // 2 warps per SMSP, which leaves the dependent FP32x2 chains exposed.
 template <int G, int CPL, int HK, bool UNION>
-__global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag_kernel(const DiagParams p) {
+__global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag_kernel(const DiagParams p) {
   constexpr bool KSM = !UNION;            // -kappa in shared memory
   constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
   constexpr int GPW = 32 / G;             // groups per warp
@@ -225,7 +234,8 @@ __global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag
   __shared__ float D_s[KSM ? G * CPL : 1], di_s[KSM ? G * CPL : 1], w_s[WSM ? G * CPL : 1];
   // ELL: (w_i, 1/w_i) pairs in the kappa layout; padded slots hold w = 1 (their u is 0)
   constexpr bool ELL = HK == HK_ELL;
-  static_assert(!(ELL && UNION), "the ellipsoidal Hamiltonian is instantiated for hopf_eval_diag only");
+  constexpr bool LINF = HK == HK_LINF;
+  static_assert(!((ELL || LINF) && UNION), "ELL / LINF are instantiated for hopf_eval_diag only");
   __shared__ __align__(16) float2 w2_s[ELL ? NP * G : 1];
   const float ksign = (HK == HK_L2) ? -1.f : 1.f;
   if (KSM) {
@@ -271,7 +281,7 @@ __global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag
   float tauS = 0.f;     // scalar threshold t/lambda
   int spec = 0;         // 0 normal, 1 t == 0, 2 invalid
   float s_cur = 1.f;    // l2: shrink factor of the pending (3.4b)
-  float mu = 0.f;       // ELL: multiplier of the last projection (warm start of the next)
+  float mu = 0.f;       // ELL / LINF: multiplier of the last projection (warm start of the next)
   bool sv_ok = false;   // l2: ||v^k - v^{k-1}||^2 <= tol of the pending iteration
   float best = 0.f;
   int bestk = -1, bestit = 0;
@@ -519,6 +529,81 @@ __global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag
         d[q] = fma2(dd, splat2(live), d[q]);
         a0 = fma2(dd, dd, a0);
       }
+    } else if constexpr (LINF) {
+      // (3.4a) and u = v + b (b holds u until the projection is known), fused with the first
+      // evaluation of the l1-ball sums at the warm-start mu: S1 = sum_{|u_i| > mu} |u_i|,
+      // S2 = #{|u_i| > mu}
+      float2 sa = splat2(0.f), na = sa;
+      float mu_e = mu;
+      {
+        const float2 muP = splat2(mu);
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          const float2 kq = lds_volatile2(kap_s + q * G + gl);
+          const float2 a = sub2(d[q], b[q]);
+          const float2 t = sub2(xh[q], v[q]);
+          const float2 dv = fma2(kq, a, t);
+          v[q] = add2(v[q], dv);
+          const float2 u = add2(v[q], b[q]);
+          b[q] = u;
+          c0 = fma2(dv, dv, c0);
+          const float ax = fabsf(u.x), ay = fabsf(u.y);
+          sa.x += ax > muP.x ? ax : 0.f;
+          sa.y += ay > muP.y ? ay : 0.f;
+          na.x += ax > muP.x ? 1.f : 0.f;
+          na.y += ay > muP.y ? 1.f : 0.f;
+        }
+      }
+      // pi_{tau B1}(u) = shrink_1(u, mu), mu >= 0 with sum_i max(|u_i| - mu, 0) = tau
+      // (eq. condition_mu_linfty); mu = 0 iff ||u||_1 <= tau (inside: d' = 0).
+      // F(mu) = sum max(|u_i| - mu, 0) - tau is convex, decreasing and piecewise affine, and its
+      // Newton step from mu is mu' = (S1(mu) - tau) / S2(mu) (the active-set average): from the
+      // right of the root it lands at or left of it, from the left it increases monotonically
+      // and stops at the root as soon as the active set stops changing.  Warm-started at the
+      // previous iteration's mu and clamped at 0.  A step whose active set is unchanged at the
+      // new mu (no |u_i| between mu and mu', a ballot, no reduction) is exact: accepted with no
+      // further evaluation.  The paper (and the oracle) sorts the breakpoints {0} U {|u_i|/tau}
+      // and interpolates on the bracketing affine piece; both give the same root (reading R28)
+      float S1, S2;
+      group_reduce3<G>(sa.x + sa.y, na.x + na.y, c0.x + c0.y, tol, S1, S2, ell_ok_sv);
+      bool act = have && !waiting && spec == 0;
+      int nit = 0;
+      for (;;) {
+        float mun = mu_e;
+        if (act) mun = S2 > 0.f ? fmaxf(__fdividef(S1 - tauS, S2), 0.f) : 0.f;
+        bool cross = false;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          const float ax = fabsf(b[q].x), ay = fabsf(b[q].y);
+          cross |= ((ax > mu_e) != (ax > mun)) || ((ay > mu_e) != (ay > mun));
+        }
+        cross = group_any<G>(cross);
+        if (act && (!cross || ++nit >= 64)) { mu = mun; act = false; }
+        if (!__any_sync(0xffffffffu, act)) break;
+        if (act) mu_e = mun;
+        float2 ta = splat2(0.f), tn = ta;
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          const float ax = fabsf(b[q].x), ay = fabsf(b[q].y);
+          ta.x += ax > mu_e ? ax : 0.f;
+          ta.y += ay > mu_e ? ay : 0.f;
+          tn.x += ax > mu_e ? 1.f : 0.f;
+          tn.y += ay > mu_e ? 1.f : 0.f;
+        }
+        S1 = group_sum<G>(ta.x + ta.y);
+        S2 = group_sum<G>(tn.x + tn.y);
+      }
+      // (3.4b): d' = u - shrink_1(u, mu) = clamp(u, -mu, mu);  (3.4c): b' = u - d'
+      const float2 muP = splat2(mu);
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const float2 u = b[q];
+        const float2 dn = clamp2(u, muP);
+        b[q] = sub2(u, dn);
+        const float2 dd = sub2(dn, d[q]);
+        d[q] = fma2(dd, splat2(live), d[q]);
+        a0 = fma2(dd, dd, a0);
+      }
     } else if (full_test) {
       trip(std::true_type{});
     } else {
@@ -531,7 +616,7 @@ __global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag
     {
       float r2;
       bool ok_sd, ok_sb, ok_sv;
-      if constexpr (ELL) {   // sv was reduced with the Newton sums
+      if constexpr (ELL || LINF) {   // sv was reduced with the Newton sums
         ok_sd = group_sum<G>(psd) <= tol;
         ok_sv = ell_ok_sv;
         ok_sb = false;
@@ -608,6 +693,8 @@ __global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag
           if (HK == HK_L2) hsum = fmaf(dq.x, dq.x, fmaf(dq.y, dq.y, hsum));
           else if (ELL)
             hsum = fmaf((ok0 ? w_s[i0] : 0.f) * dq.x, dq.x, fmaf((ok1 ? w_s[i1] : 0.f) * dq.y, dq.y, hsum));
+          else if (LINF)
+            hsum = fmaxf(hsum, fmaxf(fabsf(dq.x), fabsf(dq.y)));
           else if (HK == HK_WL1)
             hsum = fmaf(ok0 ? (KSM ? w_s[i0] : __ldg(p.w + i0)) : 0.f, fabsf(dq.x),
                         fmaf(ok1 ? (KSM ? w_s[i1] : __ldg(p.w + i1)) : 0.f, fabsf(dq.y), hsum));
@@ -617,7 +704,7 @@ __global__ void __launch_bounds__(128, (HK == 3 && CPL <= 16) ? 4 : 3) hopf_diag
       }
     }
     qs = group_sum<G>(qs);
-    hsum = group_sum<G>(hsum);
+    hsum = LINF ? group_max<G>(hsum) : group_sum<G>(hsum);
     const float gam = UNION ? __ldg(p.gk + kset) : p.gamma;
     float phiv;
     if (spec == 1) phiv = qs + gam;

@@ -85,24 +85,29 @@ static const Variant kVariants[] = {
 // HOPF_H_ELL (hopf_eval_diag only): its own list.  The projection adds per-point scalar work and
 // group reductions (Newton on mu); measured on C2e (n = 100): (8, 13) 5.3 ms, (16, 7) 6.5 ms,
 // (32, 4) 8.2 ms, so narrow groups first, as in the main list.
-#define HOPF_ELL_VARIANT(G_, C_) {G_, C_, {{hopf_diag_kernel<G_, C_, HK_ELL, false>, nullptr}}}
-static const Variant kEllVariants[] = {
-    HOPF_ELL_VARIANT(1, 4),  HOPF_ELL_VARIANT(2, 4),  HOPF_ELL_VARIANT(4, 4),
-    HOPF_ELL_VARIANT(8, 4),  HOPF_ELL_VARIANT(16, 4), HOPF_ELL_VARIANT(8, 13),
-    HOPF_ELL_VARIANT(16, 7), HOPF_ELL_VARIANT(32, 4), HOPF_ELL_VARIANT(32, 8),
-    HOPF_ELL_VARIANT(32, 16), HOPF_ELL_VARIANT(32, 32)};
+// HOPF_H_LINF (same entry points) uses the same list with its own instantiations.
+#define HOPF_X_VARIANT(HK_, G_, C_) {G_, C_, {{hopf_diag_kernel<G_, C_, HK_, false>, nullptr}}}
+#define HOPF_X_VARIANTS(HK_)                                                                 \
+  {HOPF_X_VARIANT(HK_, 1, 4),  HOPF_X_VARIANT(HK_, 2, 4),   HOPF_X_VARIANT(HK_, 4, 4),       \
+   HOPF_X_VARIANT(HK_, 8, 4),  HOPF_X_VARIANT(HK_, 16, 4),  HOPF_X_VARIANT(HK_, 8, 13),      \
+   HOPF_X_VARIANT(HK_, 16, 7), HOPF_X_VARIANT(HK_, 32, 4),  HOPF_X_VARIANT(HK_, 32, 8),      \
+   HOPF_X_VARIANT(HK_, 32, 16), HOPF_X_VARIANT(HK_, 32, 32)}
+static const Variant kEllVariants[] = HOPF_X_VARIANTS(HK_ELL);
+static const Variant kLinfVariants[] = HOPF_X_VARIANTS(HK_LINF);
 
-static const Variant *pick_variant(int n, bool is_union, bool ell = false) {
-  if (ell) {
+static const Variant *pick_variant(int n, bool is_union, int hx = -1) {
+  if (hx == HK_ELL || hx == HK_LINF) {
+    const Variant *list = hx == HK_ELL ? kEllVariants : kLinfVariants;
+    const int cnt = (int)(sizeof(kEllVariants) / sizeof(kEllVariants[0]));
     static const char *force = getenv("HOPF_DIAG_VARIANT");
     if (force) {
       int fg = 0, fc = 0;
       if (sscanf(force, "%d,%d", &fg, &fc) == 2)
-        for (const Variant &v : kEllVariants)
-          if (v.G == fg && v.CPL == fc && v.G * v.CPL >= n) return &v;
+        for (int i = 0; i < cnt; i++)
+          if (list[i].G == fg && list[i].CPL == fc && fg * fc >= n) return &list[i];
     }
-    for (const Variant &v : kEllVariants)
-      if (v.G * v.CPL >= n) return &v;
+    for (int i = 0; i < cnt; i++)
+      if (list[i].G * list[i].CPL >= n) return &list[i];
     return nullptr;
   }
   // HOPF_DIAG_VARIANT=G,CPL forces a variant (experiments)
@@ -177,9 +182,10 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
                             cudaStream_t stream) {
   DiagParams p = p_in;
   p.iter_total = g_iter_counter;
-  const bool ell = h == HOPF_H_ELL;
-  if (ell && is_union) return set_error(HOPF_EUNSUPPORTED, "HOPF_H_ELL is supported by hopf_eval_diag only");
-  const Variant *v = pick_variant(p.n, is_union, ell);
+  const bool ell = h == HOPF_H_ELL || h == HOPF_H_LINF;
+  if (ell && is_union)
+    return set_error(HOPF_EUNSUPPORTED, "HOPF_H_ELL / HOPF_H_LINF are supported by hopf_eval_diag only");
+  const Variant *v = pick_variant(p.n, is_union, h == HOPF_H_ELL ? HK_ELL : (h == HOPF_H_LINF ? HK_LINF : -1));
   if (!v) return set_error(HOPF_EUNSUPPORTED, "n=%d exceeds the compiled diag kernels", p.n);
   static const char *tm_env = getenv("HOPF_DIAG_TM");
   if (!ell && !is_union && v->G == 32 && v->CPL == 32 && !(tm_env && strcmp(tm_env, "0") == 0))
@@ -216,7 +222,9 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   g_launches += 1;
   g_last_threads = threads;
   g_last_blocks = (int)blocks;
-  g_last_kernel = is_union ? "hopf_diag_kernel<union>" : (ell ? "hopf_diag_kernel<ell>" : "hopf_diag_kernel");
+  g_last_kernel = is_union ? "hopf_diag_kernel<union>"
+                           : (h == HOPF_H_ELL ? "hopf_diag_kernel<ell>"
+                                              : (h == HOPF_H_LINF ? "hopf_diag_kernel<linf>" : "hopf_diag_kernel"));
   return check_launch("hopf_diag_kernel");
 }
 
@@ -235,7 +243,7 @@ int hopf_eval_diag(int64_t M, int32_t n, const float *X, const float *t, const f
   g_launches = 0;
   g_last_error.clear();
   if (M < 0 || n < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d", (long long)M, n);
-  if ((int)h < 0 || (int)h > 3) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
+  if ((int)h < 0 || (int)h > 4) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
   if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
   if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
@@ -258,7 +266,7 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
   g_launches = 0;
   g_last_error.clear();
   if (M < 0 || n < 1 || K < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d K=%d", (long long)M, n, K);
-  if ((int)h < 0 || (int)h > 3) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
+  if ((int)h < 0 || (int)h > 4) return set_error(HOPF_EINVAL, "unknown H kind %d", (int)h);
   if (!finite_pos(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
   if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
@@ -312,7 +320,7 @@ int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const f
   if (M < 0 || n < 1 || K < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d K=%d", (long long)M, n, K);
   if (!h_kinds || !a) return set_error(HOPF_EINVAL, "h_kinds and a (host arrays) are required");
   for (int i = 0; i < K; i++) {
-    if (h_kinds[i] < 0 || h_kinds[i] > 3) return set_error(HOPF_EINVAL, "unknown H kind %d", h_kinds[i]);
+    if (h_kinds[i] < 0 || h_kinds[i] > 4) return set_error(HOPF_EINVAL, "unknown H kind %d", h_kinds[i]);
     if (!finite_pos(a[i])) return set_error(HOPF_EINVAL, "a[%d] must be > 0 and finite", i);
     if ((h_kinds[i] == HOPF_H_WL1 || h_kinds[i] == HOPF_H_ELL) && !W)
       return set_error(HOPF_EINVAL, "W is required for HOPF_H_WL1 / HOPF_H_ELL");

@@ -134,6 +134,11 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
         wl = config("c2", M=M, n=n, seed=seed, h="ell")
         wl.name = "c2e"
         return wl
+    if name == "c2i":
+        # NEXT-2: C2's J and points with H(p) = ||p||_inf
+        wl = config("c2", M=M, n=n, seed=seed, h="linf")
+        wl.name = "c2i"
+        return wl
     if name in ("c2", "c3"):
         num = 2 if name == "c2" else 3
         n = n or (100 if num == 2 else 1000)
@@ -184,4 +189,4 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h", "c2e")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h", "c2e", "c2i")

@@ -80,7 +80,7 @@ def test_diag_configs_subset(hb, name, M):
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 13, 16, 17, 31, 33, 64, 100, 127, 200, 255, 256,
                                300, 511, 777, 1000, 1024])
-@pytest.mark.parametrize("h", ["l1", "wl1", "l2", "ell"])
+@pytest.mark.parametrize("h", ["l1", "wl1", "l2", "ell", "linf"])
 def test_diag_ragged_dimensions(hb, n, h):
     """Every compiled lane-group variant, ragged tails, shifted centre c and lambda != 1."""
     rng = np.random.default_rng(n * 7 + len(h))
@@ -473,6 +473,54 @@ def test_maxh_with_ellipsoidal_member(hb):
     W = np.stack([wl.w, np.ones_like(wl.w)]).astype(np.float32)
     phi, grad, it, ist = hb.eval_maxh(dev(X), dev(t), dev(wl.D), None, wl.gamma, kinds, a, dev(W))
     o = oracle.eval_maxh(X, t, wl.D, None, wl.gamma, kinds, a, W)
+    same = ist.cpu().numpy() == o[3]
+    assert np.mean(same) > 0.98
+    check(phi[same], grad[same], it[same], o[0][same], o[1][same], o[2][same])
+
+
+# ----------------------------------------------------------------- l_inf H (NEXT-2)
+def test_linf_c2i_subset_and_edges(hb):
+    """H = ||.||_inf on C2's J and points: t == 0, invalid points, a point inside
+    the t l1-ball (grad = 0), duplicate |u_i| (ties of the active set) and max_iter exhaustion."""
+    wl = inputs.config("c2i")
+    X, t = inputs.points(wl, 0, 20000)
+    X, t = X.copy(), t.copy()
+    t[0] = 0.0
+    X[1, 3] = np.inf
+    t[2] = np.nan
+    X[4] = 0.0
+    t[5] = 1e4
+    X[6, :] = 1.5                      # all |x_i| equal
+    X[7, ::2] = -X[7, 1::2]            # pairs of equal |x_i|
+    g = run_diag(hb, wl, X, t)
+    o = oracle_diag(wl, X, t)
+    check(*g, *o)
+    assert np.all(g[1][5].cpu().numpy() == 0) and abs(g[0][5].item() - wl.gamma) < 1e-6
+    g2 = run_diag(hb, wl, X, t, max_iter=4)
+    o2 = oracle_diag(wl, X, t, max_iter=4)
+    ok = o2[2] != oracle.INVALID
+    np.testing.assert_allclose(g2[1].cpu().numpy()[ok], o2[1][ok], atol=1e-4)
+
+
+def test_linf_one_dimension_matches_l1_gpu(hb):
+    """n = 1: ||.||_inf = |.| = ||.||_1: the l1-ball projection kernel against the l1 kernel."""
+    rng = np.random.default_rng(9)
+    X = rng.normal(0, 3, (5000, 1)).astype(np.float32)
+    t = rng.uniform(0, 3, 5000).astype(np.float32)
+    D = np.array([0.7], np.float32)
+    a = hb.eval_diag(dev(X), dev(t), dev(D), None, 0.0, "linf")
+    b = hb.eval_diag(dev(X), dev(t), dev(D), None, 0.0, "l1")
+    np.testing.assert_allclose(a[0].cpu().numpy(), b[0].cpu().numpy(), rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(a[1].cpu().numpy(), b[1].cpu().numpy(), atol=1e-5)
+
+
+def test_maxh_with_linf_member(hb):
+    """NEXT-4 with a NEXT-2 member: H = min(||p||_inf * 2, ||p||_2)."""
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 3000)
+    kinds, a = ["linf", "l2"], np.array([2.0, 1.0], np.float32)
+    phi, grad, it, ist = hb.eval_maxh(dev(X), dev(t), dev(wl.D), None, wl.gamma, kinds, a, None)
+    o = oracle.eval_maxh(X, t, wl.D, None, wl.gamma, kinds, a, None)
     same = ist.cpu().numpy() == o[3]
     assert np.mean(same) > 0.98
     check(phi[same], grad[same], it[same], o[0][same], o[1][same], o[2][same])
