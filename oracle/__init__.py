@@ -62,8 +62,10 @@ def _load():
                                               f64, dp, dp, dp, dp, ip, ip, i32]
         lib.oracle_maxh.argtypes = [i64, i32, dp, dp, dp, dp, f64, i32, ip, dp, dp, f64, i32, f64,
                                     dp, dp, ip, ip, i32]
+        lib.oracle_normsq.argtypes = [i64, i32, dp, dp, i32, f64, i32, dp, f64, i32, f64, dp, dp,
+                                      ip, i32]
         for f in (lib.oracle_diag, lib.oracle_dense, lib.oracle_union, lib.oracle_distance_union,
-                  lib.oracle_maxh):
+                  lib.oracle_maxh, lib.oracle_normsq):
             f.restype = ctypes.c_int
         lib.oracle_threads.argtypes = [i32]
         lib.oracle_threads.restype = ctypes.c_int
@@ -226,3 +228,25 @@ def eval_maxh(X, t, D, c, gamma, kinds, a, W=None, lam=1.0, max_iter=1000, tol=1
     if rc != 0:
         raise ValueError(f"oracle_maxh rejected its arguments (rc={rc})")
     return phi, grad, iters, istar
+
+
+J_KINDS = {"l1sq": 0, "linfsq": 1}
+
+
+def eval_normsq(X, t, j, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=1e-8, nthreads=0):
+    """NEXT-3: J = 1/2||.||_1^2 (j="l1sq") or 1/2||.||_inf^2 (j="linfsq") plus gamma, any H
+    (P:1488-1555).  Returns phi, grad, iters."""
+    X = _f64(X)
+    M, n = X.shape
+    t = _f64(t, (M,))
+    w = _f64(w, (n,)) if w is not None else None
+    phi = np.empty(M)
+    grad = np.empty((M, n))
+    iters = np.empty(M, dtype=np.int32)
+    ip = ctypes.POINTER(ctypes.c_int32)
+    rc = _load().oracle_normsq(M, n, _d(X), _d(t), J_KINDS[j], float(gamma), _hk(h), _d(w),
+                               float(lam), int(max_iter), float(tol), _d(phi), _d(grad),
+                               iters.ctypes.data_as(ip), int(nthreads))
+    if rc != 0:
+        raise ValueError(f"oracle_normsq rejected its arguments (rc={rc})")
+    return phi, grad, iters

@@ -336,3 +336,37 @@ def diag_linf_bisection(x, t, D, c=None, gamma=0.0, iters=200):
     v = np.clip(xt / D, -s, s)
     phi = xt @ v - 0.5 * v @ (D * v) - t * (np.abs(v).max() if v.size else 0.0) + gamma
     return float(phi), v
+
+
+# --------------------------------------------------------------------------- NEXT-3 references
+def normsq_hopf_lax(x, t, j, h):
+    """Closed forms / 1-D searches for J = 1/2||.||_p^2 (p = 1: j="l1sq", p = inf: j="linfsq")
+    from the Hopf-Lax formula phi = min_y J(y) + t L((x - y)/t), L = H* the indicator of the
+    dual unit ball — no split Bregman, no prox:
+      l1sq,   H = l1  : y = shrink_1(x, t) coordinatewise, phi = 1/2 (sum max(|x_i| - t, 0))^2
+      l1sq,   H = linf: ||x - y||_1 <= t removes t of l1 mass, phi = 1/2 max(||x||_1 - t, 0)^2
+      linfsq, H = l1  : phi = 1/2 (max_i max(|x_i| - t, 0))^2
+      linfsq, H = l2  : phi = 1/2 s^2, s the least level with dist_2(x, [-s, s]^n) <= t
+                        (bisection on sum max(|x_i| - s, 0)^2 = t^2)
+    Returns phi only (grad is not unique for linfsq)."""
+    x = np.asarray(x, np.float64)
+    if j == "l1sq" and h == "l1":
+        return 0.5 * np.sum(np.maximum(np.abs(x) - t, 0.0)) ** 2
+    if j == "l1sq" and h == "linf":
+        return 0.5 * max(np.abs(x).sum() - t, 0.0) ** 2
+    if j == "linfsq" and h == "l1":
+        return 0.5 * max(np.abs(x).max() - t, 0.0) ** 2
+    if j == "linfsq" and h == "l2":
+        a = np.abs(x)
+        f = lambda s: np.sum(np.maximum(a - s, 0.0) ** 2) - t * t
+        if f(0.0) <= 0:
+            return 0.0
+        lo, hi = 0.0, float(a.max())
+        for _ in range(200):
+            mid = 0.5 * (lo + hi)
+            if f(mid) > 0:
+                lo = mid
+            else:
+                hi = mid
+        return 0.5 * (0.5 * (lo + hi)) ** 2
+    raise KeyError((j, h))

@@ -596,3 +596,130 @@ int oracle_maxh(int64_t M, int n, const double *X, const double *t, const double
   }
   return 0;
 }
+
+/* ---------------- non-quadratic initial data (NEXT-3) ------------ */
+/* J = 1/2 ||.||_1^2 (ORACLE_J_L1SQ) or 1/2 ||.||_inf^2 (ORACLE_J_LINFSQ), plus gamma; any H.
+ * (J*: 1/2||.||_inf^2 and 1/2||.||_1^2 respectively.) */
+#define ORACLE_J_L1SQ 0
+#define ORACLE_J_LINFSQ 1
+
+/* beta >= 0 with beta = alpha ||shrink_1(z, beta)||_1 (eq. optimality_beta_l1_2): g(beta) =
+ * alpha h(beta) - beta is decreasing and piecewise affine with breakpoints {0} U {|z_i|}: sort
+ * them, search the bracketing pair g(l_j) >= 0 > g(l_{j+1}) (binary search), interpolate
+ * (P:1513-1537).  z = 0 gives 0.  sort_buf: n doubles. */
+static double beta_l1sq(int n, const double *z, double alpha, double *sort_buf) {
+  double l1 = 0.0;
+  for (int i = 0; i < n; i++) { sort_buf[i] = fabs(z[i]); l1 += sort_buf[i]; }
+  if (l1 == 0.0) return 0.0;
+  qsort(sort_buf, (size_t)n, sizeof(double), cmp_double);
+  /* breakpoint k: l_0 = 0, l_k = sort_buf[k-1]; g(l_0) = alpha ||z||_1 > 0, g(l_n) = -max|z| < 0 */
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    const double l = sort_buf[mid - 1];
+    if (alpha * h_linf(n, z, l) - l >= 0.0) lo = mid; else hi = mid;
+  }
+  const double la = lo == 0 ? 0.0 : sort_buf[lo - 1], lb = sort_buf[hi - 1];
+  const double ga = alpha * h_linf(n, z, la) - la, gb = alpha * h_linf(n, z, lb) - lb;
+  return la + ga * (lb - la) / (ga - gb);
+}
+/* prox_{(alpha/2)||.||_1^2}(z) = shrink_1(z, beta) (eq. prox_l1_2_with_beta) */
+static void prox_l1sq(int n, const double *z, double alpha, double *sort_buf, double *out) {
+  const double beta = beta_l1sq(n, z, alpha, sort_buf);
+  for (int i = 0; i < n; i++) {
+    const double a = fabs(z[i]) - beta;
+    out[i] = a > 0.0 ? (z[i] >= 0.0 ? a : -a) : 0.0;
+  }
+}
+/* prox_{(alpha/2)||.||_inf^2}(z) = z - alpha prox_{(1/(2 alpha))||.||_1^2}(z / alpha)  (Moreau,
+ * P:1549-1555; the printed form z - prox_{(alpha/2)||.||_1^2}(z) is this at alpha = 1, the
+ * paper's lambda; reading R29).  zs: n doubles of scratch. */
+static void prox_linfsq(int n, const double *z, double alpha, double *sort_buf, double *zs,
+                        double *out) {
+  for (int i = 0; i < n; i++) zs[i] = z[i] / alpha;
+  prox_l1sq(n, zs, 1.0 / alpha, sort_buf, out);
+  for (int i = 0; i < n; i++) out[i] = z[i] - alpha * out[i];
+}
+static double l1norm(int n, const double *p) {
+  double s = 0.0;
+  for (int i = 0; i < n; i++) s += fabs(p[i]);
+  return s;
+}
+static double linfnorm(int n, const double *p) {
+  double s = 0.0;
+  for (int i = 0; i < n; i++) s = fmax(s, fabs(p[i]));
+  return s;
+}
+
+static int solve_normsq_point(int n, const double *x, double t, int jk, double gamma, int h,
+                              const double *w, double lambda, int max_iter, double tol,
+                              double *phi, double *grad, double *ws) {
+  double *v = ws, *d = ws + n, *b = ws + 2 * n, *vp = ws + 3 * n, *dp = ws + 4 * n;
+  double *u = ws + 5 * n, *al = ws + 6 * n, *z = ws + 7 * n, *zs = ws + 8 * n;
+  if (point_invalid(n, x, t)) {
+    *phi = NAN;
+    for (int i = 0; i < n; i++) grad[i] = NAN;
+    return INT32_MIN;
+  }
+  if (t == 0.0) {
+    /* R6 with R30: phi = J(x); grad = the minimal-norm element of dJ(x):
+     * 1/2||x||_1^2: ||x||_1 sign(x_i) (0 where x_i = 0);
+     * 1/2||x||_inf^2: ||x||_inf sign(x_i) / m on the m maximal |x_i|, 0 elsewhere */
+    if (jk == ORACLE_J_L1SQ) {
+      const double s = l1norm(n, x);
+      for (int i = 0; i < n; i++) grad[i] = x[i] > 0.0 ? s : (x[i] < 0.0 ? -s : 0.0);
+      *phi = 0.5 * s * s + gamma;
+    } else {
+      const double s = linfnorm(n, x);
+      int m = 0;
+      for (int i = 0; i < n; i++) m += (fabs(x[i]) == s);
+      for (int i = 0; i < n; i++)
+        grad[i] = (s > 0.0 && fabs(x[i]) == s) ? (x[i] > 0.0 ? s : -s) / m : 0.0;
+      *phi = 0.5 * s * s + gamma;
+    }
+    return 0;
+  }
+  for (int i = 0; i < n; i++) { v[i] = x[i]; d[i] = x[i]; b[i] = 0.0; }
+  int iters = -max_iter;
+  for (int k = 1; k <= max_iter; k++) {
+    memcpy(vp, v, sizeof(double) * n);
+    memcpy(dp, d, sizeof(double) * n);
+    /* (3.4a): v = argmin J*(v) - <x,v> + lambda/2 ||d - v - b||^2, i.e. the prox of
+     * (1/lambda) J* at z = d - b + x/lambda */
+    for (int i = 0; i < n; i++) z[i] = d[i] - b[i] + x[i] / lambda;
+    if (jk == ORACLE_J_L1SQ) prox_linfsq(n, z, 1.0 / lambda, al, zs, v);   /* J* = 1/2||.||_inf^2 */
+    else prox_l1sq(n, z, 1.0 / lambda, al, v);                              /* J* = 1/2||.||_1^2 */
+    for (int i = 0; i < n; i++) u[i] = v[i] + b[i];
+    prox_tH(n, h, u, t, w, lambda, al, d);
+    for (int i = 0; i < n; i++) b[i] = b[i] + v[i] - d[i];
+    if (sqdist(n, v, vp) <= tol && sqdist(n, d, dp) <= tol && sqdist(n, d, v) <= tol) {
+      iters = k;
+      break;
+    }
+  }
+  double xd = 0.0;
+  for (int i = 0; i < n; i++) { xd += x[i] * d[i]; grad[i] = d[i]; }
+  const double js = jk == ORACLE_J_L1SQ ? linfnorm(n, d) : l1norm(n, d);
+  *phi = xd - 0.5 * js * js - t * H_of(n, h, d, w) + gamma;
+  return iters;
+}
+
+int oracle_normsq(int64_t M, int n, const double *X, const double *t, int jk, double gamma,
+                  int h, const double *w, double lambda, int max_iter, double tol, double *phi,
+                  double *grad, int32_t *iters, int nthreads) {
+  if (M < 0 || n < 1 || lambda <= 0.0 || max_iter < 1 || tol < 0.0) return -1;
+  if (jk != ORACLE_J_L1SQ && jk != ORACLE_J_LINFSQ) return -1;
+  if ((h == ORACLE_H_WL1 || h == ORACLE_H_ELL) && !w) return -1;
+  if (h < 0 || h > ORACLE_H_LINF) return -1;
+  int nt = nthreads_or_default(nthreads);
+#pragma omp parallel num_threads(nt)
+  {
+    double *ws = (double *)malloc(sizeof(double) * 9 * (size_t)n);
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t p = 0; p < M; p++)
+      iters[p] = solve_normsq_point(n, X + p * n, t[p], jk, gamma, h, w, lambda, max_iter, tol,
+                                    phi + p, grad + p * n, ws);
+    free(ws);
+  }
+  return 0;
+}

@@ -484,3 +484,59 @@ def test_linf_isotropic_hopf_lax_closed_form():
             y = x - p
         assert abs(phi[i] - 0.5 * y @ y) <= 1e-9 * max(1.0, phi[i])
         np.testing.assert_allclose(grad[i], y, atol=1e-6)   # grad phi = grad J(y) = y
+
+
+# ----------------------------------------------------------------- NEXT-3 (non-quadratic J)
+@pytest.mark.parametrize("j,h", [("l1sq", "l1"), ("l1sq", "linf"), ("linfsq", "l1"), ("linfsq", "l2")])
+def test_normsq_hopf_lax_closed_forms(j, h):
+    """J = 1/2||.||_1^2 or 1/2||.||_inf^2 (Tables 2-3, 5): phi against the Hopf-Lax
+    closed forms / 1-D searches of exact.normsq_hopf_lax; grad satisfies the Hopf optimality
+    (the objective at grad equals phi)."""
+    rng = np.random.default_rng(61 + len(j) + len(h))
+    n, M = 6, 120
+    X = rng.uniform(-10, 10, (M, n))
+    t = rng.uniform(0.0, 10.0, M)
+    t[0] = 0.0
+    phi, grad, it = oracle.eval_normsq(X, t, j, 0.0, h, tol=1e-24, max_iter=50000)
+    for i in range(M):
+        pe = exact.normsq_hopf_lax(X[i], t[i], j, h)
+        assert abs(phi[i] - pe) <= 1e-7 * max(1.0, pe), (i, phi[i], pe)
+    assert it[0] == 0
+    # grad attains the Hopf sup: <x,g> - J*(g) - t H(g) = phi (J* of the dual norm)
+    js = (np.abs(grad).max(axis=1) if j == "l1sq" else np.abs(grad).sum(axis=1))
+    hv = {"l1": np.abs(grad).sum(axis=1), "linf": np.abs(grad).max(axis=1),
+          "l2": np.linalg.norm(grad, axis=1)}[h]
+    obj = np.einsum("ij,ij->i", X, grad) - 0.5 * js ** 2 - t * hv
+    np.testing.assert_allclose(obj[1:], phi[1:], rtol=1e-7, atol=1e-7)
+
+
+def test_normsq_t0_and_subgradients():
+    """t = 0: J(x) and the minimal-norm subgradient (reading R30)."""
+    X = np.array([[3.0, -1.0, 0.0, 2.0], [-2.0, 2.0, 1.0, 0.5]])
+    t = np.zeros(2)
+    p1, g1, i1 = oracle.eval_normsq(X, t, "l1sq")
+    np.testing.assert_allclose(p1, [18.0, 15.125])
+    np.testing.assert_allclose(g1[0], [6.0, -6.0, 0.0, 6.0])
+    p2, g2, _ = oracle.eval_normsq(X, t, "linfsq")
+    np.testing.assert_allclose(p2, [4.5, 2.0])
+    np.testing.assert_allclose(g2[0], [3.0, 0.0, 0.0, 0.0])
+    np.testing.assert_allclose(g2[1], [-1.0, 1.0, 0.0, 0.0])
+    assert np.all(i1 == 0)
+
+
+@pytest.mark.parametrize("j", ["l1sq", "linfsq"])
+def test_normsq_bruteforce_n2(j):
+    """n = 2, H = l2 and weighted l1: the Hopf formula maximised by brute force on a fine grid."""
+    rng = np.random.default_rng(71)
+    X = rng.uniform(-3, 3, (12, 2))
+    t = rng.uniform(0.2, 2.0, 12)
+    g = np.linspace(-6, 6, 1201)
+    V1, V2 = np.meshgrid(g, g, indexing="ij")
+    js = (np.maximum(np.abs(V1), np.abs(V2)) if j == "l1sq" else np.abs(V1) + np.abs(V2))
+    w = np.array([0.7, 1.3])
+    for h in ("l2", "wl1"):
+        phi, _, _ = oracle.eval_normsq(X, t, j, 0.0, h, w, tol=1e-20, max_iter=50000)
+        Hv = np.hypot(V1, V2) if h == "l2" else w[0] * np.abs(V1) + w[1] * np.abs(V2)
+        for i in range(len(X)):
+            obj = X[i, 0] * V1 + X[i, 1] * V2 - 0.5 * js ** 2 - t[i] * Hv
+            assert abs(obj.max() - phi[i]) <= 2e-3 * max(1.0, abs(phi[i])), (h, i)
