@@ -43,10 +43,14 @@ FP32_LANES_PER_SM = 128
 # linf (NEXT-2): (3.4a) + u 6, one evaluation of the l1-ball sums 2, d' = clamp 2, b' 1, the
 # test sums 5 (min / max / compare-select counted as one flop)
 FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14, "ell": 27, "linf": 16}
+# NEXT-3 (J = 1/2||.||_1^2 or 1/2||.||_inf^2): z = d - b + x/lambda 2, one evaluation of the
+# active-set sums 2, v = clamp / shrink 2, sv 3, u 1, then the H update and the sd, sb sums:
+# l1/wl1 4 + 6, l2 3 + 6, linf 2 + 2 + 6
+FLOPS_NORMSQ = {"l1": 20, "wl1": 20, "l2": 19, "linf": 20}
 # per-point HBM bytes: x (4n) + grad (4n) + t, phi, iters (12)
 CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000, "c5d": 2048,
               "c2h": 200_000, "c2e": 200_000,
-              "c2i": 200_000}
+              "c2i": 200_000, "t5": 1_000_000}
 CPU_MIN_SECONDS = 10.0
 
 
@@ -145,6 +149,9 @@ def _oracle_once(wl, X, t):
     elif wl.kind == "distance":
         oracle.distance_union(X, wl.Dk, wl.Ck, wl.gammak, lam=wl.lam, max_iter=wl.max_iter,
                               tol=wl.tol, stol=1e-5)
+    elif wl.kind == "normsq":
+        oracle.eval_normsq(X, t, wl.jk, wl.gamma, wl.h, wl.w, lam=wl.lam, max_iter=wl.max_iter,
+                           tol=wl.tol)
     else:
         oracle.eval_dense(X, t, wl.Q, wl.Lam, wl.gamma, wl.h, lam=wl.lam, max_iter=wl.max_iter,
                           tol=wl.tol)
@@ -179,6 +186,9 @@ def run_reference(args, wl):
 def metric_name(wl):
     if wl.kind == "maxh":
         return f"Hopf evals/sec ({wl.name}: H = min of {len(wl.maxh[0])} Hamiltonians, n={wl.n})"
+    if wl.kind == "normsq":
+        jn = "1/2||.||_1^2" if wl.jk == "l1sq" else "1/2||.||_inf^2"
+        return f"Hopf evals/sec ({wl.name}: J = {jn}, H = {wl.h}, n={wl.n})"
     if wl.kind == "distance":
         return f"closest-point queries/sec ({wl.name}: union of K={wl.Dk.shape[0]} ellipsoids, n={wl.n})"
     return METRIC if wl.name == "c3" else f"Hopf evals/sec ({wl.name}, n={wl.n})"
@@ -265,6 +275,10 @@ def main():
         def step():
             mres["r"] = hb.eval_maxh(X, t, D, None, wl.gamma, kinds, av, Wd, wl.lam, wl.max_iter,
                                      wl.tol, out=out, stream=stream)
+    elif wl.kind == "normsq":
+        w = f32(wl.w)
+        step = lambda: hb.eval_normsq(X, t, wl.jk, wl.gamma, wl.h, w, wl.lam, wl.max_iter, wl.tol,
+                                      out=out, stream=stream)
     elif wl.kind == "distance":
         Dk, Ck, gk = f32(wl.Dk), f32(wl.Ck), f32(wl.gammak)
         dres = {}
@@ -286,7 +300,7 @@ def main():
     # total split Bregman iterations of one step (all solves: union sets, Newton evaluations),
     # from the library's instrumentation counter in one extra untimed step
     inner_iters = None
-    if wl.kind in ("diag", "union", "distance", "maxh"):
+    if wl.kind in ("diag", "union", "distance", "maxh", "normsq"):
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         hb.set_iteration_counter(cnt)
         step()
@@ -376,6 +390,37 @@ def main():
                "h2d_bytes_per_step": int(Xp.numel() * 4 + tp.numel() * 4),
                "d2h_bytes_per_step": int(M * 4 + M * n * 4 + M * 4),
                "api": "hopf_eval_diag_host (pinned host buffers, chunked H2D/kernel/D2H pipeline)"}
+    elif not args.no_e2e and wl.kind == "normsq":
+        # no host-buffer entry point: pinned H2D of x and t, the call, D2H of phi, grad, iters
+        Xp = torch.from_numpy(Xh).pin_memory()
+        tp = torch.from_numpy(th).pin_memory()
+        outh = (torch.empty(M, pin_memory=True), torch.empty((M, n), pin_memory=True),
+                torch.empty(M, dtype=torch.int32, pin_memory=True))
+
+        def e2e_step():
+            X.copy_(Xp, non_blocking=True)
+            t.copy_(tp, non_blocking=True)
+            step()
+            for hbuf, dbuf in zip(outh, out):
+                hbuf.copy_(dbuf, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        for _ in range(2):
+            e2e_step()
+        if ws > 1:
+            dist.barrier()
+        ksteps = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(ksteps):
+            e2e_step()
+        el = time.perf_counter() - t0
+        if ws > 1:
+            tm = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            el = float(tm.item())
+        e2e = {"value": M * ws * ksteps / el, "unit": UNIT,
+               "h2d_bytes_per_step": int(Xp.numel() * 4 + tp.numel() * 4),
+               "d2h_bytes_per_step": int(M * 4 + M * n * 4 + M * 4),
+               "api": "hopf_eval_normsq with torch pinned copies on the same stream"}
 
     if rank != 0:
         if ws > 1:
@@ -388,12 +433,14 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     conv = iters_np[iters_np > 0]
     roof = None
-    if wl.kind in ("diag", "union", "distance", "maxh"):
+    if wl.kind in ("diag", "union", "distance", "maxh", "normsq"):
         it_sum = float(inner_iters)
         # algorithmic HBM bytes per point: diag x in, grad out (4n each) + t, phi, iters;
         # union / distance also write y (closest point / projection) and k*
-        hbm_per_point = (8 * n + 12) if wl.kind in ("diag", "maxh") else (12 * n + 16)
-        flops = it_sum * n * FLOPS_PER_COORD_ITER["l1" if wl.kind == "maxh" else wl.h]
+        hbm_per_point = (8 * n + 12) if wl.kind in ("diag", "maxh", "normsq") else (12 * n + 16)
+        fpc = (FLOPS_NORMSQ[wl.h] if wl.kind == "normsq"
+               else FLOPS_PER_COORD_ITER["l1" if wl.kind == "maxh" else wl.h])
+        flops = it_sum * n * fpc
         achieved = flops / (ms_step / 1e3) / 1e12
         peak = sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
         roof = {"kernel": kernel_name, "bound": "alu", "achieved": achieved, "peak": peak,
@@ -403,7 +450,7 @@ def main():
                               "counts, max SM clock)",
                 "algorithmic_flops_per_launch": flops,
                 "inner_iterations_per_launch": inner_iters,
-                "flops_per_coord_iter": FLOPS_PER_COORD_ITER[wl.h],
+                "flops_per_coord_iter": fpc,
                 "mean_iters": float(conv.mean()) if conv.size else None,
                 "hbm_bytes_per_launch": M * hbm_per_point,
                 "hbm_GBps": M * hbm_per_point / (ms_step / 1e3) / 1e9}

@@ -98,6 +98,20 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
                     float *grad, int32_t *iters, float *Y, int32_t *kstar, float *phi_k,
                     hopf_stream_t stream);
 
+/* Non-quadratic initial data (NEXT-3; Tables 2, 3 and 5):
+ *   HOPF_J_L1SQ  : J(x) = 1/2 ||x||_1^2 + gamma    (J* = 1/2 ||.||_inf^2)
+ *   HOPF_J_LINFSQ: J(x) = 1/2 ||x||_inf^2 + gamma  (J* = 1/2 ||.||_1^2)
+ * (3.4a) is the prox of J* / lambda, found per iteration through the multiplier of
+ * eq. optimality_beta_l1_2 (Moreau for 1/2||.||_inf^2, reading R29).
+ *   h in {HOPF_H_L1, HOPF_H_WL1 (w [n] required), HOPF_H_L2, HOPF_H_LINF}; 1 <= n <= 512.
+ *   t == 0: phi = J(x), grad = the minimal-norm subgradient of J (reading R30).
+ * Other arguments, outputs, status codes and errors as hopf_eval_diag.  The minimiser grad may
+ * be non-unique for these J (J* is not strictly convex); phi is unique. */
+typedef enum { HOPF_J_L1SQ = 0, HOPF_J_LINFSQ = 1 } hopf_j_kind;
+int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const float *t, hopf_j_kind j,
+                     float gamma, hopf_h_kind h, const float *w, float lambda, int32_t max_iter,
+                     float tol, float *phi, float *grad, int32_t *iters, hopf_stream_t stream);
+
 /* Maximum over a minimum of Hamiltonians (NEXT-4): for H = min_i H_i,
  *   phi(x,t) = max_i phi_i(x,t),  phi_i the solution with H_i and the same diagonal J,
  * the lowest i winning ties; grad = the winner's gradient, iters = its status.

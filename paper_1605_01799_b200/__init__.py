@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
-__all__ = ["lib", "eval_diag", "eval_union", "eval_dense", "DensePlan", "eval_diag_host",
+__all__ = ["lib", "eval_diag", "eval_union", "eval_dense", "DensePlan", "eval_diag_host", "eval_normsq",
            "HopfError", "H_KINDS", "INVALID"]
 
 _PKG = Path(__file__).resolve().parent
@@ -38,6 +38,8 @@ def lib():
         vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
         L.hopf_eval_diag.argtypes = [i64, i32, vp, vp, vp, vp, f32, ctypes.c_int, vp, f32, i32, f32,
                                      vp, vp, vp, vp]
+        L.hopf_eval_normsq.argtypes = [i64, i32, vp, vp, ctypes.c_int, f32, ctypes.c_int, vp, f32,
+                                       i32, f32, vp, vp, vp, vp]
         L.hopf_eval_union.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, ctypes.c_int, vp, f32, i32,
                                       f32, vp, vp, vp, vp, vp, vp, vp]
         L.hopf_dense_plan_create.argtypes = [i32, vp, vp, f32, ctypes.POINTER(vp)]
@@ -52,7 +54,7 @@ def lib():
                                           vp, vp, vp, vp, vp, vp, vp]
         for f in (L.hopf_eval_diag, L.hopf_eval_union, L.hopf_dense_plan_create,
                   L.hopf_dense_plan_destroy, L.hopf_eval_dense, L.hopf_eval_diag_host,
-                  L.hopf_distance_union, L.hopf_eval_maxh):
+                  L.hopf_distance_union, L.hopf_eval_maxh, L.hopf_eval_normsq):
             f.restype = ctypes.c_int
         L.hopf_last_error.restype = ctypes.c_char_p
         L.hopf_strerror.restype = ctypes.c_char_p
@@ -128,7 +130,7 @@ def _outputs(M, n, device, out):
 
 def eval_diag(X, t, D, c=None, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=1e-8,
               out=None, stream=None):
-    """hopf_eval_diag: J(x) = 1/2<x-c, D^{-1}(x-c)> + gamma, H in {l1, wl1, l2}.
+    """hopf_eval_diag: J(x) = 1/2<x-c, D^{-1}(x-c)> + gamma, H in {l1, wl1, l2, ell, linf}.
 
     X [M,n], t [M], D [n], c [n]|None, w [n]|None: float32 CUDA tensors.
     Returns (phi [M], grad [M,n], iters [M] int32)."""
@@ -162,6 +164,24 @@ def eval_union(X, t, Dk, Ck, gammak, h="l2", w=None, lam=1.0, max_iter=1000, tol
                                _ptr(pk, "f32", M * K, "phik"), _stream(stream))
     _check(rc, "hopf_eval_union")
     return phi, grad, iters, Y, ks, pk
+
+
+J_KINDS = {"l1sq": 0, "linfsq": 1}
+
+
+def eval_normsq(X, t, j, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=1e-8, out=None,
+                stream=None):
+    """hopf_eval_normsq (NEXT-3): J = 1/2||.||_1^2 (j="l1sq") or 1/2||.||_inf^2 (j="linfsq") plus
+    gamma, H in {l1, wl1, l2, linf}.  Returns (phi [M], grad [M,n], iters [M] int32)."""
+    M, n = X.shape
+    phi, grad, iters = _outputs(M, n, X.device, out)
+    rc = lib().hopf_eval_normsq(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                                J_KINDS[j], float(gamma), H_KINDS[h], _ptr(w, "f32", n, "w"),
+                                float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                                _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                                _stream(stream))
+    _check(rc, "hopf_eval_normsq")
+    return phi, grad, iters
 
 
 def eval_maxh(X, t, D, c, gamma, kinds, a, W=None, lam=1.0, max_iter=1000, tol=1e-8, out=None,

@@ -531,8 +531,10 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
       }
     } else if constexpr (LINF) {
       // (3.4a) and u = v + b (b holds u until the projection is known), fused with the first
-      // evaluation of the l1-ball sums at the warm-start mu: S1 = sum_{|u_i| > mu} |u_i|,
-      // S2 = #{|u_i| > mu}
+      // evaluation of the l1-ball sums at the warm-start mu: S1 = sum max(|u_i| - mu, 0) (small
+      // terms: the Newton step is formed in delta form, mu + (S1 - tau) / S2, because
+      // sum_{A} |u_i| - |A| mu cancels catastrophically when the root sits just below a cluster
+      // of |u_i|), S2 = #{|u_i| > mu}
       float2 sa = splat2(0.f), na = sa;
       float mu_e = mu;
       {
@@ -547,17 +549,17 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
           const float2 u = add2(v[q], b[q]);
           b[q] = u;
           c0 = fma2(dv, dv, c0);
-          const float ax = fabsf(u.x), ay = fabsf(u.y);
-          sa.x += ax > muP.x ? ax : 0.f;
-          sa.y += ay > muP.y ? ay : 0.f;
-          na.x += ax > muP.x ? 1.f : 0.f;
-          na.y += ay > muP.y ? 1.f : 0.f;
+          const float ex = fabsf(u.x) - muP.x, ey = fabsf(u.y) - muP.y;
+          sa.x += fmaxf(ex, 0.f);
+          sa.y += fmaxf(ey, 0.f);
+          na.x += ex > 0.f ? 1.f : 0.f;
+          na.y += ey > 0.f ? 1.f : 0.f;
         }
       }
       // pi_{tau B1}(u) = shrink_1(u, mu), mu >= 0 with sum_i max(|u_i| - mu, 0) = tau
       // (eq. condition_mu_linfty); mu = 0 iff ||u||_1 <= tau (inside: d' = 0).
       // F(mu) = sum max(|u_i| - mu, 0) - tau is convex, decreasing and piecewise affine, and its
-      // Newton step from mu is mu' = (S1(mu) - tau) / S2(mu) (the active-set average): from the
+      // Newton step from mu is mu' = mu + (S1(mu) - tau) / S2(mu) (the active-set average): from the
       // right of the root it lands at or left of it, from the left it increases monotonically
       // and stops at the root as soon as the active set stops changing.  Warm-started at the
       // previous iteration's mu and clamped at 0.  A step whose active set is unchanged at the
@@ -570,7 +572,7 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
       int nit = 0;
       for (;;) {
         float mun = mu_e;
-        if (act) mun = S2 > 0.f ? fmaxf(__fdividef(S1 - tauS, S2), 0.f) : 0.f;
+        if (act) mun = S2 > 0.f ? fmaxf(mu_e + __fdividef(S1 - tauS, S2), 0.f) : 0.f;
         bool cross = false;
 #pragma unroll
         for (int q = 0; q < NP; q++) {
@@ -578,17 +580,20 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
           cross |= ((ax > mu_e) != (ax > mun)) || ((ay > mu_e) != (ay > mun));
         }
         cross = group_any<G>(cross);
-        if (act && (!cross || ++nit >= 64)) { mu = mun; act = false; }
+        // a breakpoint at the root makes fp32 steps alternate across it: a step within a few
+        // ulps of mu is accepted as the root
+        const bool tiny = fabsf(mun - mu_e) <= 4e-7f * fmaxf(mun, 1e-30f);
+        if (act && (!cross || tiny || ++nit >= 64)) { mu = mun; act = false; }
         if (!__any_sync(0xffffffffu, act)) break;
         if (act) mu_e = mun;
         float2 ta = splat2(0.f), tn = ta;
 #pragma unroll
         for (int q = 0; q < NP; q++) {
-          const float ax = fabsf(b[q].x), ay = fabsf(b[q].y);
-          ta.x += ax > mu_e ? ax : 0.f;
-          ta.y += ay > mu_e ? ay : 0.f;
-          tn.x += ax > mu_e ? 1.f : 0.f;
-          tn.y += ay > mu_e ? 1.f : 0.f;
+          const float ex = fabsf(b[q].x) - mu_e, ey = fabsf(b[q].y) - mu_e;
+          ta.x += fmaxf(ex, 0.f);
+          ta.y += fmaxf(ey, 0.f);
+          tn.x += ex > 0.f ? 1.f : 0.f;
+          tn.y += ey > 0.f ? 1.f : 0.f;
         }
         S1 = group_sum<G>(ta.x + ta.y);
         S2 = group_sum<G>(tn.x + tn.y);

@@ -1,0 +1,73 @@
+// normsq_api.cu — C ABI of NEXT-3 (hopf_eval_normsq, include/hopf.h): argument validation,
+// variant selection and launch of hopf_normsq_kernel (normsq_kernel.cuh).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "../../include/hopf.h"
+#include "normsq_kernel.cuh"
+
+namespace hopf {
+int set_error(int code, const char *fmt, ...);
+int check_launch(const char *what);
+int num_sms();
+extern thread_local int32_t g_launches;
+extern thread_local int32_t g_last_threads, g_last_blocks;
+extern thread_local const char *g_last_kernel;
+extern thread_local unsigned long long *g_iter_counter;
+
+using NormsqFn = void (*)(const NormsqParams);
+struct NormsqVariant {
+  int G, CPL;
+  NormsqFn fn[2];   // [J kind]
+};
+#define HOPF_NSQ_VARIANT(G_, C_) \
+  {G_, C_, {hopf_normsq_kernel<G_, C_, JK_L1SQ>, hopf_normsq_kernel<G_, C_, JK_LINFSQ>}}
+// thread per point up to n = 16 (the paper's Tables 2, 3 and 5 use n = 4..16), then groups
+static const NormsqVariant kNormsqVariants[] = {
+    HOPF_NSQ_VARIANT(1, 4),  HOPF_NSQ_VARIANT(1, 8),   HOPF_NSQ_VARIANT(1, 16),
+    HOPF_NSQ_VARIANT(4, 16), HOPF_NSQ_VARIANT(16, 16), HOPF_NSQ_VARIANT(32, 16)};
+}  // namespace hopf
+
+using namespace hopf;
+
+extern "C" int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const float *t,
+                                hopf_j_kind j, float gamma, hopf_h_kind h, const float *w,
+                                float lambda, int32_t max_iter, float tol, float *phi,
+                                float *grad, int32_t *iters, hopf_stream_t stream) {
+  g_launches = 0;
+  if (M < 0 || n < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d", (long long)M, n);
+  if ((int)j < 0 || (int)j > 1) return set_error(HOPF_EINVAL, "unknown J kind %d", (int)j);
+  if (!(h == HOPF_H_L1 || h == HOPF_H_WL1 || h == HOPF_H_L2 || h == HOPF_H_LINF))
+    return set_error(HOPF_EINVAL, "H kind %d is not available with hopf_eval_normsq", (int)h);
+  if (!(lambda > 0.f) || !std::isfinite(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
+  if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
+  if (h == HOPF_H_WL1 && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1");
+  const NormsqVariant *v = nullptr;
+  for (const NormsqVariant &c : kNormsqVariants)
+    if (c.G * c.CPL >= n) { v = &c; break; }
+  if (!v) return set_error(HOPF_EUNSUPPORTED, "hopf_eval_normsq supports n <= 512 (n=%d)", n);
+  if (M == 0) return HOPF_OK;
+  if (!X || !t || !phi || !grad || !iters) return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  NormsqParams p{};
+  p.M = M; p.n = n; p.X = X; p.t = t; p.w = h == HOPF_H_WL1 ? w : nullptr;
+  p.gamma = gamma; p.lambda = lambda; p.tol = tol; p.max_iter = max_iter; p.h = (int)h;
+  p.phi = phi; p.grad = grad; p.iters = iters; p.iter_total = g_iter_counter;
+  NormsqFn fn = v->fn[(int)j];
+  const int threads = 128;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  int64_t blocks = (int64_t)num_sms() * per_sm;
+  const int64_t need = (M * v->G + threads - 1) / threads;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  fn<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(p);
+  g_launches = 1;
+  g_last_threads = threads;
+  g_last_blocks = (int)blocks;
+  g_last_kernel = j == HOPF_J_L1SQ ? "hopf_normsq_kernel<l1sq>" : "hopf_normsq_kernel<linfsq>";
+  return check_launch("hopf_normsq_kernel");
+}

@@ -37,8 +37,8 @@ class Workload:
     name: str
     n: int
     M: int
-    h: str                      # "l1" | "wl1" | "l2"
-    kind: str                   # "diag" | "dense" | "union" | "distance"
+    h: str                      # "l1" | "wl1" | "l2" | "ell" | "linf"
+    kind: str                   # "diag" | "dense" | "union" | "distance" | "maxh" | "normsq"
     seed: int
     x_law: tuple                # ("uniform", lo, hi) | ("normal", std)
     t_law: tuple                # ("uniform", lo, hi)
@@ -129,6 +129,20 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
         wl.maxh = (["wl1", "l2", "l1"], np.array([1.0, 1.2, 0.8], np.float32),
                    np.stack([wl.w, np.ones_like(wl.w), np.ones_like(wl.w)]).astype(np.float32))
         return wl
+    if name.startswith("t5") or name.startswith("t3") or name.startswith("t2"):
+        # NEXT-3: the paper's Tables 2, 3 and 5 protocol: x ~ U[-10,10]^n,
+        # t ~ U[0,10], lambda = 1, tol 1e-8.  t5[_n]: J = 1/2||.||_1^2, H = ||.||_inf (Table 5's
+        # scaling setup, n = 16 by default); t3_<n>_<h>: J = 1/2||.||_1^2; t2_<n>_<h>:
+        # J = 1/2||.||_inf^2
+        body = name.split("_")
+        n = n or (int(body[1]) if len(body) > 1 else 16)
+        hh = h or (body[2] if len(body) > 2 else ("linf" if name.startswith("t5") else "l1"))
+        wl = Workload(name, n, M or 1_000_000, hh, "normsq", seed or SEED_BASE + 200 + n,
+                      ("uniform", -10.0, 10.0), ("uniform", 0.0, 10.0), gamma=0.0)
+        wl.jk = "linfsq" if name.startswith("t2") else "l1sq"
+        if hh == "wl1":
+            wl.w = (1.0 + np.arange(n) / max(n - 1, 1)).astype(np.float32)   # the paper's D_ii
+        return wl
     if name == "c2e":
         # NEXT-2: C2's J and points with H(p) = sqrt(<p, diag(w) p>), w = C2's weights
         wl = config("c2", M=M, n=n, seed=seed, h="ell")
@@ -189,4 +203,4 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h", "c2e", "c2i")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h", "c2e", "c2i", "t5")
