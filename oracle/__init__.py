@@ -64,8 +64,10 @@ def _load():
                                     dp, dp, ip, ip, i32]
         lib.oracle_normsq.argtypes = [i64, i32, dp, dp, i32, f64, i32, dp, f64, i32, f64, dp, dp,
                                       ip, i32]
+        lib.oracle_diag_A.argtypes = [i64, i32, dp, dp, dp, dp, f64, dp, dp, dp, f64, i32, f64, dp,
+                                      dp, ip, i32]
         for f in (lib.oracle_diag, lib.oracle_dense, lib.oracle_union, lib.oracle_distance_union,
-                  lib.oracle_maxh, lib.oracle_normsq):
+                  lib.oracle_maxh, lib.oracle_normsq, lib.oracle_diag_A):
             f.restype = ctypes.c_int
         lib.oracle_threads.argtypes = [i32]
         lib.oracle_threads.restype = ctypes.c_int
@@ -249,4 +251,29 @@ def eval_normsq(X, t, j, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=
                                iters.ctypes.data_as(ip), int(nthreads))
     if rc != 0:
         raise ValueError(f"oracle_normsq rejected its arguments (rc={rc})")
+    return phi, grad, iters
+
+
+def eval_diag_A(X, t, D, c, gamma, A, lam=1.0, max_iter=1000, tol=1e-8, nthreads=0):
+    """NEXT-2: diagonal J with H(p) = sqrt(<p, A p>), A SPD [n,n].  The spectral
+    form A = Q diag(Lam) Q^T the paper's projection needs is computed here in fp64 (numpy eigh);
+    returns phi, grad, iters."""
+    X = _f64(X)
+    M, n = X.shape
+    t = _f64(t, (M,))
+    D = _f64(D, (n,))
+    c = _f64(c, (n,)) if c is not None else None
+    A = _f64(A, (n, n))
+    Lam, Q = np.linalg.eigh(A)
+    Q = np.ascontiguousarray(Q)
+    Lam = np.ascontiguousarray(Lam)
+    phi = np.empty(M)
+    grad = np.empty((M, n))
+    iters = np.empty(M, dtype=np.int32)
+    ip = ctypes.POINTER(ctypes.c_int32)
+    rc = _load().oracle_diag_A(M, n, _d(X), _d(t), _d(D), _d(c), float(gamma), _d(Q), _d(Lam),
+                               _d(A), float(lam), int(max_iter), float(tol), _d(phi), _d(grad),
+                               iters.ctypes.data_as(ip), int(nthreads))
+    if rc != 0:
+        raise ValueError(f"oracle_diag_A rejected its arguments (rc={rc})")
     return phi, grad, iters

@@ -723,3 +723,84 @@ int oracle_normsq(int64_t M, int n, const double *X, const double *t, int jk, do
   }
   return 0;
 }
+
+/* ---------------- H = ||.||_A with a full SPD A (NEXT-2) ------------------- */
+/* prox of tau ||.||_A: u - tau pi_{E_A}(u / tau) (Moreau), pi_{E_A}(w) = P pi_{E_D}(P^T w) with
+ * A = P D P^T; pi_{E_D} by prox_ell's Newton on mu (the diagonal case, with
+ * w = D).  Q [n*n] row-major, columns = eigenvectors; Lam [n] eigenvalues. */
+static void prox_ellA(int n, const double *u, double tau, const double *Q, const double *Lam,
+                      double *s1, double *s2, double *out) {
+  for (int i = 0; i < n; i++) {        /* s1 = Q^T u */
+    double a = 0.0;
+    for (int k = 0; k < n; k++) a += Q[(size_t)k * n + i] * u[k];
+    s1[i] = a;
+  }
+  prox_ell(n, s1, tau, Lam, s2);       /* prox of tau ||.||_Lam in the eigenbasis */
+  for (int i = 0; i < n; i++) {        /* out = Q s2 */
+    double a = 0.0;
+    for (int k = 0; k < n; k++) a += Q[(size_t)i * n + k] * s2[k];
+    out[i] = a;
+  }
+}
+
+static int solve_diagA_point(int n, const double *x, double t, const double *D, const double *c,
+                             double gamma, const double *Q, const double *Lam, const double *A,
+                             double lambda, int max_iter, double tol, double *phi, double *grad,
+                             double *ws) {
+  double *xt = ws, *v = ws + n, *d = ws + 2 * n, *b = ws + 3 * n;
+  double *vp = ws + 4 * n, *dp = ws + 5 * n, *u = ws + 6 * n, *s1 = ws + 7 * n, *s2 = ws + 8 * n;
+  if (point_invalid(n, x, t)) {
+    *phi = NAN;
+    for (int i = 0; i < n; i++) grad[i] = NAN;
+    return INT32_MIN;
+  }
+  for (int i = 0; i < n; i++) xt[i] = x[i] - (c ? c[i] : 0.0);
+  if (t == 0.0) {
+    double J = gamma;
+    for (int i = 0; i < n; i++) { J += 0.5 * xt[i] * xt[i] / D[i]; grad[i] = xt[i] / D[i]; }
+    *phi = J;
+    return 0;
+  }
+  for (int i = 0; i < n; i++) { v[i] = xt[i]; d[i] = xt[i]; b[i] = 0.0; }
+  int iters = -max_iter;
+  for (int k = 1; k <= max_iter; k++) {
+    memcpy(vp, v, sizeof(double) * n);
+    memcpy(dp, d, sizeof(double) * n);
+    for (int i = 0; i < n; i++) v[i] = (xt[i] + lambda * (d[i] - b[i])) / (D[i] + lambda);  /* (3.4a) */
+    for (int i = 0; i < n; i++) u[i] = v[i] + b[i];
+    prox_ellA(n, u, t / lambda, Q, Lam, s1, s2, d);                                         /* (3.4b) */
+    for (int i = 0; i < n; i++) b[i] = b[i] + v[i] - d[i];                                  /* (3.4c) */
+    if (sqdist(n, v, vp) <= tol && sqdist(n, d, dp) <= tol && sqdist(n, d, v) <= tol) {
+      iters = k;
+      break;
+    }
+  }
+  double xd = 0.0, dDd = 0.0, dAd = 0.0;
+  for (int i = 0; i < n; i++) {
+    xd += xt[i] * d[i];
+    dDd += d[i] * D[i] * d[i];
+    for (int j = 0; j < n; j++) dAd += d[i] * A[(size_t)i * n + j] * d[j];
+    grad[i] = d[i];
+  }
+  *phi = xd - 0.5 * dDd - t * sqrt(fmax(dAd, 0.0)) + gamma;
+  return iters;
+}
+
+int oracle_diag_A(int64_t M, int n, const double *X, const double *t, const double *D,
+                  const double *c, double gamma, const double *Q, const double *Lam,
+                  const double *A, double lambda, int max_iter, double tol, double *phi,
+                  double *grad, int32_t *iters, int nthreads) {
+  if (M < 0 || n < 1 || !D || !Q || !Lam || !A || lambda <= 0.0 || max_iter < 1 || tol < 0.0)
+    return -1;
+  int nt = nthreads_or_default(nthreads);
+#pragma omp parallel num_threads(nt)
+  {
+    double *ws = (double *)malloc(sizeof(double) * 9 * (size_t)n);
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t p = 0; p < M; p++)
+      iters[p] = solve_diagA_point(n, X + p * n, t[p], D, c, gamma, Q, Lam, A, lambda, max_iter,
+                                   tol, phi + p, grad + p * n, ws);
+    free(ws);
+  }
+  return 0;
+}

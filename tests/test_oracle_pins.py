@@ -540,3 +540,54 @@ def test_normsq_bruteforce_n2(j):
         for i in range(len(X)):
             obj = X[i, 0] * V1 + X[i, 1] * V2 - 0.5 * js ** 2 - t[i] * Hv
             assert abs(obj.max() - phi[i]) <= 2e-3 * max(1.0, abs(phi[i])), (h, i)
+
+
+# ----------------------------------------------------------------- ||.||_A, full SPD A (NEXT-2)
+def _paper_A(n):
+    """The paper's A: A_ii = 2, A_ij = 1."""
+    return np.ones((n, n)) + np.eye(n)
+
+
+def test_ellA_diagonal_A_is_ell():
+    """A = diag(w): the rotated projection must reproduce the diagonal ellipsoid solve."""
+    rng = np.random.default_rng(81)
+    n, M = 7, 100
+    w = rng.uniform(0.5, 2.0, n)
+    D = rng.uniform(0.5, 2.0, n)
+    X = rng.normal(0, 2, (M, n))
+    t = rng.uniform(0, 2, M)
+    a = oracle.eval_diag_A(X, t, D, None, 0.1, np.diag(w))
+    b = oracle.eval_diag(X, t, D, None, 0.1, "ell", w)
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(a[1], b[1], atol=1e-7)
+
+
+def test_ellA_isotropic_J_rotation_invariance():
+    """J = 1/2||.||^2 is rotation invariant, so phi_A(x) = phi_W(Q^T x) with W = eig(A) and
+    grad_A = Q grad_W (the ellipsoid solve in the eigenbasis), for the paper's A."""
+    rng = np.random.default_rng(82)
+    n, M = 8, 60
+    A = _paper_A(n)
+    Lam, Q = np.linalg.eigh(A)
+    X = rng.uniform(-10, 10, (M, n))
+    t = rng.uniform(0, 10, M)
+    a = oracle.eval_diag_A(X, t, np.ones(n), None, 0.0, A, tol=1e-20, max_iter=20000)
+    b = oracle.eval_diag(X @ Q, t, np.ones(n), None, 0.0, "ell", Lam, tol=1e-20, max_iter=20000)
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-8, atol=1e-8)
+    np.testing.assert_allclose(a[1], b[1] @ Q.T, atol=1e-6)
+
+
+def test_ellA_bruteforce_n2():
+    """n = 2: the Hopf formula with H = sqrt(<p, A p>) maximised by brute force on a grid."""
+    rng = np.random.default_rng(83)
+    A = np.array([[2.0, 0.7], [0.7, 1.0]])
+    D = np.array([0.8, 1.5])
+    X = rng.uniform(-3, 3, (10, 2))
+    t = rng.uniform(0.2, 2.0, 10)
+    phi, _, _ = oracle.eval_diag_A(X, t, D, None, 0.0, A, tol=1e-20, max_iter=50000)
+    g = np.linspace(-6, 6, 1201)
+    V1, V2 = np.meshgrid(g, g, indexing="ij")
+    Hv = np.sqrt(A[0, 0] * V1 ** 2 + 2 * A[0, 1] * V1 * V2 + A[1, 1] * V2 ** 2)
+    for i in range(len(X)):
+        obj = X[i, 0] * V1 + X[i, 1] * V2 - 0.5 * (D[0] * V1 ** 2 + D[1] * V2 ** 2) - t[i] * Hv
+        assert abs(obj.max() - phi[i]) <= 2e-3 * max(1.0, abs(phi[i])), i
