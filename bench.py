@@ -47,10 +47,12 @@ FLOPS_PER_COORD_ITER = {"l2": 17, "l1": 14, "wl1": 14, "ell": 27, "linf": 16}
 # active-set sums 2, v = clamp / shrink 2, sv 3, u 1, then the H update and the sd, sb sums:
 # l1/wl1 4 + 6, l2 3 + 6, linf 2 + 2 + 6
 FLOPS_NORMSQ = {"l1": 20, "wl1": 20, "l2": 19, "linf": 20}
+# ||.||_A (NEXT-2): the two rotations Q^T u and Q d~ (2 n FMAs each = 4 n flops per coordinate)
+# plus the diagonal iteration with one ellipsoid Newton evaluation (27): 4 n + 27
 # per-point HBM bytes: x (4n) + grad (4n) + t, phi, iters (12)
 CPU_SAMPLE = {"c1": 1024, "c2": 1_000_000, "c3": 100_000, "c4": 4096, "c5": 100_000, "c5d": 2048,
               "c2h": 200_000, "c2e": 200_000,
-              "c2i": 200_000, "t5": 1_000_000}
+              "c2i": 200_000, "t5": 1_000_000, "t4a": 200_000}
 CPU_MIN_SECONDS = 10.0
 
 
@@ -149,6 +151,9 @@ def _oracle_once(wl, X, t):
     elif wl.kind == "distance":
         oracle.distance_union(X, wl.Dk, wl.Ck, wl.gammak, lam=wl.lam, max_iter=wl.max_iter,
                               tol=wl.tol, stol=1e-5)
+    elif wl.kind == "ella":
+        oracle.eval_diag_A(X, t, wl.D, None, wl.gamma, wl.A, lam=wl.lam, max_iter=wl.max_iter,
+                           tol=wl.tol)
     elif wl.kind == "normsq":
         oracle.eval_normsq(X, t, wl.jk, wl.gamma, wl.h, wl.w, lam=wl.lam, max_iter=wl.max_iter,
                            tol=wl.tol)
@@ -186,6 +191,8 @@ def run_reference(args, wl):
 def metric_name(wl):
     if wl.kind == "maxh":
         return f"Hopf evals/sec ({wl.name}: H = min of {len(wl.maxh[0])} Hamiltonians, n={wl.n})"
+    if wl.kind == "ella":
+        return f"Hopf evals/sec ({wl.name}: J = 1/2<x, D^-1 x>, H = ||.||_A full SPD, n={wl.n})"
     if wl.kind == "normsq":
         jn = "1/2||.||_1^2" if wl.jk == "l1sq" else "1/2||.||_inf^2"
         return f"Hopf evals/sec ({wl.name}: J = {jn}, H = {wl.h}, n={wl.n})"
@@ -275,6 +282,12 @@ def main():
         def step():
             mres["r"] = hb.eval_maxh(X, t, D, None, wl.gamma, kinds, av, Wd, wl.lam, wl.max_iter,
                                      wl.tol, out=out, stream=stream)
+    elif wl.kind == "ella":
+        import numpy as _np
+        lam_A, Q_A = _np.linalg.eigh(wl.A)
+        D, Qd, Ld = f32(wl.D), f32(_np.ascontiguousarray(Q_A)), f32(lam_A)
+        step = lambda: hb.eval_diag_A(X, t, D, None, wl.gamma, Qd, Ld, wl.lam, wl.max_iter, wl.tol,
+                                      out=out, stream=stream)
     elif wl.kind == "normsq":
         w = f32(wl.w)
         step = lambda: hb.eval_normsq(X, t, wl.jk, wl.gamma, wl.h, w, wl.lam, wl.max_iter, wl.tol,
@@ -300,7 +313,7 @@ def main():
     # total split Bregman iterations of one step (all solves: union sets, Newton evaluations),
     # from the library's instrumentation counter in one extra untimed step
     inner_iters = None
-    if wl.kind in ("diag", "union", "distance", "maxh", "normsq"):
+    if wl.kind in ("diag", "union", "distance", "maxh", "normsq", "ella"):
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         hb.set_iteration_counter(cnt)
         step()
@@ -390,7 +403,7 @@ def main():
                "h2d_bytes_per_step": int(Xp.numel() * 4 + tp.numel() * 4),
                "d2h_bytes_per_step": int(M * 4 + M * n * 4 + M * 4),
                "api": "hopf_eval_diag_host (pinned host buffers, chunked H2D/kernel/D2H pipeline)"}
-    elif not args.no_e2e and wl.kind == "normsq":
+    elif not args.no_e2e and wl.kind in ("normsq", "ella"):
         # no host-buffer entry point: pinned H2D of x and t, the call, D2H of phi, grad, iters
         Xp = torch.from_numpy(Xh).pin_memory()
         tp = torch.from_numpy(th).pin_memory()
@@ -420,7 +433,8 @@ def main():
         e2e = {"value": M * ws * ksteps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(Xp.numel() * 4 + tp.numel() * 4),
                "d2h_bytes_per_step": int(M * 4 + M * n * 4 + M * 4),
-               "api": "hopf_eval_normsq with torch pinned copies on the same stream"}
+               "api": f"{'hopf_eval_normsq' if wl.kind == 'normsq' else 'hopf_eval_diag_A'} "
+                      "with torch pinned copies on the same stream"}
 
     if rank != 0:
         if ws > 1:
@@ -433,13 +447,13 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     conv = iters_np[iters_np > 0]
     roof = None
-    if wl.kind in ("diag", "union", "distance", "maxh", "normsq"):
+    if wl.kind in ("diag", "union", "distance", "maxh", "normsq", "ella"):
         it_sum = float(inner_iters)
         # algorithmic HBM bytes per point: diag x in, grad out (4n each) + t, phi, iters;
         # union / distance also write y (closest point / projection) and k*
-        hbm_per_point = (8 * n + 12) if wl.kind in ("diag", "maxh", "normsq") else (12 * n + 16)
-        fpc = (FLOPS_NORMSQ[wl.h] if wl.kind == "normsq"
-               else FLOPS_PER_COORD_ITER["l1" if wl.kind == "maxh" else wl.h])
+        hbm_per_point = (8 * n + 12) if wl.kind in ("diag", "maxh", "normsq", "ella") else (12 * n + 16)
+        fpc = (FLOPS_NORMSQ[wl.h] if wl.kind == "normsq" else (4 * n + 27 if wl.kind == "ella"
+               else FLOPS_PER_COORD_ITER["l1" if wl.kind == "maxh" else wl.h]))
         flops = it_sum * n * fpc
         achieved = flops / (ms_step / 1e3) / 1e12
         peak = sms * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12

@@ -98,6 +98,17 @@ int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float
                     float *grad, int32_t *iters, float *Y, int32_t *kstar, float *phi_k,
                     hopf_stream_t stream);
 
+/* H(p) = ||p||_A = sqrt(<p, A p>) with a full SPD A (NEXT-2; the ||y||_A column of
+ * Tables 1-4) and the diagonal J of hopf_eval_diag.  A is given in spectral form,
+ * A = Q diag(Lam) Q^T: Q [n*n] DEVICE row-major with the eigenvectors as columns (orthogonal),
+ * Lam [n] DEVICE > 0.  The prox is u - tau Q pi_{E_Lam}(Q^T u / tau) (ellipsoid projection in the
+ * eigenbasis, Newton on its multiplier, reading R27).  1 <= n <= 128.  Other arguments, outputs,
+ * status codes and errors as hopf_eval_diag. */
+int hopf_eval_diag_A(int64_t M, int32_t n, const float *X, const float *t, const float *Dj,
+                     const float *c, float gamma, const float *Q, const float *Lam, float lambda,
+                     int32_t max_iter, float tol, float *phi, float *grad, int32_t *iters,
+                     hopf_stream_t stream);
+
 /* Non-quadratic initial data (NEXT-3; Tables 2, 3 and 5):
  *   HOPF_J_L1SQ  : J(x) = 1/2 ||x||_1^2 + gamma    (J* = 1/2 ||.||_inf^2)
  *   HOPF_J_LINFSQ: J(x) = 1/2 ||x||_inf^2 + gamma  (J* = 1/2 ||.||_1^2)

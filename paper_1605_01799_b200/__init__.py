@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
-__all__ = ["lib", "eval_diag", "eval_union", "eval_dense", "DensePlan", "eval_diag_host", "eval_normsq",
+__all__ = ["lib", "eval_diag", "eval_union", "eval_dense", "DensePlan", "eval_diag_host", "eval_normsq", "eval_diag_A",
            "HopfError", "H_KINDS", "INVALID"]
 
 _PKG = Path(__file__).resolve().parent
@@ -40,6 +40,8 @@ def lib():
                                      vp, vp, vp, vp]
         L.hopf_eval_normsq.argtypes = [i64, i32, vp, vp, ctypes.c_int, f32, ctypes.c_int, vp, f32,
                                        i32, f32, vp, vp, vp, vp]
+        L.hopf_eval_diag_A.argtypes = [i64, i32, vp, vp, vp, vp, f32, vp, vp, f32, i32, f32, vp, vp,
+                                       vp, vp]
         L.hopf_eval_union.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, ctypes.c_int, vp, f32, i32,
                                       f32, vp, vp, vp, vp, vp, vp, vp]
         L.hopf_dense_plan_create.argtypes = [i32, vp, vp, f32, ctypes.POINTER(vp)]
@@ -54,7 +56,7 @@ def lib():
                                           vp, vp, vp, vp, vp, vp, vp]
         for f in (L.hopf_eval_diag, L.hopf_eval_union, L.hopf_dense_plan_create,
                   L.hopf_dense_plan_destroy, L.hopf_eval_dense, L.hopf_eval_diag_host,
-                  L.hopf_distance_union, L.hopf_eval_maxh, L.hopf_eval_normsq):
+                  L.hopf_distance_union, L.hopf_eval_maxh, L.hopf_eval_normsq, L.hopf_eval_diag_A):
             f.restype = ctypes.c_int
         L.hopf_last_error.restype = ctypes.c_char_p
         L.hopf_strerror.restype = ctypes.c_char_p
@@ -164,6 +166,22 @@ def eval_union(X, t, Dk, Ck, gammak, h="l2", w=None, lam=1.0, max_iter=1000, tol
                                _ptr(pk, "f32", M * K, "phik"), _stream(stream))
     _check(rc, "hopf_eval_union")
     return phi, grad, iters, Y, ks, pk
+
+
+def eval_diag_A(X, t, D, c, gamma, Q, Lam, lam=1.0, max_iter=1000, tol=1e-8, out=None,
+                stream=None):
+    """hopf_eval_diag_A (NEXT-2): diagonal J, H(p) = sqrt(<p, A p>), A = Q diag(Lam) Q^T given in
+    spectral form (Q [n,n] eigenvectors as columns, Lam [n]; float32 CUDA tensors)."""
+    M, n = X.shape
+    phi, grad, iters = _outputs(M, n, X.device, out)
+    rc = lib().hopf_eval_diag_A(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                                _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma),
+                                _ptr(Q, "f32", n * n, "Q"), _ptr(Lam, "f32", n, "Lam"), float(lam),
+                                int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                                _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                                _stream(stream))
+    _check(rc, "hopf_eval_diag_A")
+    return phi, grad, iters
 
 
 J_KINDS = {"l1sq": 0, "linfsq": 1}

@@ -71,3 +71,41 @@ extern "C" int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const floa
   g_last_kernel = j == HOPF_J_L1SQ ? "hopf_normsq_kernel<l1sq>" : "hopf_normsq_kernel<linfsq>";
   return check_launch("hopf_normsq_kernel");
 }
+
+// ---------------------------------------------------------------- NEXT-2: ||.||_A, full SPD A
+#include "ella_kernel.cuh"
+
+extern "C" int hopf_eval_diag_A(int64_t M, int32_t n, const float *X, const float *t,
+                                const float *Dj, const float *c, float gamma, const float *Q,
+                                const float *Lam, float lambda, int32_t max_iter, float tol,
+                                float *phi, float *grad, int32_t *iters, hopf_stream_t stream) {
+  using namespace hopf;
+  g_launches = 0;
+  if (M < 0 || n < 1) return set_error(HOPF_EINVAL, "M=%lld n=%d", (long long)M, n);
+  if (!(lambda > 0.f) || !std::isfinite(lambda)) return set_error(HOPF_EINVAL, "lambda must be > 0 and finite");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return set_error(HOPF_EINVAL, "tol must be >= 0");
+  if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
+  if (n > 128) return set_error(HOPF_EUNSUPPORTED, "hopf_eval_diag_A supports n <= 128 (n=%d)", n);
+  if (M == 0) return HOPF_OK;
+  if (!X || !t || !Dj || !Q || !Lam || !phi || !grad || !iters)
+    return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  EllAParams p{};
+  p.M = M; p.n = n; p.X = X; p.t = t; p.D = Dj; p.c = c; p.Q = Q; p.Lam = Lam;
+  p.gamma = gamma; p.lambda = lambda; p.tol = tol; p.max_iter = max_iter;
+  p.phi = phi; p.grad = grad; p.iters = iters; p.iter_total = g_iter_counter;
+  void (*fn)(const EllAParams) = n <= 32 ? hopf_ella_kernel<1> : (n <= 64 ? hopf_ella_kernel<2> : hopf_ella_kernel<4>);
+  const size_t smem = sizeof(float) * ((size_t)2 * n * n + n + (size_t)ELLA_WARPS * n);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * ELLA_WARPS, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  int64_t blocks = (int64_t)num_sms() * per_sm;
+  const int64_t need = (M + ELLA_WARPS - 1) / ELLA_WARPS;
+  if (blocks > need) blocks = need;
+  fn<<<(unsigned)blocks, 32 * ELLA_WARPS, smem, (cudaStream_t)stream>>>(p);
+  g_launches = 1;
+  g_last_threads = 32 * ELLA_WARPS;
+  g_last_blocks = (int)blocks;
+  g_last_kernel = "hopf_ella_kernel";
+  return check_launch("hopf_ella_kernel");
+}

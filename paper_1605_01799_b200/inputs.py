@@ -143,6 +143,17 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
         if hh == "wl1":
             wl.w = (1.0 + np.arange(n) / max(n - 1, 1)).astype(np.float32)   # the paper's D_ii
         return wl
+    if name.startswith("t4a"):
+        # NEXT-2, Table 4's ||y||_A column: J = 1/2<., D^{-1}.>,
+        # D_ii = 1 + (i-1)/(n-1), H = sqrt(<p, A p>) with A_ii = 2, A_ij = 1; x ~ U[-10,10]^n,
+        # t ~ U[0,10].  t4a[_n], n = 16 by default.
+        body = name.split("_")
+        n = n or (int(body[1]) if len(body) > 1 else 16)
+        D = (1.0 + np.arange(n) / max(n - 1, 1)).astype(np.float32)
+        wl = Workload(name, n, M or 1_000_000, "A", "ella", seed or SEED_BASE + 300 + n,
+                      ("uniform", -10.0, 10.0), ("uniform", 0.0, 10.0), D=D, gamma=0.0)
+        wl.A = np.ones((n, n)) + np.eye(n)
+        return wl
     if name == "c2e":
         # NEXT-2: C2's J and points with H(p) = sqrt(<p, diag(w) p>), w = C2's weights
         wl = config("c2", M=M, n=n, seed=seed, h="ell")
@@ -203,4 +214,4 @@ def config(name: str, M: int | None = None, n: int | None = None, seed: int | No
     raise KeyError(name)
 
 
-CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h", "c2e", "c2i", "t5")
+CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5", "c5d", "c2h", "c2e", "c2i", "t5", "t4a")

@@ -585,3 +585,42 @@ def test_normsq_ragged_and_edges(hb, n, j):
     check_normsq(hb, X, t, j, h, lam=0.8 if n > 16 else 1.0)
     with pytest.raises(hb.HopfError):
         hb.eval_normsq(dev(X), dev(t), j, 0.0, "ell", dev(np.ones(n, np.float32)))
+
+
+# ----------------------------------------------------------------- ||.||_A (NEXT-2)
+def _spectral(A):
+    lam, Q = np.linalg.eigh(A)
+    return np.ascontiguousarray(Q).astype(np.float32), lam.astype(np.float32)
+
+
+@pytest.mark.parametrize("n", [4, 8, 12, 16, 33, 100, 128])
+def test_ellA_table4_protocol(hb, n):
+    """Table 4's ||y||_A column: D_ii = 1 + (i-1)/(n-1), A = I + 11^T,
+    x ~ U[-10,10]^n, t ~ U[0,10]; plus t = 0 and invalid points."""
+    wl = inputs.config(f"t4a_{n}", M=2000)
+    X, t = inputs.points(wl)
+    X, t = X.copy(), t.copy()
+    t[0] = 0.0
+    X[1, 0] = np.nan
+    Q, L = _spectral(wl.A)
+    g = hb.eval_diag_A(dev(X), dev(t), dev(wl.D), None, 0.0, dev(Q), dev(L))
+    o = oracle.eval_diag_A(X, t, wl.D, None, 0.0, wl.A)
+    check(*g, *o, iters_slack=3, frac_exact=0.8)
+
+
+def test_ellA_random_spd_shifted_centre(hb):
+    """A random SPD A (condition ~ 10), shifted centre c, lambda != 1, n = 50."""
+    rng = np.random.default_rng(91)
+    n, M = 50, 1500
+    B = rng.normal(size=(n, n))
+    Qr, _ = np.linalg.qr(B)
+    A = (Qr * rng.uniform(0.3, 3.0, n)) @ Qr.T
+    A = 0.5 * (A + A.T)
+    D = rng.uniform(0.5, 2.0, n).astype(np.float32)
+    c = rng.normal(size=n).astype(np.float32)
+    X = rng.normal(0, 3, (M, n)).astype(np.float32)
+    t = rng.uniform(0, 2, M).astype(np.float32)
+    Q, L = _spectral(A)
+    g = hb.eval_diag_A(dev(X), dev(t), dev(D), dev(c), 0.3, dev(Q), dev(L), lam=0.8)
+    o = oracle.eval_diag_A(X, t, D, c, 0.3, A, lam=0.8)
+    check(*g, *o, iters_slack=3, frac_exact=0.8)
