@@ -4,6 +4,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../include/hopf.h"
 #include "normsq_kernel.cuh"
@@ -24,10 +26,14 @@ struct NormsqVariant {
 };
 #define HOPF_NSQ_VARIANT(G_, C_) \
   {G_, C_, {hopf_normsq_kernel<G_, C_, JK_L1SQ>, hopf_normsq_kernel<G_, C_, JK_LINFSQ>}}
-// thread per point up to n = 16 (the paper's Tables 2, 3 and 5 use n = 4..16), then groups
+// thread per point up to n = 8, pairs of lanes up to 16 (the paper's Tables 2, 3 and 5 use
+// n = 4..16; at n = 16 (t5): (2, 8) 24.7 ms, (4, 4) 29.5, (1, 16) 31.6, (8, 2) 40.3, (4, 16) 77.5),
+// then groups
 static const NormsqVariant kNormsqVariants[] = {
-    HOPF_NSQ_VARIANT(1, 4),  HOPF_NSQ_VARIANT(1, 8),   HOPF_NSQ_VARIANT(1, 16),
-    HOPF_NSQ_VARIANT(4, 16), HOPF_NSQ_VARIANT(16, 16), HOPF_NSQ_VARIANT(32, 16)};
+    HOPF_NSQ_VARIANT(1, 4),  HOPF_NSQ_VARIANT(1, 8),   HOPF_NSQ_VARIANT(2, 8),
+    HOPF_NSQ_VARIANT(4, 16), HOPF_NSQ_VARIANT(16, 16), HOPF_NSQ_VARIANT(32, 16),
+    // alternatives (HOPF_NSQ_VARIANT=G,CPL selects one; experiments)
+    HOPF_NSQ_VARIANT(1, 16), HOPF_NSQ_VARIANT(4, 4),   HOPF_NSQ_VARIANT(8, 2)};
 }  // namespace hopf
 
 using namespace hopf;
@@ -46,8 +52,16 @@ extern "C" int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const floa
   if (max_iter < 1) return set_error(HOPF_EINVAL, "max_iter must be >= 1");
   if (h == HOPF_H_WL1 && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1");
   const NormsqVariant *v = nullptr;
-  for (const NormsqVariant &c : kNormsqVariants)
-    if (c.G * c.CPL >= n) { v = &c; break; }
+  static const char *force = getenv("HOPF_NSQ_VARIANT");
+  if (force) {
+    int fg = 0, fc = 0;
+    if (sscanf(force, "%d,%d", &fg, &fc) == 2)
+      for (const NormsqVariant &c : kNormsqVariants)
+        if (c.G == fg && c.CPL == fc && fg * fc >= n) { v = &c; break; }
+  }
+  if (!v)
+    for (const NormsqVariant &c : kNormsqVariants)
+      if (c.G * c.CPL >= n) { v = &c; break; }
   if (!v) return set_error(HOPF_EUNSUPPORTED, "hopf_eval_normsq supports n <= 512 (n=%d)", n);
   if (M == 0) return HOPF_OK;
   if (!X || !t || !phi || !grad || !iters) return set_error(HOPF_EINVAL, "a required pointer is NULL");
