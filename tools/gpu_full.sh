@@ -8,7 +8,7 @@ timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_$TAG.log 2
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_default_$TAG.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_default_$TAG.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref_$TAG.log
-for C in c2 c5 c1 c4 c5d c2h c2e c2i; do
+for C in c2 c5 c1 c4 c5d c2h c2e c2i t5 t4a; do
   timeout 600 python bench.py --config $C --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${C}_$TAG.log 2>&1
   echo "rc=$?" >> gpurun_out/bench_${C}_$TAG.log
 done
