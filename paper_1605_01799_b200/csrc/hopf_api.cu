@@ -194,9 +194,17 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   // Block size: the one that keeps the most warps resident per SM (register-limited kernels
   // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
   struct Occ { int threads, per_sm; };
-  static thread_local KernFn cached_fn = nullptr;
-  static thread_local Occ cached{128, 1};
-  if (cached_fn != fn) {
+  // per-kernel cache (hopf_eval_maxh alternates kernels every launch: a one-entry cache re-ran
+  // the attribute and occupancy queries on the host before each of them)
+  static thread_local KernFn cache_fn[32] = {};
+  static thread_local Occ cache_occ[32];
+  static thread_local int cache_n = 0;
+  int ci = -1;
+  for (int i = 0; i < cache_n; i++)
+    if (cache_fn[i] == fn) { ci = i; break; }
+  Occ cached{128, 1};
+  if (ci >= 0) cached = cache_occ[ci];
+  if (ci < 0) {
     // kappa lives in static shared memory: ask for the full carveout so that several small
     // blocks fit per SM (the default carveout only fits one block's 4 KB + reserved 1 KB)
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -210,7 +218,7 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
     }
     if (bestc.per_sm < 1) bestc = {128, 1};
     cached = bestc;
-    cached_fn = fn;
+    if (cache_n < 32) { cache_fn[cache_n] = fn; cache_occ[cache_n] = bestc; cache_n++; }
   }
   const int threads = cached.threads;
   const int64_t groups_needed = p.M;
