@@ -87,8 +87,11 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   const int jmax = (n - gl + G - 1) / G;   // slots j < jmax are real coordinates
   float *const D_s = reinterpret_cast<float *>(dyn_smem);
   float *const w_s = reinterpret_cast<float *>(dyn_smem + 4096);
+  float *const di_s = reinterpret_cast<float *>(dyn_smem + 8192);   // 1 / (D_i + lambda)
   for (int i = threadIdx.x; i < 1024; i += THREADS) {
-    D_s[i] = i < n ? __ldg(p.D + i) : 1.f;
+    const float Dv = i < n ? __ldg(p.D + i) : 1.f;
+    D_s[i] = Dv;
+    di_s[i] = 1.f / (Dv + lam);
     if (HK == HK_WL1) w_s[i] = i < n ? __ldg(p.w + i) : 0.f;
   }
   __syncthreads();
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       const int j0 = 2 * q, j1 = 2 * q + 1;
       const bool ok0 = active && j0 < jmax, ok1 = active && j1 < jmax;
       d[q] = make_float2(ok0 ? __ldg(xrow + gl + G * j0) : 0.f, ok1 ? __ldg(xrow + gl + G * j1) : 0.f);
-      b[q] = make_float2(ok0 ? D_s[gl + G * j0] : 1.f, ok1 ? D_s[gl + G * j1] : 1.f);
+      b[q] = make_float2(di_s[gl + G * j0], di_s[gl + G * j1]);   // padded slots: x = 0 anyway
     }
     if (p.c) {
 #pragma unroll
@@ -153,6 +156,10 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       }
     }
     const float tl = tt / lam;
+    float2 fin = splat2(0.f);   // x * 0 accumulates NaN iff some x is NaN or infinite
+#pragma unroll
+    for (int q = 0; q < NP; q++) fin = fma2(d[q], splat2(0.f), fin);
+    bad |= !(fin.x == 0.f && fin.y == 0.f);
 #pragma unroll
     for (int c = 0; c < 4; c++) {
       float xh8[8], v8[8], tau8[8];
@@ -161,9 +168,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         const int j = 8 * c + e;
         const float2 xq = d[4 * c + (e >> 1)], Dq = b[4 * c + (e >> 1)];
         const float xt = (e & 1) ? xq.y : xq.x;        // x - c (0 on padded slots)
-        const float Dv = (e & 1) ? Dq.y : Dq.x;
-        bad |= !finite_f(xt);
-        const float di = __fdividef(1.f, Dv + lam);
+        const float di = (e & 1) ? Dq.y : Dq.x;
         xh8[e] = xt * di;
         v8[e] = xt;                                     // v^0 = x - c
         if (HK == HK_WL1) tau8[e] = (active && j < jmax) ? tl * w_s[gl + G * j] : 0.f;
@@ -307,6 +312,11 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       const int j0 = 2 * q, j1 = 2 * q + 1;
       b[q] = make_float2(j0 < jmax ? D_s[gl + G * j0] : 1.f, j1 < jmax ? D_s[gl + G * j1] : 1.f);
     }
+    // spec is warp-uniform (one point per warp): one branch outside the slot loops, and no
+    // per-slot validity test in the sums (padded slots hold x_hat = 0 and d = 0, so they add 0;
+    // only the stores are predicated)
+    const bool t0 = spec == 1;
+    const float gnan = __int_as_float(0x7fc00000);
 #pragma unroll
     for (int c = 0; c < 4; c++) {
       float xh8[2][8];
@@ -316,24 +326,26 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       float g8[8];
 #pragma unroll
       for (int e = 0; e < 8; e++) {
-        const int j = 8 * c + e, i = gl + G * j;
-        const bool ok = j < jmax;
         const float2 dqq = d[4 * c + (e >> 1)], Dq = b[4 * c + (e >> 1)];
         float dq = (e & 1) ? dqq.y : dqq.x;
         if (HK == HK_L2) dq = 0.f - dq;
         const float Dv = (e & 1) ? Dq.y : Dq.x;
         const float xt = xh8[0][e] * (Dv + lam);
-        if (spec == 1) {
-          dq = ok ? __fdividef(xt, Dv) : 0.f;
+        if (t0) {
+          dq = __fdividef(xt, Dv);
           qs = fmaf(0.5f * xt, dq, qs);
-        } else if (ok) {
+        } else {
           qs = fmaf(xt, dq, qs);
           qs = fmaf(-0.5f * Dv * dq, dq, qs);
           if (HK == HK_L2) hsum = fmaf(dq, dq, hsum);
-          else if (HK == HK_WL1) hsum = fmaf(w_s[i], fabsf(dq), hsum);
+          else if (HK == HK_WL1) hsum = fmaf(w_s[gl + G * (8 * c + e)], fabsf(dq), hsum);
           else hsum += fabsf(dq);
         }
-        g8[e] = (spec == 2) ? __int_as_float(0x7fc00000) : dq;
+        g8[e] = dq;
+      }
+      if (spec == 2) {
+#pragma unroll
+        for (int e = 0; e < 8; e++) g8[e] = gnan;
       }
 #pragma unroll
       for (int e = 0; e < 8; e++)
