@@ -297,14 +297,16 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
       tt = DIST ? 0.f : __ldg(p.t + pt);   // distance mode starts at s_0 = 0 (reading R24)
       bad = !(tt >= 0.f) || !finite_f(tt);
       const float *xrow = p.X + pt * (int64_t)n;
+      float2 fin = splat2(0.f);   // x * 0 accumulates NaN iff some x is NaN or infinite
 #pragma unroll
       for (int q = 0; q < NP; q++) {
         const int j0 = 2 * q, j1 = 2 * q + 1;
         const float x0 = (j0 < CPL && j0 < jmax) ? __ldg(xrow + gl + G * j0) : 0.f;
         const float x1 = (j1 < CPL && j1 < jmax) ? __ldg(xrow + gl + G * j1) : 0.f;
-        bad |= !finite_f(x0) || !finite_f(x1);
+        fin = fma2(make_float2(x0, x1), splat2(0.f), fin);
         if (UNION) xr[q] = make_float2(x0, x1); else xh[q] = make_float2(x0, x1);
       }
+      bad |= !(fin.x == 0.f && fin.y == 0.f);
     }
     bad = group_any<G>(bad);
     if (active) {
@@ -325,11 +327,11 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
       const int i0 = gl + G * j0, i1 = gl + G * j1;
       const float c0 = (cp && ok0) ? __ldg(cp + i0) : 0.f, c1 = (cp && ok1) ? __ldg(cp + i1) : 0.f;
       const float2 xv = UNION ? xr[q] : xh[q];
-      const float xt0 = ok0 ? xv.x - c0 : 0.f, xt1 = ok1 ? xv.y - c1 : 0.f;
+      const float xt0 = xv.x - c0, xt1 = xv.y - c1;   // padded slots: x = c = 0
       float di0, di1;
-      if (KSM) {
-        di0 = ok0 ? di_s[i0] : 1.f;
-        di1 = ok1 ? di_s[i1] : 1.f;
+      if (KSM) {   // shared-memory tables are padded (D = 1, w = 0)
+        di0 = j0 < CPL ? di_s[i0] : 1.f;
+        di1 = j1 < CPL ? di_s[i1] : 1.f;
       } else {
         const float D0 = ok0 ? __ldg(Dp + i0) : 1.f, D1 = ok1 ? __ldg(Dp + i1) : 1.f;
         di0 = __fdividef(1.f, D0 + lam);
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
       }
       if (!KSM) kap[q] = make_float2(ok0 ? ksign * lam * di0 : 0.f, ok1 ? ksign * lam * di1 : 0.f);
       if (HK == HK_WL1)
-        tau[q] = KSM ? make_float2(ok0 ? tl * w_s[i0] : 0.f, ok1 ? tl * w_s[i1] : 0.f)
+        tau[q] = KSM ? make_float2(j0 < CPL ? tl * w_s[i0] : 0.f, j1 < CPL ? tl * w_s[i1] : 0.f)
                      : make_float2(ok0 ? tl * __ldg(p.w + i0) : 0.f, ok1 ? tl * __ldg(p.w + i1) : 0.f);
       const float2 xt = make_float2(xt0, xt1);
       xh[q] = make_float2(xt0 * di0, xt1 * di1);
@@ -676,35 +678,35 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
     //   x - c = x_hat (D + lambda) recovered from registers.
     // t == 0: phi = J(x) = 1/2 <x-c, D^{-1}(x-c)> + gamma, grad = D^{-1}(x-c) (reading R6)
     const float *Dp = UNION ? p.D + (size_t)kset * n : p.D;
+    // Padded slots (i >= n) hold x_hat = d = 0 and add nothing, so only global loads are
+    // guarded (shared-memory tables are padded: D = 1, w = 0).  t == 0: dq = D^{-1}(x - c) and
+    // the same expression <xt, dq> - 1/2 <dq, D dq> is J(x) - gamma = 1/2 <xt, D^{-1} xt>.
     float qs = 0.f, hsum = 0.f;
     if (done && spec != 2) {
+      const bool t0 = spec == 1;
 #pragma unroll
       for (int q = 0; q < NP; q++) {
         const int j0 = 2 * q, j1 = 2 * q + 1;
         const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
         const int i0 = gl + G * j0, i1 = gl + G * j1;
-        const float D0 = ok0 ? (KSM ? D_s[i0] : __ldg(Dp + i0)) : 1.f;
-        const float D1 = ok1 ? (KSM ? D_s[i1] : __ldg(Dp + i1)) : 1.f;
+        const float D0 = KSM ? (j0 < CPL ? D_s[i0] : 1.f) : (ok0 ? __ldg(Dp + i0) : 1.f);
+        const float D1 = KSM ? (j1 < CPL ? D_s[i1] : 1.f) : (ok1 ? __ldg(Dp + i1) : 1.f);
         const float xt0 = xh[q].x * (D0 + lam), xt1 = xh[q].y * (D1 + lam);
         float2 dq = (HK == HK_L2) ? make_float2(0.f - d[q].x, 0.f - d[q].y) : d[q];
-        if (spec == 1) {
-          dq = make_float2(ok0 ? __fdividef(xt0, D0) : 0.f, ok1 ? __fdividef(xt1, D1) : 0.f);
-          qs = fmaf(0.5f * xt0, dq.x, fmaf(0.5f * xt1, dq.y, qs));
-        } else {
-          qs = fmaf(xt0, dq.x, qs);
-          qs = fmaf(-0.5f * D0 * dq.x, dq.x, qs);
-          qs = fmaf(xt1, dq.y, qs);
-          qs = fmaf(-0.5f * D1 * dq.y, dq.y, qs);
-          if (HK == HK_L2) hsum = fmaf(dq.x, dq.x, fmaf(dq.y, dq.y, hsum));
-          else if (ELL)
-            hsum = fmaf((ok0 ? w_s[i0] : 0.f) * dq.x, dq.x, fmaf((ok1 ? w_s[i1] : 0.f) * dq.y, dq.y, hsum));
-          else if (LINF)
-            hsum = fmaxf(hsum, fmaxf(fabsf(dq.x), fabsf(dq.y)));
-          else if (HK == HK_WL1)
-            hsum = fmaf(ok0 ? (KSM ? w_s[i0] : __ldg(p.w + i0)) : 0.f, fabsf(dq.x),
-                        fmaf(ok1 ? (KSM ? w_s[i1] : __ldg(p.w + i1)) : 0.f, fabsf(dq.y), hsum));
-          else hsum += fabsf(dq.x) + fabsf(dq.y);
-        }
+        if (t0) dq = make_float2(__fdividef(xt0, D0), __fdividef(xt1, D1));
+        qs = fmaf(xt0, dq.x, qs);
+        qs = fmaf(-0.5f * D0 * dq.x, dq.x, qs);
+        qs = fmaf(xt1, dq.y, qs);
+        qs = fmaf(-0.5f * D1 * dq.y, dq.y, qs);
+        if (HK == HK_L2) hsum = fmaf(dq.x, dq.x, fmaf(dq.y, dq.y, hsum));
+        else if (ELL)
+          hsum = fmaf((j0 < CPL ? w_s[i0] : 0.f) * dq.x, dq.x, fmaf((j1 < CPL ? w_s[i1] : 0.f) * dq.y, dq.y, hsum));
+        else if (LINF)
+          hsum = fmaxf(hsum, fmaxf(fabsf(dq.x), fabsf(dq.y)));
+        else if (HK == HK_WL1)
+          hsum = fmaf(KSM ? (j0 < CPL ? w_s[i0] : 0.f) : (ok0 ? __ldg(p.w + i0) : 0.f), fabsf(dq.x),
+                      fmaf(KSM ? (j1 < CPL ? w_s[i1] : 0.f) : (ok1 ? __ldg(p.w + i1) : 0.f), fabsf(dq.y), hsum));
+        else hsum += fabsf(dq.x) + fabsf(dq.y);
         d[q] = dq;   // from here on d holds the solve's gradient (+d)
       }
     }
