@@ -667,9 +667,11 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
     }
     {
       const unsigned gbit = (gl == 0) ? 1u : 0u;
-      const int nwait = __popc(__ballot_sync(0xffffffffu, waiting && gbit));
+      const unsigned wb = __ballot_sync(0xffffffffu, waiting && gbit);
+      if (wb == 0u) continue;   // the common case: one vote
+      const int nwait = __popc(wb);
       const int nhave = __popc(__ballot_sync(0xffffffffu, have && gbit));
-      if (nwait == 0 || (nwait < WAIT_THRESHOLD && nwait < nhave)) continue;
+      if (nwait < WAIT_THRESHOLD && nwait < nhave) continue;
     }
     const bool done = waiting;
 
