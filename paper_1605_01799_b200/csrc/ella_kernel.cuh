@@ -30,9 +30,23 @@ struct EllAParams {
 
 constexpr int ELLA_WARPS = 4;
 
-// dynamic shared memory: Q, Q^T [n*n each], Lambda [n], per-warp staging [ELLA_WARPS * n]
-template <int CPL>
+// sum over the G lanes of this lane's group, with only those lanes' mask (the groups of a warp
+// may have taken different branches at the end of a point)
+template <int G>
+__device__ __forceinline__ float group_sum_sub(float v) {
+  const int lane = threadIdx.x & 31;
+  const unsigned m = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
+  return v;
+}
+
+// dynamic shared memory: Q, Q^T [n*n each], Lambda [n], per-point staging [ELLA_WARPS * 32/G * n].
+// G lanes per point (G = 16: two points per warp for n <= 16, the paper's Table 4 sizes); the
+// points of a warp iterate in lockstep, a finished one frozen until its partner stops.
+template <int G, int CPL>
 __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAParams p) {
+  constexpr int GPW = 32 / G;
   extern __shared__ float sm[];
   const int n = p.n;
   float *Qs = sm, *Qt = sm + n * n, *Ls = sm + 2 * n * n, *stg = Ls + n;
@@ -44,7 +58,8 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
   for (int i = threadIdx.x; i < n; i += blockDim.x) Ls[i] = __ldg(p.Lam + i);
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  float *buf = stg + wib * n;
+  const int gl = lane & (G - 1), sub = lane / G;
+  float *buf = stg + (wib * GPW + sub) * n;
   float lmin = __int_as_float(0x7f800000);
   for (int i = 0; i < n; i++) lmin = fminf(lmin, Ls[i]);
   const float lam = p.lambda;
@@ -52,7 +67,7 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
   float xt[CPL], kap[CPL], xh[CPL], Dv[CPL], v[CPL], d[CPL], b[CPL], L[CPL];
 #pragma unroll
   for (int j = 0; j < CPL; j++) {
-    const int i = lane + 32 * j;
+    const int i = gl + G * j;
     const bool ok = i < n;
     Dv[j] = ok ? __ldg(p.D + i) : 1.f;
     kap[j] = ok ? lam / (Dv[j] + lam) : 0.f;
@@ -63,7 +78,7 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < CPL; j++)
-      if (lane + 32 * j < n) buf[lane + 32 * j] = in[j];
+      if (gl + G * j < n) buf[gl + G * j] = in[j];
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < CPL; j++) out[j] = 0.f;
@@ -71,81 +86,77 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
       const float a = buf[k];
 #pragma unroll
       for (int j = 0; j < CPL; j++) {
-        const int i = lane + 32 * j;
+        const int i = gl + G * j;
         out[j] = fmaf(i < n ? R[k * n + i] : 0.f, a, out[j]);
       }
     }
   };
 
-  const int64_t nwarps = (int64_t)gridDim.x * ELLA_WARPS;
+  const int64_t nslots = (int64_t)gridDim.x * ELLA_WARPS * GPW;
   unsigned my_iters = 0;
-  for (int64_t pt = (int64_t)blockIdx.x * ELLA_WARPS + wib; pt < p.M; pt += nwarps) {
-    const float tt = __ldg(p.t + pt);
+  for (int64_t base = ((int64_t)blockIdx.x * ELLA_WARPS + wib) * GPW; base < p.M; base += nslots) {
+    const int64_t pt = base + sub;
+    const bool have = pt < p.M;
+    const float tt = have ? __ldg(p.t + pt) : 1.f;
     bool bad = !(tt >= 0.f) || !finite_f(tt);
 #pragma unroll
     for (int j = 0; j < CPL; j++) {
-      const int i = lane + 32 * j;
-      const float xv = i < n ? __ldg(p.X + pt * n + i) : 0.f;
+      const int i = gl + G * j;
+      const float xv = (have && i < n) ? __ldg(p.X + pt * n + i) : 0.f;
       bad |= !finite_f(xv);
       xt[j] = i < n ? xv - (p.c ? __ldg(p.c + i) : 0.f) : 0.f;
       xh[j] = xt[j] / (Dv[j] + lam);
       v[j] = d[j] = xt[j];   // v^0 = d^0 = x - c, b^0 = 0 (R5)
       b[j] = 0.f;
     }
-    bad = __any_sync(0xffffffffu, bad);
-    float *grow = p.grad + pt * n;
-    if (bad || tt == 0.f) {
-      // invalid: NaN; t == 0: J(x), grad J(x) (R6)
-      float qs = 0.f;
-#pragma unroll
-      for (int j = 0; j < CPL; j++) qs = fmaf(0.5f * xt[j], xt[j] / Dv[j], qs);
-      qs = group_sum<32>(qs);
-#pragma unroll
-      for (int j = 0; j < CPL; j++)
-        if (lane + 32 * j < n) grow[lane + 32 * j] = bad ? __int_as_float(0x7fc00000) : xt[j] / Dv[j];
-      if (lane == 0) {
-        p.phi[pt] = bad ? __int_as_float(0x7fc00000) : qs + p.gamma;
-        p.iters[pt] = bad ? INT32_MIN : 0;
-      }
-      continue;
-    }
+    bad = group_any<G>(bad);
+    const bool direct = bad || tt == 0.f;   // invalid: NaN; t == 0: J(x), grad J(x) (R6)
     const float tau = tt / lam, itau = 1.f / tau;
     float mu = 0.f, dr[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; j++) dr[j] = 0.f;
+    bool live = have && !direct;
     int status = -p.max_iter;
     for (int k = 1; k <= p.max_iter; k++) {
+      if (!__any_sync(0xffffffffu, live)) break;
       float u[CPL], ur[CPL], sv = 0.f;
 #pragma unroll
       for (int j = 0; j < CPL; j++) {
         const float vn = fmaf(kap[j], d[j] - b[j], xh[j]);   // (3.4a)
         const float dv = vn - v[j];
         sv = fmaf(dv, dv, sv);
-        v[j] = vn;
         u[j] = vn + b[j];
+        if (live) v[j] = vn;
       }
       rotate(Qs, u, ur);   // u~ = Q^T u
       // diagonal ellipsoid in the eigenbasis: S1(mu) = sum Lambda u~^2 / (Lambda + mu)^2 =
       // tau^2, Newton on 1/sqrt(S1) - 1/tau from the warm start, clamp at 0 (inside: d = 0)
+      bool act = live;
+      float mut = mu;
       for (int nit = 0; nit < 30; nit++) {
         float s1 = 0.f, s2 = 0.f;
 #pragma unroll
         for (int j = 0; j < CPL; j++) {
-          const float r = 1.f / (L[j] + mu);
+          const float r = 1.f / (L[j] + mut);
           const float h = ur[j] * r;
           const float wh2 = L[j] * h * h;
           s1 += wh2;
           s2 = fmaf(wh2, r, s2);
         }
-        s1 = group_sum<32>(s1);
-        s2 = group_sum<32>(s2);
-        const float mun = s2 > 0.f ? fmaxf(fmaf(s1 / s2, fmaf(sqrtf(s1), itau, -1.f), mu), 0.f) : 0.f;
-        const bool stop = fabsf(mun - mu) <= 1e-6f * (mun + lmin);
-        mu = mun;
-        if (stop) break;
+        s1 = group_sum<G>(s1);
+        s2 = group_sum<G>(s2);
+        if (act) {
+          const float mun = s2 > 0.f ? fmaxf(fmaf(s1 / s2, fmaf(sqrtf(s1), itau, -1.f), mut), 0.f) : 0.f;
+          act = !(fabsf(mun - mut) <= 1e-6f * (mun + lmin));
+          mut = mun;
+        }
+        if (!__any_sync(0xffffffffu, act)) break;
       }
+      float drn[CPL];
 #pragma unroll
-      for (int j = 0; j < CPL; j++) dr[j] = mu * ur[j] / (L[j] + mu);   // (3.4b) in the eigenbasis
+      for (int j = 0; j < CPL; j++) drn[j] = mut * ur[j] / (L[j] + mut);   // (3.4b) in the eigenbasis
       float dn[CPL];
-      rotate(Qt, dr, dn);   // d = Q d~
+      rotate(Qt, drn, dn);   // d = Q d~
       float sd = 0.f, sb = 0.f;
 #pragma unroll
       for (int j = 0; j < CPL; j++) {
@@ -153,13 +164,36 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
         sd = fmaf(dd, dd, sd);
         const float dmv = dn[j] - v[j];
         sb = fmaf(dmv, dmv, sb);
-        d[j] = dn[j];
-        b[j] = u[j] - dn[j];                                  // (3.4c)
       }
-      sv = group_sum<32>(sv);
-      sd = group_sum<32>(sd);
-      sb = group_sum<32>(sb);
-      if (sv <= p.tol && sd <= p.tol && sb <= p.tol) { status = k; break; }
+      sv = group_sum<G>(sv);
+      sd = group_sum<G>(sd);
+      sb = group_sum<G>(sb);
+      if (live) {
+        mu = mut;
+#pragma unroll
+        for (int j = 0; j < CPL; j++) {
+          d[j] = dn[j];
+          b[j] = u[j] - dn[j];                                // (3.4c)
+          dr[j] = drn[j];
+        }
+        if (sv <= p.tol && sd <= p.tol && sb <= p.tol) { status = k; live = false; }
+      }
+    }
+    if (!have) continue;
+    float *grow = p.grad + pt * n;
+    if (direct) {
+      float qs = 0.f;
+#pragma unroll
+      for (int j = 0; j < CPL; j++) qs = fmaf(0.5f * xt[j], xt[j] / Dv[j], qs);
+      qs = group_sum_sub<G>(qs);
+#pragma unroll
+      for (int j = 0; j < CPL; j++)
+        if (gl + G * j < n) grow[gl + G * j] = bad ? __int_as_float(0x7fc00000) : xt[j] / Dv[j];
+      if (gl == 0) {
+        p.phi[pt] = bad ? __int_as_float(0x7fc00000) : qs + p.gamma;
+        p.iters[pt] = bad ? INT32_MIN : 0;
+      }
+      continue;
     }
     my_iters += (unsigned)(status > 0 ? status : -status);
     // phi = <x - c, d> - 1/2 <d, D d> - t ||d||_A + gamma, ||d||_A^2 = sum Lambda d~^2
@@ -169,17 +203,17 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
       qs = fmaf(xt[j], d[j], fmaf(-0.5f * Dv[j] * d[j], d[j], qs));
       ha = fmaf(L[j] * dr[j], dr[j], ha);
     }
-    qs = group_sum<32>(qs);
-    ha = group_sum<32>(ha);
+    qs = group_sum_sub<G>(qs);
+    ha = group_sum_sub<G>(ha);
 #pragma unroll
     for (int j = 0; j < CPL; j++)
-      if (lane + 32 * j < n) grow[lane + 32 * j] = d[j];
-    if (lane == 0) {
+      if (gl + G * j < n) grow[gl + G * j] = d[j];
+    if (gl == 0) {
       p.phi[pt] = qs - tt * sqrtf(ha) + p.gamma;
       p.iters[pt] = status;
     }
   }
-  if (p.iter_total && lane == 0 && my_iters) atomicAdd(p.iter_total, (unsigned long long)my_iters);
+  if (p.iter_total && gl == 0 && my_iters) atomicAdd(p.iter_total, (unsigned long long)my_iters);
 }
 
 }  // namespace hopf

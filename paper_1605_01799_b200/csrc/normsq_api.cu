@@ -107,14 +107,18 @@ extern "C" int hopf_eval_diag_A(int64_t M, int32_t n, const float *X, const floa
   p.M = M; p.n = n; p.X = X; p.t = t; p.D = Dj; p.c = c; p.Q = Q; p.Lam = Lam;
   p.gamma = gamma; p.lambda = lambda; p.tol = tol; p.max_iter = max_iter;
   p.phi = phi; p.grad = grad; p.iters = iters; p.iter_total = g_iter_counter;
-  void (*fn)(const EllAParams) = n <= 32 ? hopf_ella_kernel<1> : (n <= 64 ? hopf_ella_kernel<2> : hopf_ella_kernel<4>);
-  const size_t smem = sizeof(float) * ((size_t)2 * n * n + n + (size_t)ELLA_WARPS * n);
+  // two points per warp up to n = 16, then one
+  void (*fn)(const EllAParams) = n <= 16 ? hopf_ella_kernel<16, 1>
+                                 : (n <= 32 ? hopf_ella_kernel<32, 1>
+                                            : (n <= 64 ? hopf_ella_kernel<32, 2> : hopf_ella_kernel<32, 4>));
+  const int gpw = n <= 16 ? 2 : 1;
+  const size_t smem = sizeof(float) * ((size_t)2 * n * n + n + (size_t)ELLA_WARPS * gpw * n);
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * ELLA_WARPS, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   int64_t blocks = (int64_t)num_sms() * per_sm;
-  const int64_t need = (M + ELLA_WARPS - 1) / ELLA_WARPS;
+  const int64_t need = (M + ELLA_WARPS * gpw - 1) / (ELLA_WARPS * gpw);
   if (blocks > need) blocks = need;
   fn<<<(unsigned)blocks, 32 * ELLA_WARPS, smem, (cudaStream_t)stream>>>(p);
   g_launches = 1;
