@@ -108,3 +108,56 @@ def test_config_laws():
     assert c4.Lam.min() >= 0.1 and c4.Lam.max() <= 10
     c5 = inputs.config("c5")
     assert c5.K == 16 and c5.n == 64 and np.all(c5.Dk >= 0.25) and np.all(c5.Dk <= 4.0)
+
+
+def test_host_validation_next_entry_points(libpath):
+    """NEXT entry points (union / maxh / distance / normsq / diag_A / ELL / LINF kinds): argument
+    validation before any CUDA call."""
+    L = ctypes.CDLL(str(libpath))
+    L.hopf_last_error.restype = ctypes.c_char_p
+    vp, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+    L.hopf_eval_diag.argtypes = [i64, i32, vp, vp, vp, vp, f32, ctypes.c_int, vp, f32, i32, f32,
+                                 vp, vp, vp, vp]
+    # ELL needs w; LINF does not (NULL pointers then fail on X)
+    assert L.hopf_eval_diag(10, 4, None, None, None, None, 0, 3, None, 1, 10, 1e-8,
+                            None, None, None, None) == -1
+    assert b"w is required" in L.hopf_last_error()
+    assert L.hopf_eval_diag(10, 4, None, None, None, None, 0, 4, None, 1, 10, 1e-8,
+                            None, None, None, None) == -1
+    assert b"pointer" in L.hopf_last_error()
+    assert L.hopf_eval_diag(10, 4, None, None, None, None, 0, 5, None, 1, 10, 1e-8,
+                            None, None, None, None) == -1           # unknown H
+    L.hopf_eval_normsq.argtypes = [i64, i32, vp, vp, ctypes.c_int, f32, ctypes.c_int, vp, f32, i32,
+                                   f32, vp, vp, vp, vp]
+    assert L.hopf_eval_normsq(10, 4, None, None, 2, 0, 0, None, 1, 10, 1e-8, None, None, None,
+                              None) == -1                          # unknown J
+    assert L.hopf_eval_normsq(10, 4, None, None, 0, 0, 3, None, 1, 10, 1e-8, None, None, None,
+                              None) == -1                          # ELL not available
+    assert L.hopf_eval_normsq(10, 600, None, None, 0, 0, 0, None, 1, 10, 1e-8, None, None, None,
+                              None) == -2                          # n > 512
+    assert L.hopf_eval_normsq(0, 4, None, None, 0, 0, 0, None, 1, 10, 1e-8, None, None, None,
+                              None) == 0                           # M == 0
+    L.hopf_eval_diag_A.argtypes = [i64, i32, vp, vp, vp, vp, f32, vp, vp, f32, i32, f32, vp, vp,
+                                   vp, vp]
+    assert L.hopf_eval_diag_A(10, 200, None, None, None, None, 0, None, None, 1, 10, 1e-8, None,
+                              None, None, None) == -2              # n > 128
+    assert L.hopf_eval_diag_A(10, 16, None, None, None, None, 0, None, None, 1, 10, 1e-8, None,
+                              None, None, None) == -1              # NULL Q / Lam
+    assert L.hopf_eval_diag_A(10, 16, None, None, None, None, 0, None, None, 1, 0, 1e-8, None,
+                              None, None, None) == -1              # max_iter < 1
+    L.hopf_eval_union.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, ctypes.c_int, vp, f32, i32,
+                                  f32, vp, vp, vp, vp, vp, vp, vp]
+    for h in (3, 4):   # ELL / LINF unions are not instantiated: rejected before the launch
+        rc = L.hopf_eval_union(10, 8, 2, 1, 1, 1, 1, 1, h, 1, 1.0, 10, 1e-8, 1, 1, 1, None, None,
+                               None, None)
+        assert rc == -2, rc
+    L.hopf_eval_maxh.argtypes = [i64, i32, vp, vp, vp, vp, f32, i32, vp, vp, vp, f32, i32, f32, vp,
+                                 vp, vp, vp, vp]
+    kinds = np.array([0, 3], np.int32)
+    a = np.array([1.0, 1.0], np.float32)
+    assert L.hopf_eval_maxh(10, 4, 1, 1, 1, None, 0, 2, kinds.ctypes.data, a.ctypes.data, None,
+                            1.0, 10, 1e-8, 1, 1, 1, None, None) == -1   # ELL member without W
+    a[1] = 0.0
+    kinds[1] = 0
+    assert L.hopf_eval_maxh(10, 4, 1, 1, 1, None, 0, 2, kinds.ctypes.data, a.ctypes.data, None,
+                            1.0, 10, 1e-8, 1, 1, 1, None, None) == -1   # a_i <= 0
