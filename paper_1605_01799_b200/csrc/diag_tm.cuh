@@ -50,8 +50,12 @@ __device__ __forceinline__ void st8(uint32_t taddr, const float (&v)[8]) {
 // compiler does not read them before the wait
 template <int N>
 __device__ __forceinline__ void wait_ld(float (&a)[N][8]) {
-  static_assert(N >= 2 && N <= 4, "2..4 chunks");
-  if constexpr (N == 2)
+  static_assert(N >= 1 && N <= 4, "1..4 chunks");
+  if constexpr (N == 1)
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(a[0][0]), "+f"(a[0][1]), "+f"(a[0][2]), "+f"(a[0][3]), "+f"(a[0][4]), "+f"(a[0][5]), "+f"(a[0][6]), "+f"(a[0][7])
+                 :: "memory");
+  else if constexpr (N == 2)
     asm volatile("tcgen05.wait::ld.sync.aligned;"
                  : "+f"(a[0][0]), "+f"(a[0][1]), "+f"(a[0][2]), "+f"(a[0][3]), "+f"(a[0][4]), "+f"(a[0][5]), "+f"(a[0][6]), "+f"(a[0][7]),
                    "+f"(a[1][0]), "+f"(a[1][1]), "+f"(a[1][2]), "+f"(a[1][3]), "+f"(a[1][4]), "+f"(a[1][5]), "+f"(a[1][6]), "+f"(a[1][7])
@@ -319,9 +323,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     const float gnan = __int_as_float(0x7fc00000);
 #pragma unroll
     for (int c = 0; c < 4; c++) {
-      float xh8[2][8];
+      float xh8[1][8];
       ld8(T_XH + 8 * c, xh8[0]);
-      ld8(T_XH + 8 * c, xh8[1]);
       wait_ld(xh8);
       float g8[8];
 #pragma unroll
