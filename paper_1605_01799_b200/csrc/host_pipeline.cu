@@ -5,6 +5,7 @@
 // Device buffers and streams are cached per device (grown on demand, never shrunk).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/hopf.h"
@@ -12,11 +13,18 @@
 
 namespace hopf {
 namespace {
-constexpr int kStreams = 3;
+constexpr int kMaxStreams = 8;
+
+// HOPF_HOST_STREAMS (2..8, default 3) and HOPF_HOST_CHUNK_MB (default 32): tuning knobs
+int env_int(const char *name, int dflt, int lo, int hi) {
+  const char *e = getenv(name);
+  int v = e ? atoi(e) : dflt;
+  return v < lo ? lo : (v > hi ? hi : v);
+}
 
 struct DevCache {
   bool init = false;
-  cudaStream_t s[kStreams];
+  cudaStream_t s[kMaxStreams];
   char *buf = nullptr;
   size_t bytes = 0;
 };
@@ -41,8 +49,11 @@ extern "C" int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host,
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return set_error(HOPF_EINVAL, "device index %d", dev);
-  // ~16 MB of X per chunk: large enough to amortise launch + copy latency.
-  int64_t chunk = (int64_t)((16u << 20) / ((size_t)n * sizeof(float)));
+  static const int kStreams = env_int("HOPF_HOST_STREAMS", 3, 2, kMaxStreams);
+  static const int chunk_mb = env_int("HOPF_HOST_CHUNK_MB", 32, 1, 1024);
+  // ~32 MB of X per chunk: large enough to amortise launch + copy latency (C3 e2e: 16 MB
+  // 9.2e6 evals/s, 32 MB 9.9e6, 64 MB 9.6e6; 2-4 streams alike; ~79 GB/s of PCIe both ways)
+  int64_t chunk = (int64_t)(((size_t)chunk_mb << 20) / ((size_t)n * sizeof(float)));
   if (chunk < 1024) chunk = 1024;
   if (chunk > M) chunk = M;
   const size_t xb = align_up((size_t)chunk * n * 4), vb = align_up((size_t)chunk * 4);
@@ -50,7 +61,7 @@ extern "C" int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host,
   std::lock_guard<std::mutex> lock(g_mu);
   DevCache &dc = g_cache[dev];
   if (!dc.init) {
-    for (int i = 0; i < kStreams; i++) cudaStreamCreateWithFlags(&dc.s[i], cudaStreamNonBlocking);
+    for (int i = 0; i < kMaxStreams; i++) cudaStreamCreateWithFlags(&dc.s[i], cudaStreamNonBlocking);
     dc.init = true;
   }
   if (dc.bytes < per * kStreams) {
