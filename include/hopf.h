@@ -131,8 +131,10 @@ int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const float *t, hopf_
  *   W [K*n]        DEVICE weights (row i used when h_kinds[i] is HOPF_H_WL1 / HOPF_H_ELL), else may be NULL
  *   H_i(p) = a_i H_{kind_i}(p; W_i); evaluated as the kind's solve at time a_i t (t a_i H = (a_i t) H)
  *   istar [M] or NULL   index of the winning Hamiltonian (-1 on invalid points)
- * Other arguments as hopf_eval_diag.  Launches K solves + K combine steps on `stream`
- * (stream-ordered scratch via cudaMallocAsync); results valid after the stream syncs. */
+ * Other arguments as hopf_eval_diag.  Launches K solves (each at time a_i t inside the kernel)
+ * and K-1 combine steps (+ one istar initialisation) on `stream`; scratch for K > 1 is a
+ * per-device library buffer (M (n + 2) floats, grown on demand, reused), so concurrent calls on
+ * one device must not overlap; results valid after the stream syncs. */
 int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const float *Dj,
                    const float *c, float gamma, int32_t K, const int32_t *h_kinds, const float *a,
                    const float *W, float lambda, int32_t max_iter, float tol, float *phi,

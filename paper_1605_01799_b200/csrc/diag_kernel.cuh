@@ -60,6 +60,8 @@ struct DiagParams {
   unsigned long long *iter_total = nullptr;
   // distance mode (union, H = l2; NEXT-1): non-null dist selects Newton in s on psi(y,s) = 0
   float *dist = nullptr;
+  // hopf_eval_maxh: H_i = a_i H_kind is solved as time a_i t (t a_i H = (a_i t) H)
+  float tscale = 1.f;
   int max_newton = 0;
   float stol = 0.f;
 };
@@ -152,6 +154,25 @@ __device__ __forceinline__ void group_reduce3(float s1, float s2, float sv, floa
     S1 = group_sum<G>(s1);
     S2 = group_sum<G>(s2);
     ok_sv = group_sum<G>(sv) <= tol;
+  }
+}
+
+// Group totals of two partials (sv, r2) with log2(G) shuffles (transposed butterfly): ok_sv =
+// (sv total <= tol) for the whole group, r2 broadcast.
+template <int G>
+__device__ __forceinline__ void group_reduce2(float sv, float r2, float tol, bool &ok_sv, float &R2) {
+  if constexpr (G >= 2) {
+    const int lane = threadIdx.x & 31;
+    const int base = lane & ~(G - 1);
+    const bool hi = lane & (G / 2);
+    float c = (hi ? r2 : sv) + __shfl_xor_sync(0xffffffffu, hi ? sv : r2, G / 2);
+#pragma unroll
+    for (int o = G / 4; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    ok_sv = (__ballot_sync(0xffffffffu, c <= tol) >> base) & 1u;
+    R2 = __shfl_sync(0xffffffffu, c, base + G / 2);
+  } else {
+    ok_sv = sv <= tol;
+    R2 = r2;
   }
 }
 
@@ -294,7 +315,7 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
   auto load_point = [&](bool active) {
     bool bad = false;
     if (active) {
-      tt = DIST ? 0.f : __ldg(p.t + pt);   // distance mode starts at s_0 = 0 (reading R24)
+      tt = DIST ? 0.f : p.tscale * __ldg(p.t + pt);   // distance mode starts at s_0 = 0 (R24)
       bad = !(tt >= 0.f) || !finite_f(tt);
       const float *xrow = p.X + pt * (int64_t)n;
       float2 fin = splat2(0.f);   // x * 0 accumulates NaN iff some x is NaN or infinite
@@ -628,6 +649,11 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
         ok_sv = ell_ok_sv;
         ok_sb = false;
         r2 = 0.f;
+      } else if (HK == HK_L2 && !full_test) {
+        // no group of the warp can stop at this iteration (none had ||v^k - v^{k-1}||^2 <=
+        // tol): only ||v^{k+1} - v^k||^2 and ||u_{k+1}||^2 are needed, two values per group
+        group_reduce2<G>(psv, pr2, tol, ok_sv, r2);
+        ok_sd = ok_sb = false;
       } else {
         group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
       }

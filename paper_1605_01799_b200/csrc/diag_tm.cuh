@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   auto start_point = [&](bool active) {
     bool bad = false;
     if (active) {
-      tt = __ldg(p.t + pt);
+      tt = p.tscale * __ldg(p.t + pt);
       bad = !(tt >= 0.f) || !finite_f(tt);
     }
     const float *xrow = p.X + (active ? pt : 0) * (int64_t)n;

@@ -152,11 +152,6 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
 
 
 // ---------------------------------------------------------------- NEXT-4 helpers
-// t_s = a * t (a_i H = time rescaling: t a_i H(p) = (a_i t) H(p))
-__global__ void hopf_scale_t_kernel(int64_t M, const float *t, float a, float *ts) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
-    ts[i] = a * t[i];
-}
 // istar = 0 where the first solve is valid, -1 on invalid points
 __global__ void hopf_istar_init_kernel(int64_t M, const int32_t *iters, int32_t *istar) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
@@ -340,20 +335,39 @@ int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const f
   if (M == 0) return HOPF_OK;
   if (!X || !t || !Dj || !phi || !grad || !iters) return set_error(HOPF_EINVAL, "a required pointer is NULL");
   cudaStream_t st = (cudaStream_t)stream;
-  float *ts = nullptr, *phs = nullptr, *gs = nullptr;
+  // scratch for phi_i, grad_i, iters_i (i >= 1), cached per device and grown on demand: a
+  // per-call cudaMallocAsync / cudaFreeAsync pair per buffer left host-side gaps between the
+  // dependent launches on a slow host
+  static std::mutex mu;
+  static char *scratch[64] = {};
+  static size_t scratch_bytes[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return set_error(HOPF_EINVAL, "device index %d", dev);
+  float *phs = nullptr, *gs = nullptr;
   int32_t *its = nullptr;
-  if (cudaMallocAsync((void **)&ts, sizeof(float) * M, st) != cudaSuccess ||
-      (K > 1 && (cudaMallocAsync((void **)&phs, sizeof(float) * M, st) != cudaSuccess ||
-                 cudaMallocAsync((void **)&gs, sizeof(float) * M * n, st) != cudaSuccess ||
-                 cudaMallocAsync((void **)&its, sizeof(int32_t) * M, st) != cudaSuccess)))
-    return set_error(HOPF_ECUDA, "scratch allocation failed");
+  if (K > 1) {
+    const size_t a1 = ((size_t)M * 4 + 255) & ~(size_t)255, a2 = ((size_t)M * n * 4 + 255) & ~(size_t)255;
+    const size_t need = 2 * a1 + a2;
+    std::lock_guard<std::mutex> lock(mu);
+    if (scratch_bytes[dev] < need) {
+      cudaStreamSynchronize(st);
+      if (scratch[dev]) cudaFree(scratch[dev]);
+      scratch[dev] = nullptr;
+      scratch_bytes[dev] = 0;
+      if (cudaMalloc(&scratch[dev], need) != cudaSuccess) return set_error(HOPF_ECUDA, "scratch allocation failed");
+      scratch_bytes[dev] = need;
+    }
+    phs = (float *)scratch[dev];
+    its = (int32_t *)(scratch[dev] + a1);
+    gs = (float *)(scratch[dev] + 2 * a1);
+  }
   const int nb = num_sms() * 8;
   int rc = HOPF_OK;
   for (int i = 0; i < K && rc == HOPF_OK; i++) {
-    // phi_i: the diag solve with H_i = a_i H_kind(.; w_i), as (a_i t) H_kind
-    hopf_scale_t_kernel<<<nb, 256, 0, st>>>(M, t, a[i], ts);
+    // phi_i: the diag solve with H_i = a_i H_kind(.; w_i), at time a_i t
     DiagParams p{};
-    p.M = M; p.n = n; p.X = X; p.t = ts; p.D = Dj; p.c = c;
+    p.M = M; p.n = n; p.X = X; p.t = t; p.tscale = a[i]; p.D = Dj; p.c = c;
     p.w = (h_kinds[i] == HOPF_H_WL1 || h_kinds[i] == HOPF_H_ELL) ? W + (size_t)i * n : nullptr;
     p.gamma = gamma; p.lambda = lambda; p.max_iter = max_iter; p.tol = tol; p.K = 0;
     p.phi = i == 0 ? phi : phs; p.grad = i == 0 ? grad : gs; p.iters = i == 0 ? iters : its;
@@ -365,12 +379,8 @@ int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const f
       hopf_maxh_combine_kernel<<<nb, 256, 0, st>>>(M, n, i, phs, gs, its, phi, grad, iters, istar);
     }
   }
-  cudaFreeAsync(ts, st);
-  if (phs) cudaFreeAsync(phs, st);
-  if (gs) cudaFreeAsync(gs, st);
-  if (its) cudaFreeAsync(its, st);
   if (rc != HOPF_OK) return rc;
-  g_launches = 3 * K - (istar ? 0 : 1);   // K scale, K solve, K-1 combine (+ istar init)
+  g_launches = 2 * K - (istar ? 0 : 1);   // K solves, K-1 combines (+ istar init)
   g_last_kernel = "hopf_diag kernels + hopf_maxh_combine_kernel";
   return check_launch("hopf_maxh_combine_kernel");
 }
