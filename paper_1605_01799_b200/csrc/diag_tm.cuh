@@ -46,6 +46,34 @@ __device__ __forceinline__ void st8(uint32_t taddr, const float (&v)[8]) {
                   "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])),
                   "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])));
 }
+// The same with a compile-time column offset folded into the instruction (tmem[UR + imm]): the
+// base stays in one uniform register across the loop instead of one R2UR per address per trip
+template <int OFF>
+__device__ __forceinline__ void ld8o(uint32_t base, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8+%9];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(base), "n"(OFF));
+#pragma unroll
+  for (int i = 0; i < 8; i++) v[i] = __uint_as_float(r[i]);
+}
+template <int OFF>
+__device__ __forceinline__ void st8o(uint32_t base, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0+%9], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "r"(base), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])),
+                  "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])),
+                  "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+                  "n"(OFF));
+}
+template <typename F>
+__device__ __forceinline__ void static_for4(F &&f) {
+  f(std::integral_constant<int, 0>{});
+  f(std::integral_constant<int, 1>{});
+  f(std::integral_constant<int, 2>{});
+  f(std::integral_constant<int, 3>{});
+}
+
 // wait for this thread's outstanding tcgen05.ld, naming the destination registers so the
 // compiler does not read them before the wait
 template <int N>
@@ -108,8 +136,12 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tl0 = tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16);
-  const uint32_t T_XH = tl0, T_V = tl0 + 32, T_K = tl0 + 64, T_TAU = tl0 + 96;
+  // warp-uniform TMEM base; read back through a lane-0 shuffle so that the compiler can prove it
+  // uniform and keep it in one uniform register (otherwise it re-issues an R2UR before every
+  // tcgen05.ld / st: 16 per trip)
+  const uint32_t tl0 = __shfl_sync(0xffffffffu, tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16), 0);
+  const uint32_t T_XH = tl0, T_V = tl0 + 32, T_K = tl0 + 64, T_TAU = tl0 + 96;   // (the trip
+  // uses the same layout as immediate offsets from tl0)
 
   // kappa (l2: -kappa) of this lane's slots -> TMEM, once
   const float ksign = (HK == HK_L2) ? -1.f : 1.f;
@@ -207,13 +239,13 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     const bool full_test = (HK != HK_L2) || sv_ok;   // see hopf_diag_kernel: exact
     auto trip = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
-#pragma unroll
-      for (int c = 0; c < 4; c++) {
+      static_for4([&](auto ci) {
+        constexpr int c = decltype(ci)::value;
         float ch[(HK == HK_WL1) ? 4 : 3][8];   // kappa, x_hat, v (, tau)
-        ld8(T_K + 8 * c, ch[0]);
-        ld8(T_XH + 8 * c, ch[1]);
-        ld8(T_V + 8 * c, ch[2]);
-        if constexpr (HK == HK_WL1) ld8(T_TAU + 8 * c, ch[3]);
+        ld8o<64 + 8 * c>(tl0, ch[0]);          // T_K
+        ld8o<0 + 8 * c>(tl0, ch[1]);           // T_XH
+        ld8o<32 + 8 * c>(tl0, ch[2]);          // T_V
+        if constexpr (HK == HK_WL1) ld8o<96 + 8 * c>(tl0, ch[3]);   // T_TAU
         wait_ld(ch);
 #pragma unroll
         for (int e2 = 0; e2 < 4; e2++) {
@@ -259,8 +291,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
           ch[2][2 * e2] = v.x;
           ch[2][2 * e2 + 1] = v.y;
         }
-        st8(T_V + 8 * c, ch[2]);
-      }
+        st8o<32 + 8 * c>(tl0, ch[2]);          // T_V
+      });
     };
     if (full_test) trip(std::true_type{});
     else trip(std::false_type{});
