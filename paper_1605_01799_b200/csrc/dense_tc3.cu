@@ -356,7 +356,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int part = 4 * h + j;                   // which of the 8 partials of the point
     const bool writer = part == 7;                // the one thread per slot with side effects
     const int cb = 128 * h + 32 * j;              // first coordinate of this thread
-    const uint32_t t_lane = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * j);
+    // warp-uniform; the lane-0 shuffle lets the compiler prove it and keep TMEM addresses in
+    // uniform registers (no R2UR before each tcgen05.ld / st)
+    const uint32_t t_lane = __shfl_sync(0xffffffffu, tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(32 * j), 0);
     const uint32_t t_x = t_lane + 384u;           // x of the slot's point (TMEM columns 384..511)
     const uint32_t busy_addr = (rank == 0) ? smem_u32((const void *)busy) : mapa(smem_u32((const void *)busy), 0);
     const uint32_t stage_remote = mapa(bar_stage0, 0);
