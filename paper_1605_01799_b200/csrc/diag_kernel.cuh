@@ -226,7 +226,7 @@ __device__ __forceinline__ float2 lds_volatile2(const float2 *p) {
 // SMSP has a 16K-register file); the widest variants otherwise take ~195 registers and only
 // 2 warps per SMSP, which leaves the dependent FP32x2 chains exposed.
 template <int G, int CPL, int HK, bool UNION>
-__global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag_kernel(const DiagParams p) {
+__global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3) hopf_diag_kernel(const DiagParams p) {
   constexpr bool KSM = !UNION;            // -kappa in shared memory
   constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
   constexpr int GPW = 32 / G;             // groups per warp
@@ -242,10 +242,13 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
 
   // Per-slot registers (pairs).  d holds -d on the l2 path.
   float2 xh[NP], d[NP], b[NP], v[NP];
-  float2 kap[KSM ? 1 : NP];    // union: -kappa (l2) / kappa (l1) of the current set
   float2 tau[HK == HK_WL1 ? NP : 1];
-  float2 xr[UNION ? NP : 1];   // union: the raw point x (sets translate it by c_k)
-  float2 bd[UNION ? NP : 1];   // union: grad of the best set so far
+  // union: -kappa / kappa of every set in dynamic shared memory ([K][NP*G + 1] float2, the odd
+  // row stride spreads groups at different sets over the banks); x is re-read from global (L1 /
+  // L2) at each set start, and the best set's grad (and y) go to global memory when a set
+  // improves the running minimum: no per-point vectors beyond x_hat, d, b, v in registers
+  extern __shared__ float2 kapk_s[];
+  constexpr int KROW = NP * G + 1;
 
   // -kappa_i (l2) or kappa_i (l1) = lambda/(D_i+lambda), layout [pair][G] of float2
   __shared__ __align__(16) float2 kap_s[KSM ? NP * G : 1];
@@ -285,6 +288,21 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
     }
     __syncthreads();
   }
+  if (UNION) {
+    for (int e = threadIdx.x; e < p.K * KROW; e += blockDim.x) {
+      const int k = e / KROW, r = e % KROW;
+      float2 kv = splat2(0.f);
+      if (r < NP * G) {
+        const int pp = r / G, l = r % G;
+        const int i0 = l + G * (2 * pp), i1 = l + G * (2 * pp + 1);
+        const float *Dk = p.D + (size_t)k * n;
+        kv.x = (2 * pp < CPL && i0 < n) ? ksign * __fdividef(lam, __ldg(Dk + i0) + lam) : 0.f;
+        kv.y = (2 * pp + 1 < CPL && i1 < n) ? ksign * __fdividef(lam, __ldg(Dk + i1) + lam) : 0.f;
+      }
+      kapk_s[e] = kv;
+    }
+    __syncthreads();
+  }
   // ELL: min_i w_i, the scale of the Newton stopping test on mu
   float wmin = 1.f;
   if (ELL) {
@@ -304,7 +322,7 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
   float s_cur = 1.f;    // l2: shrink factor of the pending (3.4b)
   float mu = 0.f;       // ELL / LINF: multiplier of the last projection (warm start of the next)
   bool sv_ok = false;   // l2: ||v^k - v^{k-1}||^2 <= tol of the pending iteration
-  float best = 0.f;
+  float best = 0.f, bgn = 0.f;   // union: running minimum and ||grad|| of its set
   int bestk = -1, bestit = 0;
   // distance mode: Newton evaluations at s > 0 so far, bracket (s_lo, s_hi) of the root
   int nn = 0;
@@ -325,7 +343,7 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
         const float x0 = (j0 < CPL && j0 < jmax) ? __ldg(xrow + gl + G * j0) : 0.f;
         const float x1 = (j1 < CPL && j1 < jmax) ? __ldg(xrow + gl + G * j1) : 0.f;
         fin = fma2(make_float2(x0, x1), splat2(0.f), fin);
-        if (UNION) xr[q] = make_float2(x0, x1); else xh[q] = make_float2(x0, x1);
+        if (!UNION) xh[q] = make_float2(x0, x1);   // union: re-read per set in setup_solve
       }
       bad |= !(fin.x == 0.f && fin.y == 0.f);
     }
@@ -347,7 +365,11 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
       const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
       const int i0 = gl + G * j0, i1 = gl + G * j1;
       const float c0 = (cp && ok0) ? __ldg(cp + i0) : 0.f, c1 = (cp && ok1) ? __ldg(cp + i1) : 0.f;
-      const float2 xv = UNION ? xr[q] : xh[q];
+      float2 xv = xh[q];
+      if (UNION) {
+        const float *xrow = p.X + pt * (int64_t)n;
+        xv = make_float2(ok0 ? __ldg(xrow + i0) : 0.f, ok1 ? __ldg(xrow + i1) : 0.f);
+      }
       const float xt0 = xv.x - c0, xt1 = xv.y - c1;   // padded slots: x = c = 0
       float di0, di1;
       if (KSM) {   // shared-memory tables are padded (D = 1, w = 0)
@@ -358,7 +380,6 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
         di0 = __fdividef(1.f, D0 + lam);
         di1 = __fdividef(1.f, D1 + lam);
       }
-      if (!KSM) kap[q] = make_float2(ok0 ? ksign * lam * di0 : 0.f, ok1 ? ksign * lam * di1 : 0.f);
       if (HK == HK_WL1)
         tau[q] = KSM ? make_float2(j0 < CPL ? tl * w_s[i0] : 0.f, j1 < CPL ? tl * w_s[i1] : 0.f)
                      : make_float2(ok0 ? tl * __ldg(p.w + i0) : 0.f, ok1 ? tl * __ldg(p.w + i1) : 0.f);
@@ -388,7 +409,6 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
 #pragma unroll
     for (int q = 0; q < NP; q++) {
       xh[q] = d[q] = b[q] = v[q] = splat2(0.f);
-      if (!KSM) kap[q] = splat2(0.f);
     }
   }
 
@@ -416,7 +436,7 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
       for (int q = 0; q < NP; q++) {
-        const float2 kq = KSM ? lds_volatile2(kap_s + q * G + gl) : kap[q];
+        const float2 kq = KSM ? lds_volatile2(kap_s + q * G + gl) : lds_volatile2(kapk_s + kset * KROW + q * G + gl);
         if (HK == HK_L2) {
           // d[q] = -d_{k-1}, kq = -kappa, b[q] = u_k.  d_k = s_k u_k, b_k = (1 - s_k) u_k and
           // d_k - b_k = (2 s_k - 1) u_k are scalings of u_k ((3.4b), (3.4c)); a waiting group
@@ -749,23 +769,44 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
     bool point_done = done;
     bool restart = false;   // distance mode: the same point, the K sets again at a new s
     if (UNION) {
+      // ||grad|| of this set's solve (all lanes take part in the reduction)
+      float gc = 0.f;
+#pragma unroll
+      for (int q = 0; q < NP; q++) gc = fmaf(d[q].x, d[q].x, fmaf(d[q].y, d[q].y, gc));
+      gc = sqrtf(group_sum<G>(gc));
       if (done) {
         if (p.phik && gl == 0) p.phik[pt * p.K + kset] = phiv;
         if (phiv < best) {   // strict: lowest k wins ties (R19); NaN never wins
-          best = phiv; bestk = kset; bestit = wstatus;
+          best = phiv; bestk = kset; bestit = wstatus; bgn = gc;
+          // the new best set's grad and closest point go to memory now (a later, better set
+          // overwrites them): y = x - t grad/||grad||, c_k if grad = 0 (R18);
+          // distance mode: pi = y - s grad/||grad|| at the evaluated s
+          const float ign = (gc > 0.f) ? __fdividef(1.f, gc) : 0.f;
+          float *grow = p.grad + pt * (int64_t)n;
+          float *yrow = p.Y ? p.Y + pt * (int64_t)n : nullptr;
+          const float *xrow = p.X + pt * (int64_t)n;
 #pragma unroll
-          for (int q = 0; q < NP; q++) bd[q] = d[q];
+          for (int j = 0; j < CPL; j++) {
+            const int i = gl + G * j;
+            if (j < jmax) {
+              const float gj = HOPF_SLOT(d, j);
+              grow[i] = spec == 2 ? __int_as_float(0x7fc00000) : gj;
+              if (yrow) {
+                const float xj = __ldg(xrow + i);
+                float y;
+                if (DIST) y = (tt > 0.f && gc > 0.f) ? xj - tt * (gj * ign) : xj;
+                else if (gc > 0.f) y = xj - tt * (gj * ign);
+                else y = __ldg(p.c + (size_t)kset * n + i);
+                yrow[i] = y;
+              }
+            }
+          }
         }
         point_done = (spec == 2) || (kset + 1 >= p.K);
       }
-      // ||grad|| of the winner for y (all lanes participate in the reduction)
-      float gn = 0.f;
-#pragma unroll
-      for (int q = 0; q < NP; q++) gn = fmaf(bd[q].x, bd[q].x, fmaf(bd[q].y, bd[q].y, gn));
-      gn = sqrtf(group_sum<G>(gn));
-      const float ign = (gn > 0.f) ? __fdividef(1.f, gn) : 0.f;
+      const float gn = bgn;
       if (DIST && point_done && spec != 2 && bestk >= 0) {
-        // distance mode: psi(y,s) = best, grad psi = bd; Newton in s with
+        // distance mode: psi(y,s) = best, ||grad psi|| = gn; Newton in s with
         // d psi/dt = -||grad psi||, same step / stop / safeguard order as the oracle (R24-R26)
         const float s0 = tt;
         bool fin = false;
@@ -801,22 +842,15 @@ __global__ void __launch_bounds__(128, (HK >= 3 && CPL <= 16) ? 4 : 3) hopf_diag
           if (p.kstar) p.kstar[pt] = nanpt ? -1 : bestk;
           if (DIST) p.dist[pt] = nanpt ? __int_as_float(0x7fc00000) : tt;
         }
-        float *grow = p.grad + pt * (int64_t)n;
-        float *yrow = p.Y ? p.Y + pt * (int64_t)n : nullptr;
+        if (nanpt) {   // grad and y of a valid point were written when its best set finished
+          float *grow = p.grad + pt * (int64_t)n;
+          float *yrow = p.Y ? p.Y + pt * (int64_t)n : nullptr;
 #pragma unroll
-        for (int j = 0; j < CPL; j++) {
-          const int i = gl + G * j;
-          if (j < jmax) {
-            const float gj = HOPF_SLOT(bd, j);
-            grow[i] = nanpt ? __int_as_float(0x7fc00000) : gj;
-            if (yrow) {
-              float y;
-              if (nanpt) y = __int_as_float(0x7fc00000);
-              else if (DIST) y = (tt > 0.f && gn > 0.f) ? HOPF_SLOT(xr, j) - tt * (gj * ign)
-                                                          : HOPF_SLOT(xr, j);
-              else if (gn > 0.f) y = HOPF_SLOT(xr, j) - tt * (gj * ign);
-              else y = __ldg(p.c + (size_t)bestk * n + i);                  // reading R18
-              yrow[i] = y;
+          for (int j = 0; j < CPL; j++) {
+            const int i = gl + G * j;
+            if (j < jmax) {
+              grow[i] = __int_as_float(0x7fc00000);
+              if (yrow) yrow[i] = __int_as_float(0x7fc00000);
             }
           }
         }

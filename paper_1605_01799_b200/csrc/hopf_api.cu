@@ -60,10 +60,10 @@ struct Variant {
   KernFn fn[3][2];  // [h kind][union]
 };
 
-// union kernels keep x and the best grad resident too: only CPL <= 16 is instantiated
+// union kernels: n <= 256 (G * CPL <= 256), CPL <= 32
 template <int G, int C, int H>
 constexpr KernFn union_fn() {
-  if constexpr (C <= 16) return hopf_diag_kernel<G, C, H, true>;
+  if constexpr (C <= 32 && G * C <= 256) return hopf_diag_kernel<G, C, H, true>;
   else return nullptr;
 }
 #define HOPF_VARIANT(G_, C_)                                                                 \
@@ -194,8 +194,13 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   static thread_local KernFn cache_fn[32] = {};
   static thread_local Occ cache_occ[32];
   static thread_local int cache_n = 0;
+  // union: the kappa table of all K sets in dynamic shared memory ([K][NP*G + 1] float2)
+  const size_t dyn = is_union ? (size_t)p.K * (size_t)(((v->CPL + 1) / 2) * v->G + 1) * 8 : 0;
+  if (dyn > 48 * 1024 &&
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess)
+    return set_error(HOPF_EUNSUPPORTED, "union kappa table of %zu bytes does not fit", dyn);
   int ci = -1;
-  for (int i = 0; i < cache_n; i++)
+  for (int i = 0; i < cache_n && dyn == 0; i++)
     if (cache_fn[i] == fn) { ci = i; break; }
   Occ cached{128, 1};
   if (ci >= 0) cached = cache_occ[ci];
@@ -208,12 +213,12 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
     for (int th : {128, 64, 32}) {   // the kernels are built with __launch_bounds__(128, 3)
       if (th < v->G) continue;
       int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, th, 0) != cudaSuccess) continue;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, th, dyn) != cudaSuccess) continue;
       if (per_sm * th > bestc.per_sm * bestc.threads) bestc = {th, per_sm};
     }
     if (bestc.per_sm < 1) bestc = {128, 1};
     cached = bestc;
-    if (cache_n < 32) { cache_fn[cache_n] = fn; cache_occ[cache_n] = bestc; cache_n++; }
+    if (cache_n < 32 && dyn == 0) { cache_fn[cache_n] = fn; cache_occ[cache_n] = bestc; cache_n++; }
   }
   const int threads = cached.threads;
   const int64_t groups_needed = p.M;
@@ -221,7 +226,7 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   int64_t blocks = (int64_t)num_sms() * cached.per_sm;
   if (blocks > blocks_needed) blocks = blocks_needed;
   if (blocks < 1) blocks = 1;
-  fn<<<(unsigned)blocks, threads, 0, stream>>>(p);
+  fn<<<(unsigned)blocks, threads, dyn, stream>>>(p);
   g_launches += 1;
   g_last_threads = threads;
   g_last_blocks = (int)blocks;

@@ -624,3 +624,26 @@ def test_ellA_random_spd_shifted_centre(hb):
     g = hb.eval_diag_A(dev(X), dev(t), dev(D), dev(c), 0.3, dev(Q), dev(L), lam=0.8)
     o = oracle.eval_diag_A(X, t, D, c, 0.3, A, lam=0.8)
     check(*g, *o, iters_slack=3, frac_exact=0.8)
+
+
+@pytest.mark.parametrize("n,K,h", [(3, 4, "l2"), (40, 7, "wl1"), (100, 5, "l2"), (200, 3, "l1"),
+                                   (256, 2, "l2")])
+def test_union_ragged_widths(hb, n, K, h):
+    """Union kernels across the variant widths up to the n <= 256 limit (kappa tables of K sets
+    in shared memory, x re-read per set, the best set's grad / y written when it improves)."""
+    rng = np.random.default_rng(n + K)
+    Ck = (rng.standard_normal((K, n)) * 2.0).astype(np.float32)
+    a = rng.uniform(0.5, 2.0, (K, n))
+    Dk = (a * a).astype(np.float32)
+    gk = np.full(K, -0.5, np.float32)
+    w = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    M = 300
+    X = (rng.standard_normal((M, n)) * 2.0).astype(np.float32)
+    t = rng.uniform(0, 2, M).astype(np.float32)
+    t[0] = 0.0
+    want_y = h == "l2"
+    phi, grad, it, Y, ks, pk = hb.eval_union(dev(X), dev(t), dev(Dk), dev(Ck), dev(gk), h,
+                                             dev(w) if h == "wl1" else None, want_y=want_y,
+                                             want_phik=True)
+    o = oracle.eval_union(X, t, Dk, Ck, gk, h, w if h == "wl1" else None, want_y=want_y)
+    check_union(phi, grad, it, Y if want_y else None, ks, pk, o, t)
