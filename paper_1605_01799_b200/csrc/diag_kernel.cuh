@@ -176,6 +176,25 @@ __device__ __forceinline__ void group_reduce2(float sv, float r2, float tol, boo
   }
 }
 
+// Two predicates (total_a <= tol, total_b <= tol) for the group with log2(G) shuffles + a ballot
+template <int G>
+__device__ __forceinline__ void group_test2(float va, float vb, float tol, bool &ok_a, bool &ok_b) {
+  if constexpr (G >= 2) {
+    const int lane = threadIdx.x & 31;
+    const int base = lane & ~(G - 1);
+    const bool hi = lane & (G / 2);
+    float c = (hi ? vb : va) + __shfl_xor_sync(0xffffffffu, hi ? va : vb, G / 2);
+#pragma unroll
+    for (int o = G / 4; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    const unsigned bal = __ballot_sync(0xffffffffu, c <= tol);
+    ok_a = (bal >> base) & 1u;
+    ok_b = (bal >> (base + G / 2)) & 1u;
+  } else {
+    ok_a = va <= tol;
+    ok_b = vb <= tol;
+  }
+}
+
 // ---- packed fp32x2 helpers (sm_100 FADD2 / FFMA2: two slots of FP32 work per issue) --------
 __device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 // a - b as one FFMA2 with a broadcast -1 (exact: b * -1 is exact, one rounding of the sum);
@@ -669,7 +688,12 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
         ok_sv = ell_ok_sv;
         ok_sb = false;
         r2 = 0.f;
-      } else if (HK == HK_L2 && !full_test) {
+      } else if (HK != HK_L2) {
+        // l1 / wl1: the trip accumulated only ||d^k - d^{k-1}||^2 and ||v^k - v^{k-1}||^2
+        group_test2<G>(psd, psv, tol, ok_sd, ok_sv);
+        ok_sb = false;
+        r2 = 0.f;
+      } else if (!full_test) {
         // no group of the warp can stop at this iteration (none had ||v^k - v^{k-1}||^2 <=
         // tol): only ||v^{k+1} - v^k||^2 and ||u_{k+1}||^2 are needed, two values per group
         group_reduce2<G>(psv, pr2, tol, ok_sv, r2);
