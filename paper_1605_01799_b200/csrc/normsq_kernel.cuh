@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
   bool have = pt < p.M;
   int it = 0, spec = 0;
   float tt = 0.f, tau = 0.f, beta = 0.f, mu = 0.f;
+  float dbeta = 0.f, dmu = 0.f;   // last change of each multiplier: the warm start extrapolates
   unsigned my_iters = 0;
 
   auto load = [&](bool active) {
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
       it = 0;
       beta = 0.f;
       mu = 0.f;
+      dbeta = dmu = 0.f;
     }
   };
 #pragma unroll
@@ -144,7 +146,13 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
     for (int j = 0; j < CPL; j++) z[j] = fmaf(x[j], ilam, d[j] - b[j]);
     // beta = alpha S(beta): a = alpha, c = 1, e = 0; alpha = lambda (J = 1/2||.||_1^2, the
     // rescaled multiplier) or 1/lambda (J = 1/2||.||_inf^2)
-    beta = active_set_root<G, CPL>(z, JK == JK_L1SQ ? lam : ilam, 1.f, 0.f, beta, act);
+    {
+      // warm start at the linear extrapolation of the multiplier (the split Bregman iterates
+      // converge geometrically): closer starts keep the active set, so more first steps are exact
+      const float b0 = fmaxf(beta + dbeta, 0.f);
+      const float bn = active_set_root<G, CPL>(z, JK == JK_L1SQ ? lam : ilam, 1.f, 0.f, b0, act);
+      if (act) { dbeta = bn - beta; beta = bn; }
+    }
     float sv = 0.f, u[CPL];
 #pragma unroll
     for (int j = 0; j < CPL; j++) {
@@ -162,7 +170,11 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
       for (int j = 0; j < CPL; j++) s2 = fmaf(u[j], u[j], s2);
       s2 = group_sum<G>(s2);
     }
-    if (HKr == HK_LINF) mu = active_set_root<G, CPL>(u, 1.f, 0.f, tau, mu, act);
+    if (HKr == HK_LINF) {
+      const float m0 = fmaxf(mu + dmu, 0.f);
+      const float mn = active_set_root<G, CPL>(u, 1.f, 0.f, tau, m0, act);
+      if (act) { dmu = mn - mu; mu = mn; }
+    }
     const float sh = (s2 > tau * tau) ? fmaf(-tau, rsqrtf(s2), 1.f) : 0.f;
     float sd = 0.f, sb = 0.f;
 #pragma unroll
