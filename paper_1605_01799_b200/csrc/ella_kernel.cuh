@@ -49,11 +49,14 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
   constexpr int GPW = 32 / G;
   extern __shared__ float sm[];
   const int n = p.n;
-  float *Qs = sm, *Qt = sm + n * n, *Ls = sm + 2 * n * n, *stg = Ls + n;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const float q = __ldg(p.Q + e);
-    Qs[e] = q;
-    Qt[(e % n) * n + e / n] = q;
+  // rows padded to nr = n rounded up to 16 floats (>= CPL, a multiple of 4): a lane's CPL
+  // contiguous coordinates of a row are vector loads (lane l owns coordinates CPL l + j)
+  const int nr = (n + 15) & ~15;
+  float *Qs = sm, *Qt = sm + n * nr, *Ls = sm + 2 * n * nr, *stg = Ls + n;
+  for (int e = threadIdx.x; e < n * nr; e += blockDim.x) {
+    const int r = e / nr, col = e % nr;
+    Qs[e] = col < n ? __ldg(p.Q + r * n + col) : 0.f;
+    Qt[e] = col < n ? __ldg(p.Q + col * n + r) : 0.f;
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) Ls[i] = __ldg(p.Lam + i);
   __syncthreads();
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
   float xt[CPL], kap[CPL], xh[CPL], Dv[CPL], v[CPL], d[CPL], b[CPL], L[CPL];
 #pragma unroll
   for (int j = 0; j < CPL; j++) {
-    const int i = gl + G * j;
+    const int i = CPL * gl + j;
     const bool ok = i < n;
     Dv[j] = ok ? __ldg(p.D + i) : 1.f;
     kap[j] = ok ? lam / (Dv[j] + lam) : 0.f;
@@ -78,16 +81,28 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < CPL; j++)
-      if (gl + G * j < n) buf[gl + G * j] = in[j];
+      if (CPL * gl + j < n) buf[CPL * gl + j] = in[j];
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < CPL; j++) out[j] = 0.f;
-    for (int k = 0; k < n; k++) {
-      const float a = buf[k];
+    if (CPL * gl < nr) {   // lanes past the padded row have only padded slots
+      for (int k = 0; k < n; k++) {
+        const float a = buf[k];
+        const float *row = R + k * nr + CPL * gl;   // padded columns hold 0
+        if constexpr (CPL % 4 == 0) {
 #pragma unroll
-      for (int j = 0; j < CPL; j++) {
-        const int i = gl + G * j;
-        out[j] = fmaf(i < n ? R[k * n + i] : 0.f, a, out[j]);
+          for (int j4 = 0; j4 < CPL / 4; j4++) {
+            const float4 r4 = *reinterpret_cast<const float4 *>(row + 4 * j4);
+            out[4 * j4] = fmaf(r4.x, a, out[4 * j4]); out[4 * j4 + 1] = fmaf(r4.y, a, out[4 * j4 + 1]);
+            out[4 * j4 + 2] = fmaf(r4.z, a, out[4 * j4 + 2]); out[4 * j4 + 3] = fmaf(r4.w, a, out[4 * j4 + 3]);
+          }
+        } else if constexpr (CPL == 2) {
+          const float2 r2 = *reinterpret_cast<const float2 *>(row);
+          out[0] = fmaf(r2.x, a, out[0]); out[1] = fmaf(r2.y, a, out[1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < CPL; j++) out[j] = fmaf(row[j], a, out[j]);
+        }
       }
     }
   };
@@ -101,7 +116,7 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
     bool bad = !(tt >= 0.f) || !finite_f(tt);
 #pragma unroll
     for (int j = 0; j < CPL; j++) {
-      const int i = gl + G * j;
+      const int i = CPL * gl + j;
       const float xv = (have && i < n) ? __ldg(p.X + pt * n + i) : 0.f;
       bad |= !finite_f(xv);
       xt[j] = i < n ? xv - (p.c ? __ldg(p.c + i) : 0.f) : 0.f;
@@ -188,7 +203,7 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
       qs = group_sum_sub<G>(qs);
 #pragma unroll
       for (int j = 0; j < CPL; j++)
-        if (gl + G * j < n) grow[gl + G * j] = bad ? __int_as_float(0x7fc00000) : xt[j] / Dv[j];
+        if (CPL * gl + j < n) grow[CPL * gl + j] = bad ? __int_as_float(0x7fc00000) : xt[j] / Dv[j];
       if (gl == 0) {
         p.phi[pt] = bad ? __int_as_float(0x7fc00000) : qs + p.gamma;
         p.iters[pt] = bad ? INT32_MIN : 0;
@@ -207,7 +222,7 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
     ha = group_sum_sub<G>(ha);
 #pragma unroll
     for (int j = 0; j < CPL; j++)
-      if (gl + G * j < n) grow[gl + G * j] = d[j];
+      if (CPL * gl + j < n) grow[CPL * gl + j] = d[j];
     if (gl == 0) {
       p.phi[pt] = qs - tt * sqrtf(ha) + p.gamma;
       p.iters[pt] = status;

@@ -111,7 +111,7 @@ extern "C" int hopf_eval_diag_A(int64_t M, int32_t n, const float *X, const floa
   // n <= 16 (the paper's sizes): G lanes per point, 32/G points per warp; HOPF_ELLA_G selects
   // G in {2, 4, 8, 16} (experiments)
   static const char *ev = getenv("HOPF_ELLA_G");
-  const int gsel = ev ? atoi(ev) : 4;   // t4a (n = 16): G=4 2.75 ms, 8 3.11, 16 5.33
+  const int gsel = ev ? atoi(ev) : 2;   // t4a (n = 16): G=2 2.41 ms, 4 2.61, 8 2.75, 16 5.3
   void (*fn)(const EllAParams);
   int gpw = 1;
   if (n <= 16) {
@@ -120,12 +120,13 @@ extern "C" int hopf_eval_diag_A(int64_t M, int32_t n, const float *X, const floa
       case 4: fn = hopf_ella_kernel<4, 4>; gpw = 8; break;
       case 16: fn = hopf_ella_kernel<16, 1>; gpw = 2; break;
       case 8: fn = hopf_ella_kernel<8, 2>; gpw = 4; break;
-      default: fn = hopf_ella_kernel<4, 4>; gpw = 8; break;
+      default: fn = hopf_ella_kernel<2, 8>; gpw = 16; break;
     }
   } else {
     fn = n <= 32 ? hopf_ella_kernel<32, 1> : (n <= 64 ? hopf_ella_kernel<32, 2> : hopf_ella_kernel<32, 4>);
   }
-  const size_t smem = sizeof(float) * ((size_t)2 * n * n + n + (size_t)ELLA_WARPS * gpw * n);
+  const size_t nr = (size_t)((n + 15) & ~15);   // as ella_kernel.cuh
+  const size_t smem = sizeof(float) * ((size_t)2 * n * nr + n + (size_t)ELLA_WARPS * gpw * n);
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * ELLA_WARPS, smem) != cudaSuccess || per_sm < 1)
