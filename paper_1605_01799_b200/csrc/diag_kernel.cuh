@@ -249,7 +249,10 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
   constexpr bool KSM = !UNION;            // -kappa in shared memory
   constexpr int NP = (CPL + 1) / 2;       // slot pairs (an odd CPL gets one padding slot)
   constexpr int GPW = 32 / G;             // groups per warp
-  constexpr int WAIT_THRESHOLD = GPW > 1 ? GPW / 2 : 1;
+#ifndef HOPF_WAIT_NUM
+#define HOPF_WAIT_NUM 2
+#endif
+  constexpr int WAIT_THRESHOLD = GPW > 1 ? (GPW * HOPF_WAIT_NUM / 4 > 0 ? GPW * HOPF_WAIT_NUM / 4 : 1) : 1;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
