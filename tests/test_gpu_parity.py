@@ -627,7 +627,7 @@ def test_ellA_random_spd_shifted_centre(hb):
 
 
 @pytest.mark.parametrize("n,K,h", [(3, 4, "l2"), (40, 7, "wl1"), (100, 5, "l2"), (200, 3, "l1"),
-                                   (256, 2, "l2")])
+                                   (256, 2, "l2"), (256, 64, "l2")])
 def test_union_ragged_widths(hb, n, K, h):
     """Union kernels across the variant widths up to the n <= 256 limit (kappa tables of K sets
     in shared memory, x re-read per set, the best set's grad / y written when it improves)."""
