@@ -40,6 +40,12 @@ namespace hopf {
 // P:1348-1428) = clamp(u, -mu, mu) with mu the l1-ball multiplier; see the LINF branch.
 enum { HK_L1 = 0, HK_WL1 = 1, HK_L2 = 2, HK_ELL = 3, HK_LINF = 4 };
 
+// active-set Newton (HK_LINF, normsq_kernel.cuh): a step below this fraction of the multiplier
+// is accepted as the root even if the active set changed (fp32 breakpoint noise)
+#ifndef HOPF_TINY_STEP
+#define HOPF_TINY_STEP 4e-7f
+#endif
+
 struct DiagParams {
   int64_t M;
   int n;
@@ -647,7 +653,7 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
         cross = group_any<G>(cross);
         // a breakpoint at the root makes fp32 steps alternate across it: a step within a few
         // ulps of mu is accepted as the root
-        const bool tiny = fabsf(mun - mu_e) <= 4e-7f * fmaxf(mun, 1e-30f);
+        const bool tiny = fabsf(mun - mu_e) <= HOPF_TINY_STEP * fmaxf(mun, 1e-30f);
         if (act && (!cross || tiny || ++nit >= 64)) { mu = mun; act = false; }
         if (!__any_sync(0xffffffffu, act)) break;
         if (act) mu_e = mun;

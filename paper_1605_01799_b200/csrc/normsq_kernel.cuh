@@ -79,7 +79,7 @@ __device__ __forceinline__ float active_set_root(const float (&z)[CPL], float a,
     // a breakpoint at the root (|z_i| = m: coordinates clamped exactly at the multiplier, the
     // typical state of these l1 / l_inf problems near convergence) makes fp32 steps alternate
     // across it; a step within a few ulps of m is accepted as the root
-    const bool tiny = fabsf(mn - me) <= 4e-7f * fmaxf(mn, 1e-30f);
+    const bool tiny = fabsf(mn - me) <= HOPF_TINY_STEP * fmaxf(mn, 1e-30f);
     if (act && (!cross || tiny || nit >= 63)) { m = mn; act = false; }
     if (!__any_sync(0xffffffffu, act)) break;
     if (act) me = mn;
