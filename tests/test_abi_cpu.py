@@ -161,3 +161,27 @@ def test_host_validation_next_entry_points(libpath):
     kinds[1] = 0
     assert L.hopf_eval_maxh(10, 4, 1, 1, 1, None, 0, 2, kinds.ctypes.data, a.ctypes.data, None,
                             1.0, 10, 1e-8, 1, 1, 1, None, None) == -1   # a_i <= 0
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c3", "c5", "t5", "t4a", "c2h", "c5d"])
+def test_bench_reference_arm_contract(cfg):
+    """`bench.py --impl reference` (the fp64 oracle on host cores) prints one JSON line with the
+    contract's keys, on a tiny sample (no GPU needed)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
+                        "--warmup", "0", "--config", cfg, "--cpu-sample", "16"],
+                       cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e", "impl"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"].startswith(cfg)
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
