@@ -763,8 +763,23 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
     // guarded (shared-memory tables are padded: D = 1, w = 0).  t == 0: dq = D^{-1}(x - c) and
     // the same expression <xt, dq> - 1/2 <dq, D dq> is J(x) - gamma = 1/2 <xt, D^{-1} xt>.
     float qs = 0.f, hsum = 0.f;
+    // t == 0 groups are rare: one vote keeps their pass (divisions) out of the common path; it
+    // replaces d by D^{-1}(x - c) (in the l2 path's negated storage) before the common loop
+    if (__any_sync(0xffffffffu, done && spec == 1)) {
+      if (done && spec == 1) {
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          const int j0 = 2 * q, j1 = 2 * q + 1;
+          const bool ok0 = j0 < CPL && j0 < jmax, ok1 = j1 < CPL && j1 < jmax;
+          const int i0 = gl + G * j0, i1 = gl + G * j1;
+          const float D0 = KSM ? (j0 < CPL ? D_s[i0] : 1.f) : (ok0 ? __ldg(Dp + i0) : 1.f);
+          const float D1 = KSM ? (j1 < CPL ? D_s[i1] : 1.f) : (ok1 ? __ldg(Dp + i1) : 1.f);
+          const float g0 = __fdividef(xh[q].x * (D0 + lam), D0), g1 = __fdividef(xh[q].y * (D1 + lam), D1);
+          d[q] = (HK == HK_L2) ? make_float2(0.f - g0, 0.f - g1) : make_float2(g0, g1);
+        }
+      }
+    }
     if (done && spec != 2) {
-      const bool t0 = spec == 1;
 #pragma unroll
       for (int q = 0; q < NP; q++) {
         const int j0 = 2 * q, j1 = 2 * q + 1;
@@ -774,7 +789,6 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
         const float D1 = KSM ? (j1 < CPL ? D_s[i1] : 1.f) : (ok1 ? __ldg(Dp + i1) : 1.f);
         const float xt0 = xh[q].x * (D0 + lam), xt1 = xh[q].y * (D1 + lam);
         float2 dq = (HK == HK_L2) ? make_float2(0.f - d[q].x, 0.f - d[q].y) : d[q];
-        if (t0) dq = make_float2(__fdividef(xt0, D0), __fdividef(xt1, D1));
         qs = fmaf(xt0, dq.x, qs);
         qs = fmaf(-0.5f * D0 * dq.x, dq.x, qs);
         qs = fmaf(xt1, dq.y, qs);
