@@ -205,7 +205,10 @@ def eval_normsq(X, t, j, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=
 def eval_maxh(X, t, D, c, gamma, kinds, a, W=None, lam=1.0, max_iter=1000, tol=1e-8, out=None,
               stream=None):
     """hopf_eval_maxh: phi = max_i phi_i for H = min_i a_i H_{kind_i}.
-    Returns (phi, grad, iters, istar)."""
+
+    kinds: K names from H_KINDS ("l1", "wl1", "l2", "ell", "linf"); a: K scales > 0 (host);
+    W [K, n] float32 CUDA tensor, row i used by "wl1" / "ell" members (else may be None).
+    Returns (phi, grad, iters, istar) with istar the winning member (-1 on invalid points)."""
     import numpy as np
     import torch
     M, n = X.shape
