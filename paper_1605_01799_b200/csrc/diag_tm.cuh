@@ -366,16 +366,15 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         if (HK == HK_L2) dq = 0.f - dq;
         const float Dv = (e & 1) ? Dq.y : Dq.x;
         const float xt = xh8[0][e] * (Dv + lam);
-        if (t0) {
-          dq = __fdividef(xt, Dv);
-          qs = fmaf(0.5f * xt, dq, qs);
-        } else {
-          qs = fmaf(xt, dq, qs);
-          qs = fmaf(-0.5f * Dv * dq, dq, qs);
-          if (HK == HK_L2) hsum = fmaf(dq, dq, hsum);
-          else if (HK == HK_WL1) hsum = fmaf(w_s[gl + G * (8 * c + e)], fabsf(dq), hsum);
-          else hsum += fabsf(dq);
-        }
+        // t == 0 (rare; warp-uniform): dq = D^{-1} xt, and the same quadratic form
+        // <xt, dq> - 1/2 <dq, D dq> = 1/2 <xt, D^{-1} xt> = J(x) - gamma; the division sits in a
+        // real branch (not if-converted into every finalize)
+        if (__builtin_expect(t0, 0)) dq = __fdividef(xt, Dv);
+        qs = fmaf(xt, dq, qs);
+        qs = fmaf(-0.5f * Dv * dq, dq, qs);
+        if (HK == HK_L2) hsum = fmaf(dq, dq, hsum);
+        else if (HK == HK_WL1) hsum = fmaf(w_s[gl + G * (8 * c + e)], fabsf(dq), hsum);
+        else hsum += fabsf(dq);
         g8[e] = dq;
       }
       if (spec == 2) {
