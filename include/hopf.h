@@ -223,7 +223,8 @@ const char *hopf_last_kernel(void);
 const char *hopf_last_error(void);
 const char *hopf_strerror(int code);
 
-/* Library version (semantic, e.g. 100 = 0.1.0). */
+/* Library version (semantic, e.g. 200 = 0.2.0: adds hopf_distance_union, hopf_eval_maxh,
+ * hopf_eval_normsq, hopf_eval_diag_A and the HOPF_H_ELL / HOPF_H_LINF kinds to 0.1.0). */
 int32_t hopf_version(void);
 
 #ifdef __cplusplus

@@ -417,6 +417,6 @@ const char *hopf_strerror(int code) {
   }
 }
 
-int32_t hopf_version(void) { return 100; }
+int32_t hopf_version(void) { return 200; }   // 0.2.0: NEXT-1..4 entry points
 
 }  // extern "C"
