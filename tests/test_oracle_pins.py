@@ -135,6 +135,42 @@ def test_dense_against_box_qp_bruteforce():
             np.testing.assert_allclose(g[p], gb, atol=1e-8)
 
 
+def test_dense_t0_branch_initial_value():
+    """Dense t = 0 branch (reading R6; (1.1b) P:95-98, Hopf needs t > 0 P:106-107):
+    phi(x,0) = J(x) = 1/2<x,Ax> + gamma and grad = A x, with A = Q diag(Lam) Q^T.
+    Pinned three ways, none of which is the oracle's own branch:
+      (i)  the n = 5 Hopf-Lax box QP at t = 0 by 3^n KKT enumeration (the box is the point x),
+      (ii) continuity: the split Bregman branch at t = 1e-9 (itself pinned by the certificate
+           and brute-force tests) agrees with the t = 0 branch,
+      (iii) Q = I reduces to the separable closed form at t = 0.
+    A mistake such as A^{-1} for A, a dropped 1/2 or a dropped gamma fails each of them."""
+    rng = np.random.default_rng(41)
+    for n in (5, 24):
+        Q = inputs.haar_orthogonal(rng, n)
+        Lam = np.exp(rng.uniform(np.log(0.1), np.log(10), n))
+        X = rng.normal(size=(8, n))
+        gamma = 0.375
+        phi0, g0, it0 = oracle.eval_dense(X, np.zeros(8), Q, Lam, gamma, "l1")
+        assert np.all(it0 == 0)
+        if n == 5:
+            A = (Q * Lam) @ Q.T
+            for p in range(8):
+                pb, gb, _ = exact.box_qp_bruteforce(X[p], 0.0, A, None, gamma)
+                assert abs(phi0[p] - pb) < 1e-12
+                np.testing.assert_allclose(g0[p], gb, atol=1e-12)
+        phie, ge, ite = oracle.eval_dense(X, np.full(8, 1e-9), Q, Lam, gamma, "l1", **TIGHT)
+        assert np.all(ite > 0)
+        np.testing.assert_allclose(phi0, phie, atol=1e-7 * (1 + np.abs(phie)).max())
+        np.testing.assert_allclose(g0, ge, atol=1e-7)
+    Lam = np.exp(rng.uniform(np.log(0.1), np.log(10), 9))
+    X = rng.normal(size=(6, 9))
+    phi0, g0, _ = oracle.eval_dense(X, np.zeros(6), np.eye(9), Lam, -0.25, "wl1",
+                                    rng.uniform(0.5, 1.5, 9))
+    pe, ge = exact.diag_wl1_closed(X, np.zeros(6), 1.0 / Lam, None, -0.25)
+    np.testing.assert_allclose(phi0, pe, atol=1e-12)
+    np.testing.assert_allclose(g0, ge, atol=1e-12)
+
+
 def test_dense_c4_duality_certificate():
     """C4 law at n = 256: L(v) <= phi <= U(z) with a certified gap, and the box-QP
     coordinate-descent Hopf-Lax solve agrees."""
@@ -238,6 +274,82 @@ def test_bruteforce_n2_union_hopf_lax():
         assert abs(phi[0] - pl) < 1e-7
         if np.linalg.norm(g[0]) > 0:
             np.testing.assert_allclose(Y[0], yl, atol=1e-4)
+
+
+def test_union_zero_gradient_closest_point_is_centre():
+    """Reading R18: grad phi = 0 (||x - c_k*|| <= t) => y = c_k*, the Hopf-Lax minimiser
+    argmin_{||z - x|| <= t} min_k J_k(z).  Pinned to (i) the n = 2 Hopf-Lax grid
+    argmin and (ii) at n = 64 to the defining properties of that minimiser: y is feasible
+    (||x - y|| <= t) and attains phi (min_k J_k(y) = phi), which returning x (or any other point
+    than the centre) violates because J_k is strictly convex with its minimum gamma_k at c_k."""
+    # (i) n = 2, three ellipses with distinct levels (no ties), points inside a ball around a centre
+    Dk = np.array([[0.5, 2.0], [1.5, 0.7], [1.0, 1.0]])
+    Ck = np.array([[2.0, 0.0], [-1.0, 1.5], [0.5, -2.0]])
+    gk = np.array([-0.5, -0.8, -0.3])
+    J = lambda Z: np.min(np.stack([0.5 * np.sum((Z - Ck[k]) ** 2 / Dk[k], axis=1) + gk[k]
+                                   for k in range(3)]), axis=0)
+    rng = np.random.default_rng(43)
+    hits = 0
+    for _ in range(12):
+        k = rng.integers(3)
+        x = Ck[k] + rng.normal(scale=0.3, size=2)
+        t = np.linalg.norm(x - Ck[k]) + rng.uniform(0.05, 0.6)
+        phi, g, it, Y, ks, pk = oracle.eval_union(x[None], np.array([t]), Dk, Ck, gk, "l2", **TIGHT)
+        pl, yl = exact.hopf_lax_grid_2d(x, t, J, "l2")
+        assert abs(phi[0] - pl) < 1e-7
+        if np.all(g[0] == 0):
+            hits += 1
+            np.testing.assert_allclose(Y[0], yl, atol=1e-4)
+            np.testing.assert_allclose(Y[0], Ck[ks[0]], atol=0)
+            assert abs(phi[0] - gk[ks[0]]) < 1e-12
+    assert hits >= 6
+    # (ii) n = 64 with C5's sets: points near a centre, t beyond the distance
+    wl = inputs.config("c5")
+    Dk, Ck, gk = wl.Dk.astype(float), wl.Ck.astype(float), wl.gammak.astype(float)
+    gk = gk - 0.05 * np.arange(len(gk))          # distinct levels: a unique winner
+    K, n = Dk.shape
+    X = Ck[np.arange(20) % K] + rng.normal(scale=0.2, size=(20, n))
+    t = np.linalg.norm(X - Ck[np.arange(20) % K], axis=1) + 0.5
+    phi, g, it, Y, ks, pk = oracle.eval_union(X, t, Dk, Ck, gk, "l2")
+    Jk = lambda z: min(0.5 * np.sum((z - Ck[k]) ** 2 / Dk[k]) + gk[k] for k in range(K))
+    zero = np.all(g == 0, axis=1)
+    assert zero.sum() >= 10
+    for p in np.nonzero(zero)[0]:
+        assert np.linalg.norm(X[p] - Y[p]) <= t[p] + 1e-12
+        assert abs(Jk(Y[p]) - phi[p]) < 1e-12
+        assert abs(phi[p] - min(pk[p])) == 0
+
+
+def test_dense_and_union_status_codes_and_ties():
+    """Status conventions of the ABI on the dense and union branches, and the union
+    tie rule R19 (lowest k wins): a duplicated set can never win over its first copy."""
+    rng = np.random.default_rng(47)
+    n = 6
+    Q = inputs.haar_orthogonal(rng, n)
+    Lam = np.exp(rng.uniform(np.log(0.1), np.log(10), n))
+    X = rng.normal(size=(4, n))
+    X[2, 1] = np.inf
+    t = np.array([0.5, -0.1, 0.5, 0.3])
+    phi, g, it = oracle.eval_dense(X, t, Q, Lam, 0.0, "l1", max_iter=2)
+    assert it[0] == -2 and np.isfinite(phi[0]) and np.all(np.isfinite(g[0]))
+    assert it[1] == oracle.INVALID and np.isnan(phi[1]) and np.all(np.isnan(g[1]))
+    assert it[2] == oracle.INVALID
+    # not converged after 2 iterations: outputs are the Hopf objective at the last d (R1, R2)
+    A = (Q * Lam) @ Q.T
+    L = exact.dual_lower_bound(X[0], t[0], g[0], np.linalg.inv(A))
+    assert abs(phi[0] - L) < 1e-12
+    Dk = np.stack([np.full(n, 1.3), np.full(n, 0.8), np.full(n, 1.3)])
+    Ck = np.stack([np.zeros(n), np.ones(n), np.zeros(n)])      # set 2 duplicates set 0
+    gk = np.array([-0.5, -0.5, -0.5])
+    Xu = rng.normal(scale=0.5, size=(40, n))
+    tu = rng.uniform(0.1, 1.0, 40)
+    tu[5] = np.nan
+    phi, g, it, Y, ks, pk = oracle.eval_union(Xu, tu, Dk, Ck, gk, "l2")
+    assert ks[5] == -1 and it[5] == oracle.INVALID and np.isnan(phi[5]) and np.all(np.isnan(Y[5]))
+    ok = np.arange(40) != 5
+    assert np.all(ks[ok] != 2)
+    assert np.array_equal(pk[ok, 0], pk[ok, 2])
+    assert np.all(ks[ok] == np.argmin(pk[ok], axis=1))
 
 
 def test_invariants_initial_value_monotone_fd_gradient_pde():
