@@ -34,8 +34,15 @@
  *    INT32_MIN: invalid point (t < 0 or a non-finite x/t coordinate), phi/grad = NaN.
  *  - Outputs: grad := d at termination (reading R1 of DESIGN.md); phi := the Hopf
  *    objective (3.3) evaluated at d (R2).
- *  - Thread safety: calls on different streams or devices may run concurrently; the
- *    library keeps no mutable global state besides the per-thread error string.
+ *  - Thread safety and concurrency: every entry point may be called from several host threads
+ *    at once and on several streams / devices at once.  Per-call scratch (the maxh member
+ *    buffers, the dense fix-up list) is stream-ordered memory from a library-owned pool of the
+ *    current device (allocated and freed on the call's `stream`), so calls on different
+ *    streams never share it.  hopf_eval_diag_host takes one of a per-device pool of pipeline
+ *    contexts (internal streams + buffers) for the duration of the call.  Process-wide state
+ *    otherwise consists of write-once caches (SM count, kernel attributes per device) and the
+ *    per-thread error string / launch statistics.  All device pointers of a call, and a dense
+ *    plan, must belong to the CURRENT device (hopf_eval_dense checks the plan's).
  */
 #ifndef HOPF_H_
 #define HOPF_H_
@@ -132,9 +139,9 @@ int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const float *t, hopf_
  *   H_i(p) = a_i H_{kind_i}(p; W_i); evaluated as the kind's solve at time a_i t (t a_i H = (a_i t) H)
  *   istar [M] or NULL   index of the winning Hamiltonian (-1 on invalid points)
  * Other arguments as hopf_eval_diag.  Launches K solves (each at time a_i t inside the kernel)
- * and K-1 combine steps (+ one istar initialisation) on `stream`; scratch for K > 1 is a
- * per-device library buffer (M (n + 2) floats, grown on demand, reused), so concurrent calls on
- * one device must not overlap; results valid after the stream syncs. */
+ * and K-1 combine steps (+ one istar initialisation) on `stream`; scratch for K > 1 (M (n + 2)
+ * floats) is stream-ordered per call (see the concurrency convention above); results valid
+ * after the stream syncs. */
 int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const float *Dj,
                    const float *c, float gamma, int32_t K, const int32_t *h_kinds, const float *a,
                    const float *W, float lambda, int32_t max_iter, float tol, float *phi,
@@ -183,8 +190,10 @@ int hopf_dense_plan_destroy(hopf_dense_plan *plan);
  * n == 256 with H in {l1, wl1} runs the tensor-core kernel (tcgen05, fp16 hi/lo split of
  * M_lambda and of x + lambda (d - b), fp32 accumulation in TMEM); its points with t == 0,
  * invalid input or no convergence are re-solved by the FP32 kernel from a device-side list.
- * Other n (multiples of 32 up to 256) and H = l2 run the FP32 SIMT kernel.  The plan owns that
- * list: calls that share a plan must be ordered on one stream. */
+ * Other n (multiples of 32 up to 256) and H = l2 run the FP32 SIMT kernel.  The list is
+ * per-call stream-ordered scratch, so one plan may serve concurrent calls on several streams
+ * (the plan itself is read-only after creation).  HOPF_EINVAL if the current device is not the
+ * device the plan was created on. */
 int hopf_eval_dense(int64_t M, int32_t n, const float *X, const float *t,
                     const hopf_dense_plan *plan, float gamma, hopf_h_kind h, const float *w,
                     float lambda, int32_t max_iter, float tol, float *phi, float *grad,
@@ -195,7 +204,11 @@ int hopf_eval_dense(int64_t M, int32_t n, const float *X, const float *t,
  * pointers as above.  The call splits the points into chunks and pipelines
  * host->device copies, kernels and device->host copies on internal streams of the
  * current device; it returns after all results are in host memory (synchronous).
- * Device work buffers and streams are cached per device (grown on demand).                                              */
+ * Ordering: the first chunk starts after all work enqueued earlier on the legacy default
+ * stream of the current device (an event recorded there at entry; the legacy stream itself
+ * waits for all blocking streams), so parameters written there (e.g. by PyTorch's default
+ * stream) are visible; writes on the caller's non-blocking streams must be synchronised first.
+ * Internal streams and buffers are pooled per device (one context per concurrent call).     */
 int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host, const float *t_host,
                         const float *Dj, const float *c, float gamma, hopf_h_kind h,
                         const float *w, float lambda, int32_t max_iter, float tol,

@@ -7,6 +7,7 @@ CPU fallback: if the extension is missing this module raises on import of ``lib(
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from pathlib import Path
 
@@ -113,11 +114,47 @@ def _ptr(tensor, dtype_name, numel=None, name="tensor"):
     return tensor.data_ptr()
 
 
+def _host(tensor, dtype_name, numel, name):
+    """Validate a HOST tensor handed to hopf_eval_diag_host (dtype, size, contiguity): the library
+    copies exactly numel elements to / from its address."""
+    import torch
+    if not isinstance(tensor, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    want = {"f32": torch.float32, "i32": torch.int32}[dtype_name]
+    if tensor.dtype != want:
+        raise TypeError(f"{name} must be {want}, got {tensor.dtype}")
+    if tensor.is_cuda:
+        raise ValueError(f"{name} must be a host tensor (eval_diag_host)")
+    if not tensor.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if tensor.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {tensor.numel()}")
+    return tensor.data_ptr()
+
+
 def _stream(stream):
     import torch
     if stream is None:
         stream = torch.cuda.current_stream()
     return stream.cuda_stream
+
+
+@contextlib.contextmanager
+def _device_of(*tensors, stream=None):
+    """Run the enclosed library call with the tensors' device as the current CUDA device.
+
+    Every tensor (None entries skipped) and the stream must live on that device: the library
+    launches on the current device, so a foreign-device pointer would fault."""
+    import torch
+    ts = [x for x in tensors if x is not None]
+    dev = ts[0].device
+    for x in ts[1:]:
+        if x.device != dev:
+            raise ValueError(f"all tensors must live on {dev}, got one on {x.device}")
+    if stream is not None and stream.device != dev:
+        raise ValueError(f"stream is on {stream.device}, the tensors on {dev}")
+    with torch.cuda.device(dev):
+        yield
 
 
 def _outputs(M, n, device, out):
@@ -138,11 +175,12 @@ def eval_diag(X, t, D, c=None, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000
     Returns (phi [M], grad [M,n], iters [M] int32)."""
     M, n = X.shape
     phi, grad, iters = _outputs(M, n, X.device, out)
-    rc = lib().hopf_eval_diag(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
-                              _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma),
-                              H_KINDS[h], _ptr(w, "f32", n, "w"), float(lam), int(max_iter),
-                              float(tol), _ptr(phi, "f32", M, "phi"), _ptr(grad, "f32", M * n, "grad"),
-                              _ptr(iters, "i32", M, "iters"), _stream(stream))
+    with _device_of(X, t, D, c, w, phi, grad, iters, stream=stream):
+        rc = lib().hopf_eval_diag(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                                  _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma),
+                                  H_KINDS[h], _ptr(w, "f32", n, "w"), float(lam), int(max_iter),
+                                  float(tol), _ptr(phi, "f32", M, "phi"), _ptr(grad, "f32", M * n, "grad"),
+                                  _ptr(iters, "i32", M, "iters"), _stream(stream))
     _check(rc, "hopf_eval_diag")
     return phi, grad, iters
 
@@ -157,13 +195,14 @@ def eval_union(X, t, Dk, Ck, gammak, h="l2", w=None, lam=1.0, max_iter=1000, tol
     Y = torch.empty((M, n), dtype=torch.float32, device=X.device) if want_y else None
     ks = torch.empty(M, dtype=torch.int32, device=X.device) if want_kstar else None
     pk = torch.empty((M, K), dtype=torch.float32, device=X.device) if want_phik else None
-    rc = lib().hopf_eval_union(M, n, K, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
-                               _ptr(Dk, "f32", K * n, "Dk"), _ptr(Ck, "f32", K * n, "Ck"),
-                               _ptr(gammak, "f32", K, "gammak"), H_KINDS[h], _ptr(w, "f32", n, "w"),
-                               float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
-                               _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
-                               _ptr(Y, "f32", M * n, "Y"), _ptr(ks, "i32", M, "kstar"),
-                               _ptr(pk, "f32", M * K, "phik"), _stream(stream))
+    with _device_of(X, t, Dk, Ck, gammak, w, phi, grad, iters, Y, ks, pk, stream=stream):
+        rc = lib().hopf_eval_union(M, n, K, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                                   _ptr(Dk, "f32", K * n, "Dk"), _ptr(Ck, "f32", K * n, "Ck"),
+                                   _ptr(gammak, "f32", K, "gammak"), H_KINDS[h], _ptr(w, "f32", n, "w"),
+                                   float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                                   _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                                   _ptr(Y, "f32", M * n, "Y"), _ptr(ks, "i32", M, "kstar"),
+                                   _ptr(pk, "f32", M * K, "phik"), _stream(stream))
     _check(rc, "hopf_eval_union")
     return phi, grad, iters, Y, ks, pk
 
@@ -174,12 +213,13 @@ def eval_diag_A(X, t, D, c, gamma, Q, Lam, lam=1.0, max_iter=1000, tol=1e-8, out
     spectral form (Q [n,n] eigenvectors as columns, Lam [n]; float32 CUDA tensors)."""
     M, n = X.shape
     phi, grad, iters = _outputs(M, n, X.device, out)
-    rc = lib().hopf_eval_diag_A(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
-                                _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma),
-                                _ptr(Q, "f32", n * n, "Q"), _ptr(Lam, "f32", n, "Lam"), float(lam),
-                                int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
-                                _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
-                                _stream(stream))
+    with _device_of(X, t, D, c, Q, Lam, phi, grad, iters, stream=stream):
+        rc = lib().hopf_eval_diag_A(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                                    _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma),
+                                    _ptr(Q, "f32", n * n, "Q"), _ptr(Lam, "f32", n, "Lam"), float(lam),
+                                    int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                                    _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                                    _stream(stream))
     _check(rc, "hopf_eval_diag_A")
     return phi, grad, iters
 
@@ -193,11 +233,12 @@ def eval_normsq(X, t, j, gamma=0.0, h="l1", w=None, lam=1.0, max_iter=1000, tol=
     gamma, H in {l1, wl1, l2, linf}.  Returns (phi [M], grad [M,n], iters [M] int32)."""
     M, n = X.shape
     phi, grad, iters = _outputs(M, n, X.device, out)
-    rc = lib().hopf_eval_normsq(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
-                                J_KINDS[j], float(gamma), H_KINDS[h], _ptr(w, "f32", n, "w"),
-                                float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
-                                _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
-                                _stream(stream))
+    with _device_of(X, t, w, phi, grad, iters, stream=stream):
+        rc = lib().hopf_eval_normsq(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                                    J_KINDS[j], float(gamma), H_KINDS[h], _ptr(w, "f32", n, "w"),
+                                    float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                                    _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                                    _stream(stream))
     _check(rc, "hopf_eval_normsq")
     return phi, grad, iters
 
@@ -219,12 +260,13 @@ def eval_maxh(X, t, D, c, gamma, kinds, a, W=None, lam=1.0, max_iter=1000, tol=1
     av = np.ascontiguousarray(a, dtype=np.float32)
     if av.shape != (K,):
         raise ValueError("a must have one scale per Hamiltonian")
-    rc = lib().hopf_eval_maxh(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
-                              _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma), K,
-                              hk.ctypes.data, av.ctypes.data, _ptr(W, "f32", K * n, "W"),
-                              float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
-                              _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
-                              _ptr(ist, "i32", M, "istar"), _stream(stream))
+    with _device_of(X, t, D, c, W, phi, grad, iters, ist, stream=stream):
+        rc = lib().hopf_eval_maxh(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"),
+                                  _ptr(D, "f32", n, "D"), _ptr(c, "f32", n, "c"), float(gamma), K,
+                                  hk.ctypes.data, av.ctypes.data, _ptr(W, "f32", K * n, "W"),
+                                  float(lam), int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                                  _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                                  _ptr(ist, "i32", M, "istar"), _stream(stream))
     _check(rc, "hopf_eval_maxh")
     return phi, grad, iters, ist
 
@@ -244,13 +286,14 @@ def distance_union(Y, Dk, Ck, gammak, lam=1.0, max_iter=1000, tol=1e-8, max_newt
     grad = torch.empty((M, n), dtype=torch.float32, device=dev)
     ks = torch.empty(M, dtype=torch.int32, device=dev)
     nn = torch.empty(M, dtype=torch.int32, device=dev)
-    rc = lib().hopf_distance_union(M, n, K, _ptr(Y, "f32", M * n, "Y"), _ptr(Dk, "f32", K * n, "Dk"),
-                                   _ptr(Ck, "f32", K * n, "Ck"), _ptr(gammak, "f32", K, "gammak"),
-                                   float(lam), int(max_iter), float(tol), int(max_newton),
-                                   float(stol), _ptr(dist, "f32", M, "dist"),
-                                   _ptr(proj, "f32", M * n, "proj"), _ptr(psi, "f32", M, "psi"),
-                                   _ptr(grad, "f32", M * n, "grad"), _ptr(ks, "i32", M, "kstar"),
-                                   _ptr(nn, "i32", M, "newton"), _stream(stream))
+    with _device_of(Y, Dk, Ck, gammak, dist, proj, psi, grad, ks, nn, stream=stream):
+        rc = lib().hopf_distance_union(M, n, K, _ptr(Y, "f32", M * n, "Y"), _ptr(Dk, "f32", K * n, "Dk"),
+                                       _ptr(Ck, "f32", K * n, "Ck"), _ptr(gammak, "f32", K, "gammak"),
+                                       float(lam), int(max_iter), float(tol), int(max_newton),
+                                       float(stol), _ptr(dist, "f32", M, "dist"),
+                                       _ptr(proj, "f32", M * n, "proj"), _ptr(psi, "f32", M, "psi"),
+                                       _ptr(grad, "f32", M * n, "grad"), _ptr(ks, "i32", M, "kstar"),
+                                       _ptr(nn, "i32", M, "newton"), _stream(stream))
     _check(rc, "hopf_distance_union")
     return dist, proj, psi, grad, ks, nn
 
@@ -289,11 +332,12 @@ def eval_dense(X, t, plan: DensePlan, gamma=0.0, h="l1", w=None, max_iter=1000, 
     """hopf_eval_dense with a DensePlan.  Returns (phi, grad, iters)."""
     M, n = X.shape
     phi, grad, iters = _outputs(M, n, X.device, out)
-    rc = lib().hopf_eval_dense(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"), plan._h,
-                               float(gamma), H_KINDS[h], _ptr(w, "f32", n, "w"), float(plan.lam),
-                               int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
-                               _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
-                               _stream(stream))
+    with _device_of(X, t, w, phi, grad, iters, stream=stream):
+        rc = lib().hopf_eval_dense(M, n, _ptr(X, "f32", M * n, "X"), _ptr(t, "f32", M, "t"), plan._h,
+                                   float(gamma), H_KINDS[h], _ptr(w, "f32", n, "w"), float(plan.lam),
+                                   int(max_iter), float(tol), _ptr(phi, "f32", M, "phi"),
+                                   _ptr(grad, "f32", M * n, "grad"), _ptr(iters, "i32", M, "iters"),
+                                   _stream(stream))
     _check(rc, "hopf_eval_dense")
     return phi, grad, iters
 
@@ -303,20 +347,27 @@ def eval_diag_host(X, t, D, c=None, gamma=0.0, h="l1", w=None, lam=1.0, max_iter
     """hopf_eval_diag_host: HOST (ideally pinned) X, t in and phi, grad, iters out; D/c/w on device.
     Copies are pipelined inside the library.  Returns host tensors (phi, grad, iters)."""
     import torch
+    if X.dim() != 2:
+        raise ValueError("X must be 2-D [M, n]")
     M, n = X.shape
-    if X.is_cuda or t.is_cuda:
-        raise ValueError("eval_diag_host takes host tensors")
     if out is None:
         out = (torch.empty(M, dtype=torch.float32, pin_memory=True),
                torch.empty((M, n), dtype=torch.float32, pin_memory=True),
                torch.empty(M, dtype=torch.int32, pin_memory=True))
     phi, grad, iters = out
-    for a, nm in ((X, "X"), (t, "t"), (phi, "phi"), (grad, "grad"), (iters, "iters")):
-        if not a.is_contiguous():
-            raise ValueError(f"{nm} must be contiguous")
-    rc = lib().hopf_eval_diag_host(M, n, X.data_ptr(), t.data_ptr(), _ptr(D, "f32", n, "D"),
-                                   _ptr(c, "f32", n, "c"), float(gamma), H_KINDS[h],
-                                   _ptr(w, "f32", n, "w"), float(lam), int(max_iter), float(tol),
-                                   phi.data_ptr(), grad.data_ptr(), iters.data_ptr())
+    _host(X, "f32", M * n, "X")
+    _host(t, "f32", M, "t")
+    _host(phi, "f32", M, "phi")
+    _host(grad, "f32", M * n, "grad")
+    _host(iters, "i32", M, "iters")
+    dev = D.device
+    for a in (c, w):
+        if a is not None and a.device != dev:
+            raise ValueError(f"D, c and w must live on one device, got {a.device} and {dev}")
+    with torch.cuda.device(dev):
+        rc = lib().hopf_eval_diag_host(M, n, X.data_ptr(), t.data_ptr(), _ptr(D, "f32", n, "D"),
+                                       _ptr(c, "f32", n, "c"), float(gamma), H_KINDS[h],
+                                       _ptr(w, "f32", n, "w"), float(lam), int(max_iter), float(tol),
+                                       phi.data_ptr(), grad.data_ptr(), iters.data_ptr())
     _check(rc, "hopf_eval_diag_host")
     return phi, grad, iters

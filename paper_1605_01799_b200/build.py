@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         return OUT
     BUILD.mkdir(exist_ok=True)
     extra = ["-Xptxas", "-v"] if ptxas_v else []
-    # experiments only (e.g. -DHOPF_TC3_TRACE for the dense kernel's per-round timestamps)
+    # experiments only (extra -D flags)
     extra += os.environ.get("HOPF_EXTRA_NVCC_FLAGS", "").split()
 
     def compile_one(src: Path):

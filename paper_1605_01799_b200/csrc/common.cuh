@@ -13,4 +13,10 @@ extern thread_local const char *g_last_kernel;
 int set_error(int code, const char *fmt, ...);
 int check_launch(const char *what);
 int num_sms();
+// Stream-ordered scratch (per call): allocated from a library-owned memory pool of the current
+// device (release threshold = unlimited, so after warm-up an allocation is a pool hit with no
+// host synchronisation) and freed on the same stream.  Calls on different streams therefore
+// never share scratch; the pool's event tracking orders reuse across streams.
+int scratch_alloc(void **ptr, size_t bytes, cudaStream_t stream);
+void scratch_free(void *ptr, cudaStream_t stream);
 }  // namespace hopf

@@ -32,16 +32,10 @@ struct DensePlanDev {
   float *Ml = nullptr;    // [n*n] fp32 M_lambda
   float *Ainv = nullptr;  // [n*n] fp32 A^{-1}
   float *A = nullptr;     // [n*n] fp32 A
-  // tensor-core operands (n == 256): fp16 hi/lo blocks of 2^s M_lambda in smem order
-  void *tc_blocks = nullptr;   // single-CTA kernel (dense_tc.cu)
-  float tc_scale_inv = 0.f;
-  void *tc2_rows = nullptr;    // CTA-pair kernel v3 (dense_tc2.cu)
-  float tc2_scale_inv = 0.f;
-  void *tc3_rows = nullptr;    // CTA-pair pipelined kernel v4 (dense_tc3.cu), the default
+  // tensor-core operands (n == 256): fp16 hi/lo rows of 2^s M_lambda in smem order for the
+  // CTA-pair kernel (dense_tc3.cu)
+  void *tc3_rows = nullptr;
   float tc3_scale_inv = 0.f;
-  // fix-up list workspace [count, idx...] (grown on demand)
-  int *fix = nullptr;
-  int64_t fix_cap = 0;
 };
 
 bool dense_supported_n(int n);
@@ -49,13 +43,7 @@ const char *dense_supported_list();
 int dense_plan_upload(int n, const double *Ml, const double *Ainv, const double *A,
                       DensePlanDev *out);
 void dense_plan_free(DensePlanDev *d);
-int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t stream);
-int dense_tc_prepare(int n, const double *Ml, void **blocks_dev, float *mscale_inv);
-int dense_tc_launch(const DenseParams &p, int hk, const void *blocks, float mscale_inv,
-                    int *fix_count, int *fix_list, cudaStream_t stream);
-int dense_tc2_prepare(int n, const double *Ml, void **rows_dev, float *mscale_inv);
-int dense_tc2_launch(const DenseParams &p, int hk, const void *rows, float mscale_inv,
-                     int *fix_count, int *fix_list, cudaStream_t stream);
+int dense_launch(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream_t stream);
 int dense_tc3_prepare(int n, const double *Ml, void **rows_dev, float *mscale_inv);
 int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscale_inv,
                      int *fix_count, int *fix_list, cudaStream_t stream);

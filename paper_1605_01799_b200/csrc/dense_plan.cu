@@ -95,9 +95,12 @@ extern "C" int hopf_eval_dense(int64_t M, int32_t n, const float *X, const float
   if (h == HOPF_H_WL1 && !w) return set_error(HOPF_EINVAL, "w is required for HOPF_H_WL1");
   if (M == 0) return HOPF_OK;
   if (!X || !t || !phi || !grad || !iters) return set_error(HOPF_EINVAL, "a required pointer is NULL");
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != plan->device)
+    return set_error(HOPF_EINVAL, "the plan lives on device %d, the current device is %d", plan->device, dev);
   DenseParams p{};
   p.M = M; p.n = n; p.X = X; p.t = t; p.w = w; p.gamma = gamma; p.lambda = lambda;
   p.max_iter = max_iter; p.tol = tol; p.phi = phi; p.grad = grad; p.iters = iters;
-  // the fix-up workspace is per-plan scratch (calls on one plan must share a stream)
-  return dense_launch(p, (int)h, const_cast<hopf_dense_plan *>(plan)->dev, (cudaStream_t)stream);
+  return dense_launch(p, (int)h, plan->dev, (cudaStream_t)stream);
 }

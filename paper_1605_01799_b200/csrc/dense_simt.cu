@@ -28,11 +28,7 @@ int dense_plan_upload(int n, const double *Ml, const double *Ainv, const double 
   for (size_t i = 0; i < nn; i++) a[i] = (float)Amat[i];
   out->n = n;
   if (n == 256) {   // tensor-core operands for the tcgen05 kernels
-    int rc = dense_tc_prepare(n, Ml, &out->tc_blocks, &out->tc_scale_inv);
-    if (rc != HOPF_OK) return rc;
-    rc = dense_tc2_prepare(n, Ml, &out->tc2_rows, &out->tc2_scale_inv);
-    if (rc != HOPF_OK) return rc;
-    rc = dense_tc3_prepare(n, Ml, &out->tc3_rows, &out->tc3_scale_inv);
+    int rc = dense_tc3_prepare(n, Ml, &out->tc3_rows, &out->tc3_scale_inv);
     if (rc != HOPF_OK) return rc;
   }
   if (cudaMalloc(&out->Ml, nn * 4) != cudaSuccess || cudaMalloc(&out->Ainv, nn * 4) != cudaSuccess ||
@@ -55,16 +51,9 @@ void dense_plan_free(DensePlanDev *d) {
   if (d->Ml) cudaFree(d->Ml);
   if (d->Ainv) cudaFree(d->Ainv);
   if (d->A) cudaFree(d->A);
-  if (d->tc_blocks) cudaFree(d->tc_blocks);
-  if (d->tc2_rows) cudaFree(d->tc2_rows);
-  d->tc2_rows = nullptr;
   if (d->tc3_rows) cudaFree(d->tc3_rows);
-  d->tc3_rows = nullptr;
-  if (d->fix) cudaFree(d->fix);
   d->Ml = d->Ainv = d->A = nullptr;
-  d->tc_blocks = nullptr;
-  d->fix = nullptr;
-  d->fix_cap = 0;
+  d->tc3_rows = nullptr;
 }
 
 namespace {
@@ -324,34 +313,24 @@ static int launch_simt(const DenseParams &p, int hk, const DensePlanDev &plan, c
 
 // n == 256 and H in {l1, wl1}: tcgen05 kernel, then the exact SIMT kernel on its fix-up list
 // (t == 0, invalid points, fp16 overflow, no convergence within max_iter).  Otherwise SIMT.
-int dense_launch(const DenseParams &p, int hk, DensePlanDev &plan, cudaStream_t stream) {
-  const bool use_tc = plan.tc_blocks && p.n == 256 && hk != HK_L2 && p.M <= 0x7fffffffLL - (1LL << 20);
+int dense_launch(const DenseParams &p, int hk, const DensePlanDev &plan, cudaStream_t stream) {
+  const bool use_tc = plan.tc3_rows && p.n == 256 && hk != HK_L2 && p.M <= 0x7fffffffLL - (1LL << 20);
   if (!use_tc) return launch_simt(p, hk, plan, stream);
-  if (plan.fix_cap < p.M + 1) {
-    if (plan.fix) cudaFree(plan.fix);
-    plan.fix = nullptr;
-    plan.fix_cap = 0;
-    if (cudaMalloc(&plan.fix, sizeof(int) * (size_t)(p.M + 1)) != cudaSuccess)
-      return set_error(HOPF_ECUDA, "cudaMalloc of the fix-up list failed");
-    plan.fix_cap = p.M + 1;
-  }
-  cudaMemsetAsync(plan.fix, 0, sizeof(int), stream);
-  // HOPF_DENSE_KERNEL=tc1 / tc2 select the earlier tensor-core kernels (comparison only)
-  static const char *sel = getenv("HOPF_DENSE_KERNEL");
-  int rc;
-  if (sel && strcmp(sel, "tc1") == 0)
-    rc = dense_tc_launch(p, hk, plan.tc_blocks, plan.tc_scale_inv, plan.fix, plan.fix + 1, stream);
-  else if (sel && strcmp(sel, "tc2") == 0)
-    rc = dense_tc2_launch(p, hk, plan.tc2_rows, plan.tc2_scale_inv, plan.fix, plan.fix + 1, stream);
-  else
-    rc = dense_tc3_launch(p, hk, plan.tc3_rows, plan.tc3_scale_inv, plan.fix, plan.fix + 1, stream);
+  // the fix-up list [count, idx...] is per call and stream-ordered (scratch_alloc), so calls on
+  // different streams never share it, whatever plan they use
+  int *fix = nullptr;
+  int rc = scratch_alloc((void **)&fix, sizeof(int) * (size_t)(p.M + 1), stream);
   if (rc != HOPF_OK) return rc;
-  DenseParams q = p;
-  q.idx = plan.fix + 1;
-  q.idx_count = plan.fix;
-  rc = launch_simt(q, hk, plan, stream);
-  g_last_kernel = (sel && strcmp(sel, "tc1") == 0) ? "hopf_dense_tc_kernel"
-                  : (sel && strcmp(sel, "tc2") == 0) ? "hopf_dense_tc2_kernel" : "hopf_dense_tc3_kernel";
+  cudaMemsetAsync(fix, 0, sizeof(int), stream);
+  rc = dense_tc3_launch(p, hk, plan.tc3_rows, plan.tc3_scale_inv, fix, fix + 1, stream);
+  if (rc == HOPF_OK) {
+    DenseParams q = p;
+    q.idx = fix + 1;
+    q.idx_count = fix;
+    rc = launch_simt(q, hk, plan, stream);
+  }
+  scratch_free(fix, stream);
+  g_last_kernel = "hopf_dense_tc3_kernel";
   return rc;
 }
 

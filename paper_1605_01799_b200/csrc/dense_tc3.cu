@@ -34,18 +34,12 @@
 //   pl = 32 (q & 1) + lane, coordinates c = 128 (q >> 1) + 32 j + [0, 32) ("2x2" layout of the
 //   M = 128 pair MMA, profiles/r01/tcgen05_2sm_probe.txt); stage s handles c0 + 8 s .. + 8.
 //   pi(c) = 64 s + 32 h + 8 j + i for c = 128 h + 32 j + 8 s + i.
-//
-// HOPF_TC3_TRACE (compile flag) + HOPF_TC3_TRACE=<file> (env) record per-round clock64 stamps of
-// CTAs 0/1 (epilogue warps, MMA thread) for the timeline analysis in DESIGN.md.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
-#include <cstdio>
-#include <cstdlib>
-#include <string>
 #include <vector>
 
 #include "../../include/hopf.h"
@@ -233,16 +227,6 @@ __device__ __forceinline__ void split2(float2 u, uint32_t &hw, uint32_t &lw) {
   lw = *reinterpret_cast<const uint32_t *>(&lo);
 }
 
-// optional per-round timestamps (HOPF_TC3_TRACE=<file>): CTAs 0/1, threads 0 and 160,
-// rounds [TR0, TR0 + 64), events: start, decided, mma ready, stage 0-3 arrived, partials, issue 0-3
-__device__ long long *g_tc3_trace = nullptr;
-__device__ long long *g_tc3_trace2 = nullptr;   // [2 CTAs][16 warps][64 rounds][4]: mma, st0, st3, red
-__device__ long long *g_tc3_trace3 = nullptr;   // MMA warp: [64 rounds][8]: stage s observed, issued
-#ifndef HOPF_TC3_TR0
-#define HOPF_TC3_TR0 200
-#endif
-constexpr int TR0 = HOPF_TC3_TR0;
-
 template <int HK, bool SCALED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     hopf_dense_tc3_kernel(const DenseParams p, const uint4 *__restrict__ mlam_rows,
@@ -292,9 +276,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp >= EPI_WARPS) {
     // ================= MMA warpgroup: warp 16 of the leader issues, the others idle =========
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(MMA_REGS));
-#ifdef HOPF_TC3_TRACE
-    long long *const tr3 = (blockIdx.x == 0 && lane == 0) ? g_tc3_trace3 : nullptr;
-#endif
     if (rank == 0 && warp == EPI_WARPS && lane == 0) {
       // one thread issues (an elect.sync form issued by the converged warp ran the round
       // skeleton 2.5-4x slower: tools/tcgen05_probe/probe_round.cu)
@@ -310,9 +291,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // remote arrives are default .release.cta; the tensor core reads the peer's shared
           // memory through the async proxy after the writers' fence.proxy.async)
           mbar_wait_hint(bar_stage0 + 8 * s, r & 1);
-#ifdef HOPF_TC3_TRACE
-          if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s] = clock64();
-#endif
           // the busy word is complete once stage 0 has arrived; its value is only needed
           // after the last stage, so the shared load stays off the MMA issue path
           if (s == 0) any_busy = busy[r & 1];
@@ -325,9 +303,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             mma2_f16(d_tmem, a_l0 + o, b_h0 + o, idesc, 1u);                 // Ul Mh
             mma2_f16(d_tmem, a_h0 + o, b_l0 + o, idesc, 1u);                 // Uh Ml
           }
-#ifdef HOPF_TC3_TRACE
-          if (tr3 && r >= TR0 && r < TR0 + 64) tr3[(r - TR0) * 8 + 2 * s + 1] = clock64();
-#endif
         }
         busy[r & 1] = 0;
         if (!any_busy) {
@@ -400,24 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
     };
 
-#ifdef HOPF_TC3_TRACE
-    long long *trace = nullptr;
-    if (g_tc3_trace && blockIdx.x < 2 && (tid == 0 || tid == 448))
-      trace = g_tc3_trace + (size_t)(blockIdx.x * 2 + (tid == 448)) * 64 * 16;
-    auto tmark = [&](uint32_t r, int e) {
-      if (trace && r >= TR0 && r < TR0 + 64) trace[(r - TR0) * 16 + e] = clock64();
-    };
-    long long *trace2 = nullptr;
-    if (g_tc3_trace2 && blockIdx.x < 2 && lane == 0) trace2 = g_tc3_trace2 + (size_t)(blockIdx.x * 16 + warp) * 64 * 4;
-    auto tmark2 = [&](uint32_t r, int e) {
-      if (trace2 && r >= TR0 && r < TR0 + 64) trace2[(r - TR0) * 4 + e] = clock64();
-    };
-#else
-    auto tmark = [](uint32_t, int) {};
-    auto tmark2 = [](uint32_t, int) {};
-#endif
     for (uint32_t r = 0;; r++) {
-      tmark(r, 0);
       // ---- every thread of a slot reads the 8 partial sums of round r-1 and decides ----------
       if (r == 0) {
         int q; float tq = 0.f;
@@ -426,7 +384,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       } else {
         if (lane == 0) mbar_wait_hint(bar_red + 8 * (q & 1), (r - 1) & 1);
         __syncwarp();
-        tmark(r, 12);
         float s4[4] = {0.f, 0.f, 0.f, 0.f};
         const float4 *rp = red + (size_t)((r - 1) & 1) * 8 * PTS + pl;
 #pragma unroll
@@ -456,8 +413,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           dmode = M_ACTIVE;
         }
       }
-      tmark(r, 13);
-      tmark(r, 1);
       const int pt = dpt;
       const int mode = dmode, it = dit;
       const float tt = dtt;
@@ -483,7 +438,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const bool wb = __any_sync(0xffffffffu, lane_busy);
         if (lane == 0 && wb) red_or_cluster(busy_addr + 4u * (r & 1), 1u);
       }
-      tmark(r, tid == 0 ? 15 : 14);
       const bool any_st = __any_sync(0xffffffffu, st), any_fin = __any_sync(0xffffffffu, fin);
       // START: tau_old = tau = 0 and v := x give u = x, d^0 = x, b^0 = 0 and U^1 = (1 + lambda) x;
       // k = 1: tau_old = 0 gives b^0 = 0, d^0 = u = x (R5), and v_prev = x from TMEM (R3)
@@ -492,11 +446,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // ---- wait for MMA r (v^k in D[r % 3]) or termination -----------------------------------
       if (r > 0) {
         if (lane == 0) mbar_wait_hint(bar_mma, (r - 1) & 1);
-        if (tid != 0) tmark(r, 15);
         __syncwarp();
         if (mbar_test(bar_term, 0)) break;
-        tmark(r, 2);
-        tmark2(r, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
       }
       const uint32_t tbuf = t_lane + 128u * (r % 3), tpbuf = t_lane + 128u * ((r + 2) % 3);
@@ -602,9 +553,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (rank == 0) mbar_arrive_local(bar_stage0 + 8 * s);
           else mbar_arrive_remote(stage_remote + 8 * s);
         }
-        tmark(r, 3 + s);
-        if (s == 0) tmark2(r, 1);
-        if (s == 3) tmark2(r, 2);
         if (s < 3 && r > 0) tmem_wait_ld3(va, vpa, xa);
       }
       // ---- partial sums of this round -> red[r & 1]; released through bar_red ---------------
@@ -614,8 +562,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_local(bar_red + 8 * (q & 1));
-      tmark(r, 7);
-      tmark2(r, 3);
       if (fin && nxt < (int)p.M) {   // the next point of a finished slot: x into us now (START next round)
         const float4 *xr = reinterpret_cast<const float4 *>(p.X + nxt * (int64_t)N_DIM + cb);
 #pragma unroll
@@ -680,64 +626,8 @@ int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscal
   const int64_t need = (p.M + 2 * tc3::PTS - 1) / (2 * tc3::PTS);
   if (pairs > need) pairs = need;
   if (pairs < 1) pairs = 1;
-#ifdef HOPF_TC3_TRACE
-  static const char *trace_path = getenv("HOPF_TC3_TRACE");
-#else
-  const char *trace_path = nullptr;
-#endif
-  long long *dtrace = nullptr, *dtrace2 = nullptr, *dtrace3 = nullptr;
-  if (trace_path) {
-    cudaMalloc(&dtrace, 4 * 64 * 16 * sizeof(long long));
-    cudaMemset(dtrace, 0, 4 * 64 * 16 * sizeof(long long));
-#ifdef HOPF_TC3_TRACE
-    cudaMemcpyToSymbol(tc3::g_tc3_trace, &dtrace, sizeof(dtrace));
-    cudaMalloc(&dtrace2, 2 * 16 * 64 * 4 * sizeof(long long));
-    cudaMemset(dtrace2, 0, 2 * 16 * 64 * 4 * sizeof(long long));
-    cudaMemcpyToSymbol(tc3::g_tc3_trace2, &dtrace2, sizeof(dtrace2));
-    cudaMalloc(&dtrace3, 64 * 8 * sizeof(long long));
-    cudaMemset(dtrace3, 0, 64 * 8 * sizeof(long long));
-    cudaMemcpyToSymbol(tc3::g_tc3_trace3, &dtrace3, sizeof(dtrace3));
-#endif
-  }
   fn<<<(unsigned)(2 * pairs), tc3::THREADS, tc3::SMEM_BYTES, stream>>>(
       p, reinterpret_cast<const uint4 *>(rows), mscale_inv, fix_count, fix_list);
-  if (trace_path) {
-    std::vector<long long> ht(4 * 64 * 16);
-    cudaMemcpy(ht.data(), dtrace, ht.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-    if (FILE *f = fopen(trace_path, "w")) {
-      for (size_t i = 0; i < ht.size(); i += 16) {
-        for (int e = 0; e < 16; e++) fprintf(f, "%lld ", ht[i + e]);
-        fprintf(f, "\n");
-      }
-      fclose(f);
-    }
-#ifdef HOPF_TC3_TRACE
-    long long *z = nullptr;
-    cudaMemcpyToSymbol(tc3::g_tc3_trace, &z, sizeof(z));
-    cudaMemcpyToSymbol(tc3::g_tc3_trace2, &z, sizeof(z));
-    std::vector<long long> h2(2 * 16 * 64 * 4);
-    cudaMemcpy(h2.data(), dtrace2, h2.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-    std::string p2 = std::string(trace_path) + ".warps";
-    if (FILE *f = fopen(p2.c_str(), "w")) {
-      for (size_t i = 0; i < h2.size(); i += 4) fprintf(f, "%lld %lld %lld %lld\n", h2[i], h2[i + 1], h2[i + 2], h2[i + 3]);
-      fclose(f);
-    }
-    cudaFree(dtrace2);
-    cudaMemcpyToSymbol(tc3::g_tc3_trace3, &z, sizeof(z));
-    std::vector<long long> h3(64 * 8);
-    cudaMemcpy(h3.data(), dtrace3, h3.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-    std::string p3 = std::string(trace_path) + ".mma";
-    if (FILE *f = fopen(p3.c_str(), "w")) {
-      for (size_t i = 0; i < h3.size(); i += 8) {
-        for (int e = 0; e < 8; e++) fprintf(f, "%lld ", h3[i + e]);
-        fprintf(f, "\n");
-      }
-      fclose(f);
-    }
-    cudaFree(dtrace3);
-#endif
-    cudaFree(dtrace);
-  }
   g_launches += 1;
   return check_launch("hopf_dense_tc3_kernel");
 }

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -40,16 +41,54 @@ int check_launch(const char *what) {
 }
 
 int num_sms() {
-  static int sms[64] = {0};
+  static std::atomic<int> sms[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  if (sms[dev] == 0) {
-    int v = 0;
+  int v = sms[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    sms[dev] = v > 0 ? v : 148;
+    if (v <= 0) v = 148;
+    sms[dev].store(v, std::memory_order_relaxed);
   }
-  return sms[dev];
+  return v;
+}
+
+int scratch_alloc(void **ptr, size_t bytes, cudaStream_t stream) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  *ptr = nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return set_error(HOPF_EINVAL, "device index %d", dev);
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaMemPool_t p = nullptr;
+      if (cudaMemPoolCreate(&p, &props) != cudaSuccess)
+        return set_error(HOPF_ECUDA, "cudaMemPoolCreate failed");
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev] = p;
+    }
+    pool = pools[dev];
+  }
+  if (bytes == 0) return HOPF_OK;
+  cudaError_t e = cudaMallocFromPoolAsync(ptr, bytes, pool, stream);
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return set_error(HOPF_ECUDA, "scratch allocation of %zu bytes: %s", bytes, cudaGetErrorString(e));
+  }
+  return HOPF_OK;
+}
+
+void scratch_free(void *ptr, cudaStream_t stream) {
+  if (ptr) cudaFreeAsync(ptr, stream);
 }
 
 // ---------------------------------------------------------------- diag / union variants
@@ -132,10 +171,14 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
   using namespace dtm;
   KernFn fn = h == HOPF_H_L2 ? hopf_diag_tm_kernel<HK_L2>
               : (h == HOPF_H_WL1 ? hopf_diag_tm_kernel<HK_WL1> : hopf_diag_tm_kernel<HK_L1>);
-  static bool attr_done[3] = {false, false, false};
-  if (!attr_done[(int)h]) {
+  // the attribute is per device: one flag bit per (device, H kind)
+  static std::atomic<uint32_t> attr_done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint32_t bit = 1u << (int)h;
+  if (dev < 0 || dev >= 64 || !(attr_done[dev].load(std::memory_order_relaxed) & bit)) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_SMEM);
-    attr_done[(int)h] = true;
+    if (dev >= 0 && dev < 64) attr_done[dev].fetch_or(bit, std::memory_order_relaxed);
   }
   int64_t blocks = (int64_t)num_sms() * 4;
   const int64_t need = (p.M + 3) / 4;   // 4 points (warps) per block
@@ -191,9 +234,13 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   struct Occ { int threads, per_sm; };
   // per-kernel cache (hopf_eval_maxh alternates kernels every launch: a one-entry cache re-ran
   // the attribute and occupancy queries on the host before each of them)
+  // (keyed by device too: the carveout attribute is set per device)
   static thread_local KernFn cache_fn[32] = {};
+  static thread_local int cache_dev[32] = {};
   static thread_local Occ cache_occ[32];
   static thread_local int cache_n = 0;
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
   // union: the kappa table of all K sets in dynamic shared memory ([K][NP*G + 1] float2)
   const size_t dyn = is_union ? (size_t)p.K * (size_t)(((v->CPL + 1) / 2) * v->G + 1) * 8 : 0;
   if (dyn > 48 * 1024 &&
@@ -201,7 +248,7 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
     return set_error(HOPF_EUNSUPPORTED, "union kappa table of %zu bytes does not fit", dyn);
   int ci = -1;
   for (int i = 0; i < cache_n && dyn == 0; i++)
-    if (cache_fn[i] == fn) { ci = i; break; }
+    if (cache_fn[i] == fn && cache_dev[i] == cur_dev) { ci = i; break; }
   Occ cached{128, 1};
   if (ci >= 0) cached = cache_occ[ci];
   if (ci < 0) {
@@ -218,7 +265,12 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
     }
     if (bestc.per_sm < 1) bestc = {128, 1};
     cached = bestc;
-    if (cache_n < 32 && dyn == 0) { cache_fn[cache_n] = fn; cache_occ[cache_n] = bestc; cache_n++; }
+    if (cache_n < 32 && dyn == 0) {
+      cache_fn[cache_n] = fn;
+      cache_dev[cache_n] = cur_dev;
+      cache_occ[cache_n] = bestc;
+      cache_n++;
+    }
   }
   const int threads = cached.threads;
   const int64_t groups_needed = p.M;
@@ -340,32 +392,18 @@ int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const f
   if (M == 0) return HOPF_OK;
   if (!X || !t || !Dj || !phi || !grad || !iters) return set_error(HOPF_EINVAL, "a required pointer is NULL");
   cudaStream_t st = (cudaStream_t)stream;
-  // scratch for phi_i, grad_i, iters_i (i >= 1), cached per device and grown on demand: a
-  // per-call cudaMallocAsync / cudaFreeAsync pair per buffer left host-side gaps between the
-  // dependent launches on a slow host
-  static std::mutex mu;
-  static char *scratch[64] = {};
-  static size_t scratch_bytes[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return set_error(HOPF_EINVAL, "device index %d", dev);
+  // scratch for phi_i, grad_i, iters_i (i >= 1): stream-ordered, per call (scratch_alloc), so
+  // calls on different streams never share it
   float *phs = nullptr, *gs = nullptr;
   int32_t *its = nullptr;
+  char *scratch = nullptr;
   if (K > 1) {
     const size_t a1 = ((size_t)M * 4 + 255) & ~(size_t)255, a2 = ((size_t)M * n * 4 + 255) & ~(size_t)255;
-    const size_t need = 2 * a1 + a2;
-    std::lock_guard<std::mutex> lock(mu);
-    if (scratch_bytes[dev] < need) {
-      cudaStreamSynchronize(st);
-      if (scratch[dev]) cudaFree(scratch[dev]);
-      scratch[dev] = nullptr;
-      scratch_bytes[dev] = 0;
-      if (cudaMalloc(&scratch[dev], need) != cudaSuccess) return set_error(HOPF_ECUDA, "scratch allocation failed");
-      scratch_bytes[dev] = need;
-    }
-    phs = (float *)scratch[dev];
-    its = (int32_t *)(scratch[dev] + a1);
-    gs = (float *)(scratch[dev] + 2 * a1);
+    int rc0 = scratch_alloc((void **)&scratch, 2 * a1 + a2, st);
+    if (rc0 != HOPF_OK) return rc0;
+    phs = (float *)scratch;
+    its = (int32_t *)(scratch + a1);
+    gs = (float *)(scratch + 2 * a1);
   }
   const int nb = num_sms() * 8;
   int rc = HOPF_OK;
@@ -384,6 +422,7 @@ int hopf_eval_maxh(int64_t M, int32_t n, const float *X, const float *t, const f
       hopf_maxh_combine_kernel<<<nb, 256, 0, st>>>(M, n, i, phs, gs, its, phi, grad, iters, istar);
     }
   }
+  scratch_free(scratch, st);
   if (rc != HOPF_OK) return rc;
   g_launches = 2 * K - (istar ? 0 : 1);   // K solves, K-1 combines (+ istar init)
   g_last_kernel = "hopf_diag kernels + hopf_maxh_combine_kernel";

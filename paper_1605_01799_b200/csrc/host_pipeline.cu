@@ -2,11 +2,13 @@
 // Points are processed in chunks; chunk c runs on internal stream c % kStreams as
 //   H2D(X_c, t_c) -> hopf_diag_kernel -> D2H(grad_c, phi_c, iters_c)
 // so the PCIe copies of neighbouring chunks overlap each other (full duplex) and the kernels.
-// Device buffers and streams are cached per device (grown on demand, never shrunk).
+// Streams and device buffers live in pooled per-device contexts (one per concurrent call, buffers
+// grown on demand, never shrunk).
 #include <cuda_runtime.h>
 
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "../../include/hopf.h"
 #include "common.cuh"
@@ -22,16 +24,42 @@ int env_int(const char *name, int dflt, int lo, int hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
 
-struct DevCache {
-  bool init = false;
+// One pipeline context = internal streams + device chunk buffers + the entry event.  Contexts
+// are pooled per device: a call takes a free one (or creates one) under a per-device mutex that
+// is held only for the pop / push, so concurrent calls (threads, devices) never share buffers
+// and never wait for each other's copies or kernels.
+struct Ctx {
   cudaStream_t s[kMaxStreams];
+  cudaEvent_t entry;
   char *buf = nullptr;
   size_t bytes = 0;
 };
-std::mutex g_mu;
-DevCache g_cache[64];
+struct DevPool {
+  std::mutex mu;
+  std::vector<Ctx *> free;
+};
+DevPool g_pool[64];
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+Ctx *ctx_take(int dev) {
+  {
+    std::lock_guard<std::mutex> lock(g_pool[dev].mu);
+    if (!g_pool[dev].free.empty()) {
+      Ctx *c = g_pool[dev].free.back();
+      g_pool[dev].free.pop_back();
+      return c;
+    }
+  }
+  Ctx *c = new Ctx();
+  for (int i = 0; i < kMaxStreams; i++) cudaStreamCreateWithFlags(&c->s[i], cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->entry, cudaEventDisableTiming);
+  return c;
+}
+void ctx_give(int dev, Ctx *c) {
+  std::lock_guard<std::mutex> lock(g_pool[dev].mu);
+  g_pool[dev].free.push_back(c);
+}
 }  // namespace
 }  // namespace hopf
 
@@ -58,20 +86,23 @@ extern "C" int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host,
   if (chunk > M) chunk = M;
   const size_t xb = align_up((size_t)chunk * n * 4), vb = align_up((size_t)chunk * 4);
   const size_t per = 2 * xb + 3 * vb;  // X, grad, t, phi, iters
-  std::lock_guard<std::mutex> lock(g_mu);
-  DevCache &dc = g_cache[dev];
-  if (!dc.init) {
-    for (int i = 0; i < kMaxStreams; i++) cudaStreamCreateWithFlags(&dc.s[i], cudaStreamNonBlocking);
-    dc.init = true;
-  }
+  Ctx *ctx = ctx_take(dev);
+  Ctx &dc = *ctx;
   if (dc.bytes < per * kStreams) {
     if (dc.buf) cudaFree(dc.buf);
     dc.buf = nullptr;
     dc.bytes = 0;
-    if (cudaMalloc(&dc.buf, per * kStreams) != cudaSuccess)
+    if (cudaMalloc(&dc.buf, per * kStreams) != cudaSuccess) {
+      ctx_give(dev, ctx);
       return set_error(HOPF_ECUDA, "cudaMalloc of %zu bytes failed", per * kStreams);
+    }
     dc.bytes = per * kStreams;
   }
+  // ordering contract: the chunks run after all work enqueued earlier on the legacy default
+  // stream of this device (which itself waits for every blocking stream), e.g. the caller's
+  // writes of Dj / c / w; work on the caller's non-blocking streams must be synchronised first
+  cudaEventRecord(dc.entry, cudaStreamLegacy);
+  for (int i = 0; i < kStreams; i++) cudaStreamWaitEvent(dc.s[i], dc.entry, 0);
   int32_t launches = 0;
   int rc = HOPF_OK;
   for (int64_t off = 0, ci = 0; off < M; off += chunk, ci++) {
@@ -97,6 +128,7 @@ extern "C" int hopf_eval_diag_host(int64_t M, int32_t n, const float *X_host,
     if (e != cudaSuccess && rc == HOPF_OK)
       rc = set_error(HOPF_ECUDA, "hopf_eval_diag_host: %s", cudaGetErrorString(e));
   }
+  ctx_give(dev, ctx);
   g_launches = launches;
   return rc;
 }

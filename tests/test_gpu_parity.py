@@ -387,6 +387,92 @@ def test_host_pipeline_matches_device(hb):
     assert torch.equal(ph, pd.cpu()) and torch.equal(gh, gd.cpu()) and torch.equal(ih, idv.cpu())
 
 
+def test_host_pipeline_orders_after_default_stream(hb):
+    """hopf_eval_diag_host runs after work enqueued earlier on the legacy default stream (an
+    event recorded there at entry): D written by a just-launched default-stream kernel is seen."""
+    import torch
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 4096)
+    Xh, th = torch.from_numpy(X).pin_memory(), torch.from_numpy(t).pin_memory()
+    Dd = torch.zeros(wl.n, device="cuda")
+    Dsrc = dev(wl.D)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(50_000_000)           # ~25 ms of default-stream work before the write
+    Dd.copy_(Dsrc)
+    ph, gh, ih = hb.eval_diag_host(Xh, th, Dd, None, wl.gamma, wl.h, dev(wl.w))
+    pd, gd, idv = run_diag(hb, wl, X, t)
+    torch.cuda.synchronize()
+    assert torch.equal(ph, pd.cpu()) and torch.equal(gh, gd.cpu())
+
+
+def test_concurrent_calls_two_threads_two_streams(hb):
+    """Two host threads, each on its own stream, issue diag, maxh and dense calls concurrently
+    (include/hopf.h concurrency convention: per-call stream-ordered scratch, per-plan read-only
+    data); every result must equal the serial run bit for bit."""
+    import threading
+    import torch
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 30000)
+    w4 = inputs.config("c4")
+    X4, t4 = inputs.points(w4, 0, 3000)
+    plan = hb.DensePlan(w4.Q, w4.Lam)
+    kinds, a = ["wl1", "l2", "l1"], np.array([1.0, 1.2, 0.8], np.float32)
+    W = dev(np.stack([wl.w, np.ones_like(wl.w), np.ones_like(wl.w)]))
+    args = [(dev(X[s::2]), dev(t[s::2])) for s in (0, 1)]
+    args4 = [(dev(X4[s::2]), dev(t4[s::2])) for s in (0, 1)]
+    Dd, wd = dev(wl.D), dev(wl.w)
+
+    def work(s, stream):
+        out = []
+        for _ in range(3):
+            out.append(hb.eval_diag(*args[s], Dd, None, wl.gamma, "wl1", wd, stream=stream))
+            out.append(hb.eval_maxh(*args[s], Dd, None, wl.gamma, kinds, a, W, stream=stream))
+            out.append(hb.eval_dense(*args4[s], plan, 0.0, "l1", stream=stream))
+        return out
+
+    serial = [work(s, torch.cuda.current_stream()) for s in (0, 1)]
+    torch.cuda.synchronize()
+    res, errs = [None, None], []
+
+    def thread_main(s):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                res[s] = work(s, st)
+            st.synchronize()
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append(e)
+
+    ths = [threading.Thread(target=thread_main, args=(s,)) for s in (0, 1)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    assert not errs, errs
+    for s in (0, 1):
+        for r, q in zip(res[s], serial[s]):
+            for u, v in zip(r, q):
+                assert torch.equal(u, v)
+
+
+def test_binding_rejects_foreign_and_malformed_tensors(hb):
+    """The binding validates host tensors of eval_diag_host (dtype, size) and device placement."""
+    import torch
+    wl = inputs.config("c2")
+    X, t = inputs.points(wl, 0, 64)
+    Xh, th = torch.from_numpy(X), torch.from_numpy(t)
+    D = dev(wl.D)
+    with pytest.raises(TypeError):
+        hb.eval_diag_host(Xh.double(), th, D, None, wl.gamma, "l1")
+    with pytest.raises(ValueError):
+        hb.eval_diag_host(Xh, th[:10], D, None, wl.gamma, "l1")
+    bad_out = (torch.empty(64), torch.empty(10), torch.empty(64, dtype=torch.int32))
+    with pytest.raises(ValueError):
+        hb.eval_diag_host(Xh, th, D, None, wl.gamma, "l1", out=bad_out)
+    with pytest.raises(ValueError):
+        hb.eval_diag(dev(X), th, D, None, wl.gamma, "l1")      # t on the host
+
+
 # ----------------------------------------------------------------- distance mode (NEXT-1)
 DIST_RTOL, PROJ_RTOL = 1e-4, 1e-3
 
