@@ -173,7 +173,7 @@ __host__ __device__ constexpr size_t smem_bytes() {
 }
 
 #ifndef HOPF_TMG_WAIT
-#define HOPF_TMG_WAIT 2   // finalize when this many quarters of the warp's groups wait
+#define HOPF_TMG_WAIT 3   // finalize when this many quarters of the warp's groups wait (C2: 1 -> 1.65 ms, 2 -> 1.54, 3 -> 1.50)
 #endif
 
 // bulk = the rows of X and grad are 16-byte aligned (n % 4 == 0, aligned bases): x of a group's
@@ -357,6 +357,24 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   };
   refill(have);
 
+  // A stopped group's result d^k goes to its grad row buffer at once (grad := d, R1; NaN for an
+  // invalid point): the group then keeps iterating harmlessly until the warp finalizes, so the
+  // trip needs no per-slot select to freeze d.  Collective; `stop` marks the stopping groups.
+  auto stash = [&](bool stop) {
+    if (bulk) {   // the group's previous grad row has left the buffer
+      if (stop && gl == 0) bulk_wait_read();
+      __syncwarp();
+    }
+    if (stop) {
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const float2 g = L2 ? make_float2(-d[q].x, -d[q].y) : d[q];
+        my_g[G * (2 * q)] = spec == 2 ? __int_as_float(0x7fc00000) : g.x;
+        my_g[G * (2 * q + 1)] = spec == 2 ? __int_as_float(0x7fc00000) : g.y;
+      }
+    }
+  };
+
   unsigned my_iters = 0;   // this lane's share of p.iter_total (group lane 0 counts)
   bool any_have = __any_sync(0xffffffffu, have);
   while (any_have) {
@@ -392,10 +410,10 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
               const float2 dd = fma2(sP, u, d[q]);                  // d_k - d_{k-1}
               const float2 nd = sub2(d[q], dd);                     // -d_k
               const float2 dmv = add2(nd, v);                       // v^k - d^k
-              d[q] = sel2(live, nd, d[q]);
+              d[q] = nd;
               a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0);
             } else {
-              d[q] = sel2(live, __fmul2_rn(nsP, u), d[q]);         // -d_k
+              d[q] = __fmul2_rn(nsP, u);                             // -d_k
             }
             const float2 bk = __fmul2_rn(omsP, u);                  // b_k
             const float2 na = __fmul2_rn(na_sP, u);                 // -(d_k - b_k)
@@ -413,7 +431,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
             b[q] = clamp2(u, tq);                                   // projection (Moreau)
             const float2 dn = sub2(u, b[q]);                        // (3.4b) shrink_1
             const float2 dd = sub2(dn, d[q]);                       // d^k - d^{k-1}
-            d[q] = sel2(live, dn, d[q]);                            // frozen while waiting
+            d[q] = dn;
             a0 = fma2(dd, dd, a0); c0 = fma2(dv, dv, c0);
           }
           ch[2][2 * e2] = vn.x;
@@ -447,6 +465,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
         wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -lim));
         if (spec == 0) my_iters += (unsigned)kdone;
       }
+      stash(stop);
     } else {
       it += live ? 1 : 0;
       kdone = it;
@@ -482,11 +501,13 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
         conv = need && sb <= tol;
       }
       const bool stop = cand && (spec != 0 || conv || kdone >= lim);
+      if (!__any_sync(0xffffffffu, stop)) continue;
       if (stop) {
         waiting = true;
         wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -lim));
         if (spec == 0) my_iters += (unsigned)kdone;
       }
+      stash(stop);
     }
     {
       const unsigned gbit = (gl == 0) ? 1u : 0u;
@@ -501,7 +522,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
     // t == 0: d := D^{-1}(x - c), the same expression gives J(x) (R6); invalid: NaN (R6)
     const bool done = waiting;
     const float gnan = __int_as_float(0x7fc00000);
-    if (__any_sync(0xffffffffu, done && spec == 1)) {   // rare: t == 0 points
+    if (__any_sync(0xffffffffu, done && spec == 1)) {   // rare: t == 0 points, grad = D^{-1}(x - c)
       for_chunks<CPL>([&](auto ci, auto szc) {
         constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
         float xh8[1][8];
@@ -511,20 +532,15 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
 #pragma unroll
           for (int e = 0; e < SZ; e++) {
             const float4 B = my_B[G * (8 * c + e)];
-            const float g = xh8[0][e] * B.x * B.w;   // D^{-1}(x - c)
-            float &dv = (e & 1) ? d[4 * c + (e >> 1)].y : d[4 * c + (e >> 1)].x;
-            dv = L2 ? -g : g;
+            my_g[G * (8 * c + e)] = xh8[0][e] * B.x * B.w;
           }
         }
       });
     }
-    if (bulk) {   // every group's previous grad row has left its buffer (all lanes write below)
-      if (gl == 0) bulk_wait_read();
-      __syncwarp();
-    }
+    // the grad rows (stashed at stop) are read back for phi; non-finalized lanes read their own
+    // (irrelevant) buffer contents
     float qs0 = 0.f, qs1 = 0.f, hs0 = 0.f, hs1 = 0.f;
     float *const grow = p.grad + pt * (int64_t)n + gl;
-    const bool nanout = spec == 2;
     for_chunks<CPL>([&](auto ci, auto szc) {
       constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
       float xh8[1][8];
@@ -534,8 +550,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       for (int e = 0; e < SZ; e++) {
         const int j = 8 * c + e;
         const float4 B = my_B[G * j];
-        const float2 dqq = d[4 * c + (e >> 1)];
-        const float dq = L2 ? -((e & 1) ? dqq.y : dqq.x) : ((e & 1) ? dqq.y : dqq.x);
+        const float dq = my_g[G * j];
         const float xt = xh8[0][e] * B.x;
         float &qs = (e & 1) ? qs1 : qs0;
         float &hs = (e & 1) ? hs1 : hs0;
@@ -544,9 +559,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
         if (L2) hs = fmaf(dq, dq, hs);
         else if (WL1) hs = fmaf(B.y, fabsf(dq), hs);
         else hs += fabsf(dq);
-        const float g = nanout ? gnan : dq;
-        if (bulk) my_g[G * j] = g;   // unconditional: only finalized groups' rows are sent
-        else if (done && j < jmax) grow[G * j] = g;
+        if (!bulk && done && j < jmax) grow[G * j] = dq;
       }
     });
     if (bulk) {
