@@ -371,10 +371,29 @@ def main():
         ms_small = timed(lambda: shard.gather_results([phi, iters]))
         ms_grad = timed(lambda: shard.gather_results([grad]))
         gbytes = grad.numel() * 4 * ws
-        gather = {"what": "all_gather of every rank's results (NCCL), outside the timed step",
+        gather = {"what": "all_gather_into_tensor of every rank's results (NCCL), outside the timed step",
                   "phi_iters_ms": ms_small, "grad_ms": ms_grad,
                   "grad_bytes_gathered": gbytes,
                   "grad_GBps_per_rank_in": gbytes * (ws - 1) / ws / (ms_grad / 1e3) / 1e9}
+        if wl.kind == "diag":
+            # the evaluation chunk by chunk with each chunk's phi, grad, iters all-gathered on NCCL's
+            # stream while the next chunk computes: end-to-end step with the gather
+            full = (torch.empty(M * ws, device=dev), torch.empty((M * ws, n), device=dev),
+                    torch.empty(M * ws, dtype=torch.int32, device=dev))
+            Dg, cg, wg = f32(wl.D), f32(wl.c), f32(wl.w)
+
+            def ev_chunk(lo, hi):
+                o = (phi[lo:hi], grad[lo:hi], iters[lo:hi])
+                hb.eval_diag(X[lo:hi], t[lo:hi], Dg, cg, wl.gamma, wl.h, wg, wl.lam, wl.max_iter,
+                             wl.tol, out=o, stream=stream)
+                return o
+            chunk = max(1, M // 8)
+            ms_pipe = timed(lambda: shard.eval_gather_pipelined(ev_chunk, M, chunk, full))
+            gather.update({"pipelined_step_ms": ms_pipe, "pipelined_chunks": -(-M // chunk),
+                           "compute_only_step_ms": ms_step,
+                           "pipelined_value": M * ws / (ms_pipe / 1e3),
+                           "pipelined_what": "eval + all_gather of phi, grad, iters per chunk, "
+                                             "gather of chunk i overlapped with compute of chunk i+1"})
 
     # ---- end to end through the host-buffer entry point (diag path) ----------------------------
     e2e = None
