@@ -356,6 +356,10 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
   int nn = 0;
   float s_lo = 0.f, s_hi = 0.f;
   const bool DIST = UNION && p.dist != nullptr;
+  // thread per point (G = 1, CPL a multiple of 4) with 16-byte aligned rows (n % 4 == 0 and aligned
+  // bases; warp-uniform): x loads and grad stores as float4 (padded slots hold zeros)
+  const bool VEC1 = (G == 1 && CPL % 4 == 0 && !UNION) && (n & 3) == 0 &&
+                    (((uintptr_t)p.X | (uintptr_t)p.grad) & 15) == 0;
 
   // ---- load the point (x, t) into registers; detect t == 0 / invalid (collective) -----------
   auto load_point = [&](bool active) {
@@ -365,6 +369,17 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
       bad = !(tt >= 0.f) || !finite_f(tt);
       const float *xrow = p.X + pt * (int64_t)n;
       float2 fin = splat2(0.f);   // x * 0 accumulates NaN iff some x is NaN or infinite
+      if (VEC1) {
+        // thread per point with 16-byte rows: the row as float4 loads (slots j = coordinates)
+#pragma unroll
+        for (int q4 = 0; q4 < NP / 2; q4++) {
+          const float4 x4 = (4 * q4 < jmax) ? __ldg(reinterpret_cast<const float4 *>(xrow) + q4)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+          fin = fma2(make_float2(x4.x, x4.y), splat2(0.f), fin);
+          fin = fma2(make_float2(x4.z, x4.w), splat2(0.f), fin);
+          if (!UNION) { xh[2 * q4] = make_float2(x4.x, x4.y); xh[2 * q4 + 1] = make_float2(x4.z, x4.w); }
+        }
+      } else {
 #pragma unroll
       for (int q = 0; q < NP; q++) {
         const int j0 = 2 * q, j1 = 2 * q + 1;
@@ -372,6 +387,7 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
         const float x1 = (j1 < CPL && j1 < jmax) ? __ldg(xrow + gl + G * j1) : 0.f;
         fin = fma2(make_float2(x0, x1), splat2(0.f), fin);
         if (!UNION) xh[q] = make_float2(x0, x1);   // union: re-read per set in setup_solve
+      }
       }
       bad |= !(fin.x == 0.f && fin.y == 0.f);
     }
@@ -905,10 +921,20 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
     } else if (done) {
       if (gl == 0) { p.phi[pt] = phiv; p.iters[pt] = wstatus; }
       float *grow = p.grad + pt * (int64_t)n;
+      if (VEC1) {   // the row as float4 stores
+        const float g = (spec == 2) ? __int_as_float(0x7fc00000) : 1.f;
+#pragma unroll
+        for (int q4 = 0; q4 < NP / 2; q4++)
+          if (4 * q4 < jmax)
+            reinterpret_cast<float4 *>(grow)[q4] =
+                (spec == 2) ? make_float4(g, g, g, g)
+                            : make_float4(d[2 * q4].x, d[2 * q4].y, d[2 * q4 + 1].x, d[2 * q4 + 1].y);
+      } else {
 #pragma unroll
       for (int j = 0; j < CPL; j++) {
         const int i = gl + G * j;
         if (j < jmax) grow[i] = (spec == 2) ? __int_as_float(0x7fc00000) : HOPF_SLOT(d, j);
+      }
       }
     }
     // ---- refill: the next set of the point (union) or the next point of this group ---------
