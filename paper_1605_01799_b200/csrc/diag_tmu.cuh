@@ -1,0 +1,393 @@
+// diag_tmu.cuh — K4g: the union of K diagonal initial data (phi = min_k phi_k) with
+// G lanes per point and tensor memory as an extension of the register file (H = l2; C5).
+// sm_100a, FP32 SIMT; no MMA.
+//
+// Paper: min over initial data P:628-667 (phi = min_k phi_k, the lowest k wins ties, R19); each
+// phi_k by split Bregman (3.4a)-(3.4c) P:832-844 on the centred problem at x - c_k (R5) with the
+// paper's stopping rule P:1595-1601, shrink_2 P:279-287, phi_k = (3.3) at d (R2); the closest
+// (Hopf-Lax terminal) point y = x - t grad/||grad||, y = c_k* when
+// grad = 0 (R18).  Same arithmetic as hopf_diag_kernel<G, CPL, HK_L2, true> (diag_kernel.cuh);
+// the storage and control flow are those of the grouped kernel (diag_tmg.cuh):
+//
+//   registers : d (as -d), b (the pending u) of the current set — 2 x CPL floats per lane
+//   TMEM      : x_hat_k (columns 0-31), v (32-63), -kappa_k (64-95) of the current set
+//   shared    : (D_k, c_k) of every set and gamma_k; per group two x rows (the current point and
+//               the prefetched next one, bulk copies), and two grad rows (the best set's grad and
+//               the candidate of the set that just stopped)
+//
+// A group's K set solves run one after another; a set that stops parks its d in the candidate
+// row and the group waits.  When enough groups of the warp wait, the warp runs one batched event:
+// phi_k of every parked set, the running minimum (the candidate row becomes the best row on an
+// improvement: a swap, no copy), the point's outputs for groups whose last set finished (phi,
+// iters, k*, the grad row and the y row by bulk stores, y formed in place in the x row), and the
+// next set's (or next point's) x_hat, v, kappa into TMEM.  x is read once per point from HBM.
+#pragma once
+#include <cfloat>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "diag_tmg.cuh"
+
+namespace hopf {
+namespace dtu {
+
+using dtg::THREADS;
+using dtg::TMEM_COLS;
+using dtg::DYN_SMEM;
+using dtg::C_XH;
+using dtg::C_V;
+using dtg::C_K;
+
+// shared-memory bytes for K sets: (D, c) tables, gamma, 4 rows per group, 2 mbarriers per group
+template <int G, int CPL>
+__host__ __device__ constexpr size_t smem_bytes(int K) {
+  return (size_t)K * G * CPL * 8 + (((size_t)K * 4 + 15) & ~(size_t)15) +
+         (size_t)4 * (THREADS / G) * dtg::row_pitch(G * CPL, G) * 4 + (size_t)(THREADS / G) * 16;
+}
+
+#ifndef HOPF_TMU_WAIT
+#define HOPF_TMU_WAIT 3   // run the event when this many quarters of the warp's groups wait
+#endif
+
+template <int G, int CPL>
+__global__ void __launch_bounds__(THREADS, 4) hopf_union_tmg_kernel(const DiagParams p) {
+  static_assert(G >= 2 && G <= 16 && (G & (G - 1)) == 0, "G in {2, 4, 8, 16}");
+  static_assert(CPL % 2 == 0 && CPL <= 32 && (CPL % 8 == 0 || CPL % 8 == 2 || CPL % 8 == 4),
+                "CPL = 8 a + {0, 2, 4}, at most 32");
+  constexpr int NP = CPL / 2;
+  constexpr int GPW = 32 / G, GPB = THREADS / G;
+  constexpr int PITCH = dtg::row_pitch(G * CPL, G);
+  constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMU_WAIT / 4) > 0 ? (GPW * HOPF_TMU_WAIT / 4) : 1;
+  using dtg::ldn;
+  using dtg::stn;
+  using dtg::wait_ld;
+  using dtg::for_chunks;
+  extern __shared__ __align__(16) uint8_t dyn_smem[];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = threadIdx.x / G;
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int n = p.n, K = p.K;
+  const int64_t M = p.M;
+  const float lam = p.lambda, tol = p.tol;
+  const int jmax = (n - gl + G - 1) / G;
+  // shared memory layout (see smem_bytes)
+  float2 *const DC_s = reinterpret_cast<float2 *>(dyn_smem);            // [K][G * CPL] (D, c)
+  float *const gk_s = reinterpret_cast<float *>(DC_s + K * G * CPL);    // [K]
+  float *const rows = reinterpret_cast<float *>(dyn_smem + (((size_t)K * G * CPL * 8 + (size_t)K * 4 + 15) & ~(size_t)15));
+  float *const xrow0 = rows + (size_t)(4 * grp) * PITCH;   // x rows 0, 1; grad rows 2, 3
+  uint64_t *const bars = reinterpret_cast<uint64_t *>(rows + (size_t)4 * GPB * PITCH) + 2 * grp;
+  const uint32_t row_bytes = (uint32_t)n * 4u;
+  for (int e = threadIdx.x; e < K * G * CPL; e += THREADS) {
+    const int k = e / (G * CPL), i = e % (G * CPL);
+    const bool real = i < n;
+    DC_s[e] = make_float2(real ? __ldg(p.D + (size_t)k * n + i) : 1.f,
+                          real ? __ldg(p.c + (size_t)k * n + i) : 0.f);
+  }
+  for (int k = threadIdx.x; k < K; k += THREADS) gk_s[k] = __ldg(p.gk + k);
+  if (gl == 0) {
+    dtg::mbar_init(dtg::smem_u32(bars), 1);
+    dtg::mbar_init(dtg::smem_u32(bars + 1), 1);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_slot)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tl0 = __shfl_sync(0xffffffffu, tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16), 0);
+  auto xrow = [&](int s) { return xrow0 + s * PITCH; };
+  auto grow_s = [&](int s) { return xrow0 + (2 + s) * PITCH; };
+
+  float2 d[NP], b[NP];   // -d, pending u (l2 storage of the trip)
+  int64_t pt = gid;
+  bool have = pt < M;
+  bool waiting = false;
+  int wstatus = 0, it = 0, lim = 0, spec = 0, kset = 0;
+  float tt = 0.f, tauS = 0.f, s_cur = 1.f;
+  bool sv_ok = false;
+  float tpre = have ? __ldg(p.t + pt) : 0.f;
+  uint32_t xph = 0;        // parity bits of the two x-row mbarriers
+  int xs = 0;              // x row of the current point
+  int cand = 0;            // grad row that receives the next stopped set's d (the other is the best)
+  float best = 0.f, bgn = 0.f;
+  int bestk = -1, bestit = 0;
+#pragma unroll
+  for (int q = 0; q < NP; q++) d[q] = b[q] = splat2(0.f);
+  if (gl == 0 && have) {
+    dtg::bulk_load(dtg::smem_u32(xrow(0)), p.X + pt * (int64_t)n, row_bytes, dtg::smem_u32(bars));
+    if (pt + ngroups < M)
+      dtg::bulk_load(dtg::smem_u32(xrow(1)), p.X + (pt + ngroups) * (int64_t)n, row_bytes, dtg::smem_u32(bars + 1));
+  }
+
+  // ---- set k of the current point for the groups with `fresh` (collective): x_hat = (x - c_k) /
+  // (D_k + lambda), v^0 = d^0 = x - c_k, b^0 = 0 (R5), -kappa_k = -lambda / (D_k + lambda)
+  auto set_setup = [&](bool fresh) {
+    const float *xr = xrow(xs) + gl;
+    const float2 *dc = DC_s + kset * (G * CPL) + gl;
+    for_chunks<CPL>([&](auto ci, auto szc) {
+      constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
+      float ch[3][8];
+      ldn<SZ, C_XH + 8 * c>(tl0, ch[0]);
+      ldn<SZ, C_V + 8 * c>(tl0, ch[1]);
+      ldn<SZ, C_K + 8 * c>(tl0, ch[2]);
+      wait_ld(ch);
+      if (fresh) {
+#pragma unroll
+        for (int e = 0; e < SZ; e++) {
+          const int j = 8 * c + e;
+          const float2 Dc = dc[G * j];
+          const float xt = (j < jmax) ? xr[G * j] - Dc.y : 0.f;
+          const float di = __fdividef(1.f, Dc.x + lam);
+          ch[0][e] = xt * di;
+          ch[1][e] = xt;
+          ch[2][e] = -__fdividef(lam, Dc.x + lam);
+          float2 &dq = d[4 * c + (e >> 1)];
+          float2 &bq = b[4 * c + (e >> 1)];
+          if (e & 1) { dq.y = -xt; bq.y = xt; } else { dq.x = -xt; bq.x = xt; }
+        }
+      }
+      stn<SZ, C_XH + 8 * c>(tl0, ch[0]);
+      stn<SZ, C_V + 8 * c>(tl0, ch[1]);
+      stn<SZ, C_K + 8 * c>(tl0, ch[2]);
+    });
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    if (fresh) {
+      lim = spec ? 0 : p.max_iter;
+      it = 0;
+      s_cur = 1.f;
+      sv_ok = false;
+      waiting = false;
+    }
+  };
+
+  // ---- start the point pt (x already requested into row xs): t, validity, running minimum ----
+  auto point_start = [&](bool fresh) {
+    bool bad = false;
+    if (fresh) {
+      tt = tpre;
+      bad = !(tt >= 0.f) || !finite_f(tt);
+      const int64_t nx = pt + ngroups;
+      tpre = nx < M ? __ldg(p.t + nx) : 0.f;
+      dtg::mbar_wait(dtg::smem_u32(bars + xs), (xph >> xs) & 1u);
+      xph ^= 1u << xs;
+      float fin = 0.f;   // x * 0 accumulates NaN iff some x is NaN or infinite
+      const float *xr = xrow(xs) + gl;
+#pragma unroll
+      for (int j = 0; j < CPL; j++)
+        if (j < jmax) fin = fmaf(xr[G * j], 0.f, fin);
+      bad |= !(fin == 0.f);
+      if (gl == 0) dtg::bulk_wait_read();   // this group's previous grad / y rows have left
+    }
+    __syncwarp();
+    bad = group_any<G>(bad);
+    if (fresh) {
+      spec = bad ? 2 : (tt == 0.f ? 1 : 0);
+      tauS = tt / lam;
+      kset = 0;
+      best = __int_as_float(0x7f800000);
+      bestk = -1;
+      bestit = 0;
+      bgn = 0.f;
+    }
+  };
+  point_start(have);
+  set_setup(have);
+
+  // a stopped set parks its d^k (grad := d, R1) in the candidate row; collective
+  auto park = [&](bool stop) {
+    if (stop) {
+      float *gr = grow_s(cand) + gl;
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        gr[G * (2 * q)] = -d[q].x;
+        gr[G * (2 * q + 1)] = -d[q].y;
+      }
+    }
+  };
+
+  unsigned my_iters = 0;
+  bool any_have = __any_sync(0xffffffffu, have);
+  while (any_have) {
+    const bool live = have && !waiting;
+    float2 a0 = splat2(0.f), b0 = a0, c0 = a0, r0 = a0;
+    const float2 sP = splat2(s_cur);
+    const float2 nsP = splat2(-s_cur), omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
+    const bool full_test = __any_sync(0xffffffffu, live && sv_ok);
+    auto trip = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      for_chunks<CPL>([&](auto ci, auto szc) {
+        constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
+        float ch[3][8];   // -kappa, x_hat, v
+        ldn<SZ, C_K + 8 * c>(tl0, ch[0]);
+        ldn<SZ, C_XH + 8 * c>(tl0, ch[1]);
+        ldn<SZ, C_V + 8 * c>(tl0, ch[2]);
+        wait_ld(ch);
+#pragma unroll
+        for (int e2 = 0; e2 < SZ / 2; e2++) {
+          const int q = 4 * c + e2;
+          const float2 kq = make_float2(ch[0][2 * e2], ch[0][2 * e2 + 1]);
+          const float2 xh = make_float2(ch[1][2 * e2], ch[1][2 * e2 + 1]);
+          const float2 v = make_float2(ch[2][2 * e2], ch[2][2 * e2 + 1]);
+          // d[q] = -d_{k-1}, b[q] = u_k; d_k = s_k u_k, b_k = (1 - s_k) u_k, d_k - b_k = (2 s_k - 1) u_k
+          const float2 u = b[q];
+          if (FULL) {
+            const float2 dd = fma2(sP, u, d[q]);                  // d_k - d_{k-1}
+            d[q] = sub2(d[q], dd);                                // -d_k
+            const float2 dmv = add2(d[q], v);                     // v^k - d^k
+            a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0);
+          } else {
+            d[q] = __fmul2_rn(nsP, u);                            // -d_k
+          }
+          const float2 bk = __fmul2_rn(omsP, u);                  // b_k
+          const float2 na = __fmul2_rn(na_sP, u);                 // -(d_k - b_k)
+          const float2 vn = fma2(kq, na, xh);                     // (3.4a): v_{k+1}
+          const float2 dv = sub2(vn, v);
+          b[q] = add2(vn, bk);                                    // u_{k+1} = v_{k+1} + b_k
+          c0 = fma2(dv, dv, c0);
+          r0 = fma2(b[q], b[q], r0);
+          ch[2][2 * e2] = vn.x;
+          ch[2][2 * e2 + 1] = vn.y;
+        }
+        stn<SZ, C_V + 8 * c>(tl0, ch[2]);
+      });
+    };
+    if (full_test) trip(std::true_type{});
+    else trip(std::false_type{});
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    {
+      const float psd = a0.x + a0.y, psb = b0.x + b0.y, psv = c0.x + c0.y, pr2 = r0.x + r0.y;
+      float r2;
+      bool ok_sd = false, ok_sb = false, ok_sv;
+      if (full_test) group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
+      else group_reduce2<G>(psv, pr2, tol, ok_sv, r2);
+      const int kdone = it;
+      const bool conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it
+      sv_ok = ok_sv;
+      s_cur = (r2 > tauS * tauS) ? fmaf(-tauS, rsqrtf(r2), 1.f) : 0.f;   // P:283-285, R20
+      it += live ? 1 : 0;
+      const bool stop = live && (spec != 0 || (kdone >= 1 && (conv || kdone >= lim)));
+      if (!__any_sync(0xffffffffu, stop)) continue;
+      if (stop) {
+        waiting = true;
+        wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -lim));
+        if (spec == 0) my_iters += (unsigned)kdone;
+      }
+      park(stop);
+    }
+    {
+      const unsigned gbit = (gl == 0) ? 1u : 0u;
+      const int nwait = __popc(__ballot_sync(0xffffffffu, waiting && gbit));
+      const int nhave = __popc(__ballot_sync(0xffffffffu, have && gbit));
+      if (nwait < WAIT_THRESHOLD && nwait < nhave) continue;
+    }
+
+    // ================= event: the parked sets of the waiting groups ===========================
+    const bool done = waiting;
+    const float gnan = __int_as_float(0x7fc00000);
+    const float *xr = xrow(xs) + gl;
+    const float2 *dc = DC_s + kset * (G * CPL) + gl;
+    float *const cr = grow_s(cand) + gl;
+    // t == 0 (R6): the set's grad is grad J_k(x) = D_k^{-1}(x - c_k)
+    if (done && spec == 1) {
+#pragma unroll
+      for (int j = 0; j < CPL; j++) {
+        const float2 Dc = dc[G * j];
+        cr[G * j] = (j < jmax) ? __fdividef(xr[G * j] - Dc.y, Dc.x) : 0.f;
+      }
+    }
+    // phi_k = <x - c_k, g> - 1/2 <g, D_k g> - t ||g|| + gamma_k ((3.3) at d, R2)
+    float qs0 = 0.f, qs1 = 0.f, hs0 = 0.f, hs1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < CPL; j++) {
+      const float2 Dc = dc[G * j];
+      const float g = cr[G * j];
+      const float xt = (j < jmax) ? xr[G * j] - Dc.y : 0.f;
+      float &qs = (j & 1) ? qs1 : qs0;
+      float &hs = (j & 1) ? hs1 : hs0;
+      qs = fmaf(xt, g, qs);
+      qs = fmaf(-0.5f * Dc.x * g, g, qs);
+      hs = fmaf(g, g, hs);
+    }
+    const float qs = group_sum<G>(qs0 + qs1), hs = group_sum<G>(hs0 + hs1);
+    const float gnorm = sqrtf(hs);
+    float phik = (spec == 1) ? qs + gk_s[kset] : qs - tt * gnorm + gk_s[kset];
+    bool point_done = false;
+    if (done) {
+      if (spec == 2) phik = gnan;
+      if (p.phik && gl == 0) p.phik[pt * K + kset] = phik;
+      if (phik < best) {   // strict: the lowest k wins ties (R19); NaN never wins
+        best = phik; bestk = kset; bestit = wstatus; bgn = gnorm;
+        cand ^= 1;         // the parked row becomes the best row
+      }
+      point_done = spec == 2 || kset + 1 >= K;
+    }
+    // ---- the point's outputs (groups whose last set finished) ---------------------------------
+    if (__any_sync(0xffffffffu, point_done)) {
+      float *const br = grow_s(cand ^ 1) + gl;   // best grad row
+      float *const yr = xrow(xs) + gl;           // y formed in place in the x row
+      const bool nanpt = spec == 2 || bestk < 0;
+      if (point_done) {
+        const float ign = bgn > 0.f ? __fdividef(1.f, bgn) : 0.f;
+        const float2 *dck = DC_s + (bestk < 0 ? 0 : bestk) * (G * CPL) + gl;
+#pragma unroll
+        for (int j = 0; j < CPL; j++) {
+          const float g = br[G * j];
+          // y = x - t grad / ||grad||, c_k* if grad = 0 (R18)
+          const float y = bgn > 0.f ? yr[G * j] - tt * (g * ign) : dck[G * j].y;
+          br[G * j] = nanpt ? gnan : g;
+          yr[G * j] = nanpt ? gnan : y;
+        }
+        if (gl == 0) {
+          p.phi[pt] = nanpt ? gnan : best;
+          p.iters[pt] = nanpt ? INT32_MIN : bestit;
+          if (p.kstar) p.kstar[pt] = nanpt ? -1 : bestk;
+        }
+      }
+      dtg::fence_proxy_async();
+      __syncwarp();
+      if (point_done && gl == 0) {
+        dtg::bulk_store(p.grad + pt * (int64_t)n, dtg::smem_u32(br - gl), row_bytes);
+        if (p.Y) dtg::bulk_store(p.Y + pt * (int64_t)n, dtg::smem_u32(yr - gl), row_bytes);
+        // the x row is free once y has left it: the point after the next one goes there
+        const int64_t nn2 = pt + 2 * ngroups;
+        if (nn2 < M) {
+          dtg::bulk_wait_read();
+          dtg::bulk_load(dtg::smem_u32(yr - gl), p.X + nn2 * (int64_t)n, row_bytes, dtg::smem_u32(bars + xs));
+        }
+      }
+    }
+    // ---- next set, or next point --------------------------------------------------------------
+    const bool next_set = done && !point_done;
+    if (next_set) kset++;
+    if (point_done) {
+      pt += ngroups;
+      have = pt < M;
+      xs ^= 1;
+      if (!have) {
+        waiting = false;
+        spec = 0;
+#pragma unroll
+        for (int q = 0; q < NP; q++) d[q] = b[q] = splat2(0.f);
+      }
+    }
+    const bool started = point_done && have;
+    if (__any_sync(0xffffffffu, started)) point_start(started);
+    if (__any_sync(0xffffffffu, next_set || started)) set_setup(next_set || started);
+    any_have = __any_sync(0xffffffffu, have);
+  }
+  if (gl == 0) dtg::bulk_wait_all();
+  if (p.iter_total && gl == 0 && my_iters) atomicAdd(p.iter_total, (unsigned long long)my_iters);
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem_slot), "r"(TMEM_COLS));
+}
+
+}  // namespace dtu
+}  // namespace hopf

@@ -16,6 +16,7 @@
 #include "diag_kernel.cuh"
 #include "diag_tm.cuh"
 #include "diag_tmg.cuh"
+#include "diag_tmu.cuh"
 
 namespace hopf {
 
@@ -245,6 +246,49 @@ static int launch_diag_tmg(const DiagParams &p, hopf_h_kind h, const TmgVariant 
   return check_launch("hopf_diag_tmg_kernel");
 }
 
+// Union with H = l2 (diag_tmu.cuh): G lanes per point, TMEM, x read once per point by bulk copies,
+// the best set's grad kept in shared memory.  Used when the rows are 16-byte aligned and the
+// per-set tables fit the block's shared memory; HOPF_UNION_TMG=0 selects the register kernel.
+using TmuFn = void (*)(const DiagParams);
+struct TmuVariant {
+  int G, CPL;
+  TmuFn fn;
+  size_t (*smem)(int K);
+};
+#define HOPF_TMU(G_, C_) {G_, C_, dtu::hopf_union_tmg_kernel<G_, C_>, dtu::smem_bytes<G_, C_>}
+static const TmuVariant kTmuVariants[] = {HOPF_TMU(4, 16)};
+
+static const TmuVariant *pick_tmu(const DiagParams &p) {
+  static const char *env = getenv("HOPF_UNION_TMG");
+  if (env && strcmp(env, "0") == 0) return nullptr;
+  if (p.n % 4 != 0 || (((uintptr_t)p.X | (uintptr_t)p.grad | (uintptr_t)p.Y) & 15) != 0) return nullptr;
+  for (const TmuVariant &v : kTmuVariants)
+    if (v.G * v.CPL >= p.n && v.G * (v.CPL - 2) < p.n && v.smem(p.K) <= (size_t)dtu::DYN_SMEM) return &v;
+  return nullptr;
+}
+
+static int launch_union_tmg(const DiagParams &p, const TmuVariant *v, cudaStream_t stream) {
+  static std::atomic<uint64_t> attr_done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (int)(v - kTmuVariants);
+  if (dev < 0 || dev >= 64 || !(attr_done[dev].load(std::memory_order_relaxed) & bit)) {
+    cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dtu::DYN_SMEM);
+    if (dev >= 0 && dev < 64) attr_done[dev].fetch_or(bit, std::memory_order_relaxed);
+  }
+  const int per_block = dtu::THREADS / v->G;
+  int64_t blocks = (int64_t)num_sms() * 4;
+  const int64_t need = (p.M + per_block - 1) / per_block;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  v->fn<<<(unsigned)blocks, dtu::THREADS, dtu::DYN_SMEM, stream>>>(p);
+  g_launches += 1;
+  g_last_threads = dtu::THREADS;
+  g_last_blocks = (int)blocks;
+  g_last_kernel = "hopf_union_tmg_kernel<l2>";
+  return check_launch("hopf_union_tmg_kernel");
+}
+
 // ---------------------------------------------------------------- NEXT-4 helpers
 // istar = 0 where the first solve is valid, -1 on invalid points
 __global__ void hopf_istar_init_kernel(int64_t M, const int32_t *iters, int32_t *istar) {
@@ -281,6 +325,8 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
     return launch_diag_tm(p, h, stream);
   if (!ell && !is_union)
     if (const TmgVariant *tv = pick_tmg(p.n)) return launch_diag_tmg(p, h, tv, stream);
+  if (is_union && h == HOPF_H_L2 && p.dist == nullptr)
+    if (const TmuVariant *uv = pick_tmu(p)) return launch_union_tmg(p, uv, stream);
   KernFn fn = ell ? v->fn[0][0] : v->fn[(int)h][is_union ? 1 : 0];
   // Block size: the one that keeps the most warps resident per SM (register-limited kernels
   // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
