@@ -259,19 +259,38 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_union_tmg_kernel(const DiagPa
     };
     if (full_test) trip(std::true_type{});
     else trip(std::false_type{});
-    asm volatile("tcgen05.wait::st.sync.aligned;");
     {
-      const float psd = a0.x + a0.y, psb = b0.x + b0.y, psv = c0.x + c0.y, pr2 = r0.x + r0.y;
-      float r2;
-      bool ok_sd = false, ok_sb = false, ok_sv;
-      if (full_test) group_reduce4<G>(psd, psb, psv, pr2, tol, r2, ok_sd, ok_sb, ok_sv);
-      else group_reduce2<G>(psv, pr2, tol, ok_sv, r2);
+      // group totals by a plain xor butterfly (every lane ends with every total: no broadcast, the
+      // dependent chain is log2(G) shuffles deep); the stores of v drain meanwhile
+      float sd = 0.f, sb = 0.f, sv, r2;
+      if (full_test) {
+        float4 t4 = make_float4(a0.x + a0.y, b0.x + b0.y, c0.x + c0.y, r0.x + r0.y);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          t4.x += __shfl_xor_sync(0xffffffffu, t4.x, o);
+          t4.y += __shfl_xor_sync(0xffffffffu, t4.y, o);
+          t4.z += __shfl_xor_sync(0xffffffffu, t4.z, o);
+          t4.w += __shfl_xor_sync(0xffffffffu, t4.w, o);
+        }
+        sd = t4.x; sb = t4.y; sv = t4.z; r2 = t4.w;
+      } else {
+        float2 t2 = make_float2(c0.x + c0.y, r0.x + r0.y);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+          t2.x += __shfl_xor_sync(0xffffffffu, t2.x, o);
+          t2.y += __shfl_xor_sync(0xffffffffu, t2.y, o);
+        }
+        sv = t2.x; r2 = t2.y;
+      }
       const int kdone = it;
-      const bool conv = (it >= 1) && sv_ok && ok_sd && ok_sb;   // P:1597-1601 for iteration k = it
-      sv_ok = ok_sv;
+      // P:1597-1601 for iteration k = it (sd, sb are only formed in FULL trips, where sv_ok may hold)
+      const bool conv = full_test && sv_ok && sd <= tol && sb <= tol;
+      sv_ok = sv <= tol;
       s_cur = (r2 > tauS * tauS) ? fmaf(-tauS, rsqrtf(r2), 1.f) : 0.f;   // P:283-285, R20
       it += live ? 1 : 0;
-      const bool stop = live && (spec != 0 || (kdone >= 1 && (conv || kdone >= lim)));
+      // t == 0 / invalid points have lim = 0 and stop at their first trip
+      const bool stop = live && ((kdone >= 1 && conv) || kdone >= lim);
+      asm volatile("tcgen05.wait::st.sync.aligned;");
       if (!__any_sync(0xffffffffu, stop)) continue;
       if (stop) {
         waiting = true;
