@@ -45,9 +45,9 @@ __host__ __device__ constexpr size_t smem_bytes(int K) {
          (size_t)4 * (THREADS / G) * dtg::row_pitch(G * CPL, G) * 4 + (size_t)(THREADS / G) * 16;
 }
 
-#ifndef HOPF_TMU_WAIT
-#define HOPF_TMU_WAIT 3   // run the event when this many quarters of the warp's groups wait
-#endif
+#ifndef HOPF_TMU_WAIT8
+#define HOPF_TMU_WAIT8 4  // run the event when this many eighths of the warp's groups wait
+#endif                    // (C5, 8 groups: 2 -> 11.75 ms, 4 -> 11.04, 6 -> 12.53)
 
 template <int G, int CPL>
 __global__ void __launch_bounds__(THREADS, 4) hopf_union_tmg_kernel(const DiagParams p) {
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_union_tmg_kernel(const DiagPa
   constexpr int NP = CPL / 2;
   constexpr int GPW = 32 / G, GPB = THREADS / G;
   constexpr int PITCH = dtg::row_pitch(G * CPL, G);
-  constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMU_WAIT / 4) > 0 ? (GPW * HOPF_TMU_WAIT / 4) : 1;
+  constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMU_WAIT8 / 8) > 0 ? (GPW * HOPF_TMU_WAIT8 / 8) : 1;
   using dtg::ldn;
   using dtg::stn;
   using dtg::wait_ld;
