@@ -172,9 +172,9 @@ __host__ __device__ constexpr size_t smem_bytes() {
          (size_t)(THREADS / G) * 8;
 }
 
-#ifndef HOPF_TMG_WAIT
-#define HOPF_TMG_WAIT 3   // finalize when this many quarters of the warp's groups wait (C2: 1 -> 1.65 ms, 2 -> 1.54, 3 -> 1.50)
-#endif
+#ifndef HOPF_TMG_WAIT8
+#define HOPF_TMG_WAIT8 6  // finalize when this many eighths of the warp's groups wait
+#endif                    // (C2, 8 groups: 2 -> 1.65 ms, 4 -> 1.54, 6 -> 1.50)
 
 // bulk = the rows of X and grad are 16-byte aligned (n % 4 == 0, aligned bases): x of a group's
 // next point is prefetched into shared memory by a bulk copy one point ahead, and grad leaves
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   constexpr int NP = CPL / 2;
   constexpr int GPW = 32 / G, GPB = THREADS / G;
   constexpr int PITCH = row_pitch(G * CPL, G);
-  constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMG_WAIT / 4) > 0 ? (GPW * HOPF_TMG_WAIT / 4) : 1;
+  constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMG_WAIT8 / 8) > 0 ? (GPW * HOPF_TMG_WAIT8 / 8) : 1;
   constexpr bool L2 = HK == HK_L2, WL1 = HK == HK_WL1;
   extern __shared__ __align__(16) uint8_t dyn_smem[];
   __shared__ uint32_t tmem_slot;

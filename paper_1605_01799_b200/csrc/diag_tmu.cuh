@@ -32,11 +32,18 @@ namespace hopf {
 namespace dtu {
 
 using dtg::THREADS;
-using dtg::TMEM_COLS;
-using dtg::DYN_SMEM;
-using dtg::C_XH;
-using dtg::C_V;
-using dtg::C_K;
+// TMEM: three regions of 16 columns (x_hat, v, -kappa) fit a 64-column allocation for CPL <= 16,
+// so up to 8 blocks fit the SM's 512 columns; registers and shared memory then set residency
+template <int CPL> struct Cols {
+  static constexpr int R = CPL <= 16 ? 16 : 32;          // region width
+  static constexpr int XH = 0, V = R, K = 2 * R;
+  static constexpr int ALLOC = 3 * R <= 64 ? 64 : 128;   // power of two >= 32
+};
+#ifndef HOPF_TMU_BLOCKS
+#define HOPF_TMU_BLOCKS 4   // resident blocks per SM (C5: 4 -> 11.04 ms at 127 registers, 5 -> 12.07 at 96, 6 -> 15.6)
+#endif
+constexpr int BLOCKS_PER_SM = HOPF_TMU_BLOCKS;
+constexpr int DYN_SMEM = (226 * 1024) / BLOCKS_PER_SM - 1024;
 
 // shared-memory bytes for K sets: (D, c) tables, gamma, 4 rows per group, 2 mbarriers per group
 template <int G, int CPL>
@@ -50,7 +57,8 @@ __host__ __device__ constexpr size_t smem_bytes(int K) {
 #endif                    // (C5, 8 groups: 2 -> 11.75 ms, 4 -> 11.04, 6 -> 12.53)
 
 template <int G, int CPL>
-__global__ void __launch_bounds__(THREADS, 4) hopf_union_tmg_kernel(const DiagParams p) {
+__global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(const DiagParams p) {
+  constexpr int C_XH = Cols<CPL>::XH, C_V = Cols<CPL>::V, C_K = Cols<CPL>::K, TMEM_COLS = Cols<CPL>::ALLOC;
   static_assert(G >= 2 && G <= 16 && (G & (G - 1)) == 0, "G in {2, 4, 8, 16}");
   static_assert(CPL % 2 == 0 && CPL <= 32 && (CPL % 8 == 0 || CPL % 8 == 2 || CPL % 8 == 4),
                 "CPL = 8 a + {0, 2, 4}, at most 32");

@@ -277,7 +277,7 @@ static int launch_union_tmg(const DiagParams &p, const TmuVariant *v, cudaStream
     if (dev >= 0 && dev < 64) attr_done[dev].fetch_or(bit, std::memory_order_relaxed);
   }
   const int per_block = dtu::THREADS / v->G;
-  int64_t blocks = (int64_t)num_sms() * 4;
+  int64_t blocks = (int64_t)num_sms() * dtu::BLOCKS_PER_SM;
   const int64_t need = (p.M + per_block - 1) / per_block;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
