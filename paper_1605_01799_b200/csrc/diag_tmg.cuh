@@ -173,8 +173,8 @@ __host__ __device__ constexpr size_t smem_bytes() {
 }
 
 #ifndef HOPF_TMG_WAIT8
-#define HOPF_TMG_WAIT8 6  // finalize when this many eighths of the warp's groups wait
-#endif                    // (C2, 8 groups: 2 -> 1.65 ms, 4 -> 1.54, 6 -> 1.50)
+#define HOPF_TMG_WAIT8 8  // finalize when this many eighths of the warp's groups wait
+#endif                    // (C2, 8 groups: 2 -> 1.65 ms, 4 -> 1.54, 5 -> 1.66, 6 -> 1.50, 7 -> 1.38, 8 -> 1.26)
 
 // bulk = the rows of X and grad are 16-byte aligned (n % 4 == 0, aligned bases): x of a group's
 // next point is prefetched into shared memory by a bulk copy one point ahead, and grad leaves

@@ -53,8 +53,8 @@ __host__ __device__ constexpr size_t smem_bytes(int K) {
 }
 
 #ifndef HOPF_TMU_WAIT8
-#define HOPF_TMU_WAIT8 4  // run the event when this many eighths of the warp's groups wait
-#endif                    // (C5, 8 groups: 2 -> 11.75 ms, 4 -> 11.04, 6 -> 12.53)
+#define HOPF_TMU_WAIT8 8  // run the event when this many eighths of the warp's groups wait
+#endif                    // (C5, 8 groups: 2 -> 11.75 ms, 3 -> 12.38, 4 -> 11.04, 5 -> 13.98, 6 -> 12.53, 7 -> 11.39, 8 -> 9.79)
 
 template <int G, int CPL>
 __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(const DiagParams p) {
