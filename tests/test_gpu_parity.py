@@ -549,6 +549,16 @@ def test_iteration_counter_matches_iters(hb):
     assert int(cnt.item()) == int(np.abs(itn[itn != oracle.INVALID]).sum())
     wu = inputs.config("c5")
     Xu, tu = inputs.points(wu, 0, 300)
+    # K = 1: the counter equals the returned (winning = only) set's iteration counts exactly
+    cnt.zero_()
+    hb.set_iteration_counter(cnt)
+    _, _, it1, _, _, _ = hb.eval_union(dev(Xu), dev(tu), dev(wu.Dk[:1]), dev(wu.Ck[:1]), dev(wu.gammak[:1]), "l2")
+    torch.cuda.synchronize()
+    hb.set_iteration_counter(None)
+    i1 = it1.cpu().numpy()
+    assert int(cnt.item()) == int(np.abs(i1[i1 != oracle.INVALID]).sum())
+    # K = 16: every set solve counts; reference = 16 single-set evaluations.  They may run another
+    # kernel (other reduction order), so a set's count can differ by one at the threshold
     cnt.zero_()
     hb.set_iteration_counter(cnt)
     hb.eval_union(dev(Xu), dev(tu), dev(wu.Dk), dev(wu.Ck), dev(wu.gammak), "l2")
@@ -559,7 +569,7 @@ def test_iteration_counter_matches_iters(hb):
         _, _, itk = hb.eval_diag(dev(Xu), dev(tu), dev(wu.Dk[k]), dev(wu.Ck[k]), float(wu.gammak[k]), "l2")
         ik = itk.cpu().numpy()
         total += int(np.abs(ik[ik != oracle.INVALID]).sum())
-    assert int(cnt.item()) == total
+    assert abs(int(cnt.item()) - total) <= 0.002 * total
 
 
 # ----------------------------------------------------------------- max over min of H (NEXT-4)
