@@ -225,6 +225,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--M", type=int, default=None, help="points per GPU (default: the config's)")
+    ap.add_argument("--n", type=int, default=None, help="dimension override (experiments; default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -232,7 +233,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
-    wl = inputs.config(args.config, M=args.M)
+    wl = inputs.config(args.config, M=args.M, n=args.n)
     if args.impl == "reference":
         return run_reference(args, wl)
 
@@ -250,7 +251,7 @@ def main():
     # ---- inputs: this rank's shard of the global points (generated by global index) ----------
     M = wl.M
     r0, r1 = shard.weak_range(M, rank)
-    wl_g = inputs.config(args.config, M=M * ws)
+    wl_g = inputs.config(args.config, M=M * ws, n=args.n)
     Xh, th = inputs.points(wl_g, r0, r1)
     X = torch.from_numpy(Xh).to(dev)
     t = torch.from_numpy(th).to(dev)

@@ -42,7 +42,7 @@ namespace hopf {
 namespace dtg {
 
 constexpr int THREADS = 128, TMEM_COLS = 128;
-constexpr int DYN_SMEM = 48 * 1024;   // caps residency at 4 CTAs per SM (4 x 128 TMEM columns)
+constexpr int DYN_SMEM = 55 * 1024;   // caps residency at 4 CTAs per SM (4 x 128 TMEM columns)
 constexpr int C_XH = 0, C_V = 32, C_K = 64, C_TAU = 96;
 
 // tcgen05.ld / st of N in {2, 4, 8} consecutive columns of this thread's lane, column offset OFF

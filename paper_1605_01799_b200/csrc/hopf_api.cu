@@ -15,8 +15,7 @@
 #include "common.cuh"
 #include "diag_kernel.cuh"
 #include "diag_tm.cuh"
-#include "diag_tmg.cuh"
-#include "diag_tmu.cuh"
+#include "tmg_api.h"
 
 namespace hopf {
 
@@ -195,100 +194,6 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
   return check_launch("hopf_diag_tm_kernel");
 }
 
-// Grouped TMEM kernel (diag_tmg.cuh): G lanes per point, several points per warp, non-union
-// l1 / wl1 / l2.  Ordered by padded width G * CPL; the first with G * CPL >= n is used.
-// HOPF_DIAG_TMG=0 selects the register kernel (A/B experiments).
-using TmgFn = void (*)(const DiagParams);
-struct TmgVariant {
-  int G, CPL;
-  TmgFn fn[2][3];   // [bulk][h]
-};
-#define HOPF_TMG1(G_, C_, B_)                                                                \
-  {dtg::hopf_diag_tmg_kernel<G_, C_, HK_L1, B_>, dtg::hopf_diag_tmg_kernel<G_, C_, HK_WL1, B_>, \
-   dtg::hopf_diag_tmg_kernel<G_, C_, HK_L2, B_>}
-#define HOPF_TMG(G_, C_) {G_, C_, {HOPF_TMG1(G_, C_, false), HOPF_TMG1(G_, C_, true)}}
-static const TmgVariant kTmgVariants[] = {HOPF_TMG(4, 26)};
-
-static const TmgVariant *pick_tmg(int n) {
-  static const char *env = getenv("HOPF_DIAG_TMG");
-  if (env && strcmp(env, "0") == 0) return nullptr;
-  for (const TmgVariant &v : kTmgVariants)
-    if (v.G * v.CPL >= n && v.G * (v.CPL - 2) < n) return &v;   // padding below one slot pair
-  return nullptr;
-}
-
-static int launch_diag_tmg(const DiagParams &p, hopf_h_kind h, const TmgVariant *v,
-                           cudaStream_t stream) {
-  // rows move by bulk copies when they are 16-byte aligned (HOPF_TMG_BULK=0 disables)
-  static const char *benv = getenv("HOPF_TMG_BULK");
-  const bool bulk = !(benv && strcmp(benv, "0") == 0) && p.n % 4 == 0 &&
-                    ((uintptr_t)p.X % 16) == 0 && ((uintptr_t)p.grad % 16) == 0;
-  TmgFn fn = v->fn[bulk ? 1 : 0][(int)h];
-  static std::atomic<uint64_t> attr_done[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t bit = 1ull << (6 * (int)(v - kTmgVariants) + 3 * (bulk ? 1 : 0) + (int)h);
-  if (dev < 0 || dev >= 64 || !(attr_done[dev].load(std::memory_order_relaxed) & bit)) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dtg::DYN_SMEM);
-    if (dev >= 0 && dev < 64) attr_done[dev].fetch_or(bit, std::memory_order_relaxed);
-  }
-  const int per_block = dtg::THREADS / v->G;   // points in flight per block
-  int64_t blocks = (int64_t)num_sms() * 4;
-  const int64_t need = (p.M + per_block - 1) / per_block;
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  fn<<<(unsigned)blocks, dtg::THREADS, dtg::DYN_SMEM, stream>>>(p);
-  g_launches += 1;
-  g_last_threads = dtg::THREADS;
-  g_last_blocks = (int)blocks;
-  g_last_kernel = h == HOPF_H_L2 ? "hopf_diag_tmg_kernel<l2>"
-                  : (h == HOPF_H_WL1 ? "hopf_diag_tmg_kernel<wl1>" : "hopf_diag_tmg_kernel<l1>");
-  return check_launch("hopf_diag_tmg_kernel");
-}
-
-// Union with H = l2 (diag_tmu.cuh): G lanes per point, TMEM, x read once per point by bulk copies,
-// the best set's grad kept in shared memory.  Used when the rows are 16-byte aligned and the
-// per-set tables fit the block's shared memory; HOPF_UNION_TMG=0 selects the register kernel.
-using TmuFn = void (*)(const DiagParams);
-struct TmuVariant {
-  int G, CPL;
-  TmuFn fn;
-  size_t (*smem)(int K);
-};
-#define HOPF_TMU(G_, C_) {G_, C_, dtu::hopf_union_tmg_kernel<G_, C_>, dtu::smem_bytes<G_, C_>}
-static const TmuVariant kTmuVariants[] = {HOPF_TMU(4, 16)};
-
-static const TmuVariant *pick_tmu(const DiagParams &p) {
-  static const char *env = getenv("HOPF_UNION_TMG");
-  if (env && strcmp(env, "0") == 0) return nullptr;
-  if (p.n % 4 != 0 || (((uintptr_t)p.X | (uintptr_t)p.grad | (uintptr_t)p.Y) & 15) != 0) return nullptr;
-  for (const TmuVariant &v : kTmuVariants)
-    if (v.G * v.CPL >= p.n && v.G * (v.CPL - 2) < p.n && v.smem(p.K) <= (size_t)dtu::DYN_SMEM) return &v;
-  return nullptr;
-}
-
-static int launch_union_tmg(const DiagParams &p, const TmuVariant *v, cudaStream_t stream) {
-  static std::atomic<uint64_t> attr_done[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t bit = 1ull << (int)(v - kTmuVariants);
-  if (dev < 0 || dev >= 64 || !(attr_done[dev].load(std::memory_order_relaxed) & bit)) {
-    cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dtu::DYN_SMEM);
-    if (dev >= 0 && dev < 64) attr_done[dev].fetch_or(bit, std::memory_order_relaxed);
-  }
-  const int per_block = dtu::THREADS / v->G;
-  int64_t blocks = (int64_t)num_sms() * dtu::BLOCKS_PER_SM;
-  const int64_t need = (p.M + per_block - 1) / per_block;
-  if (blocks > need) blocks = need;
-  if (blocks < 1) blocks = 1;
-  v->fn<<<(unsigned)blocks, dtu::THREADS, dtu::DYN_SMEM, stream>>>(p);
-  g_launches += 1;
-  g_last_threads = dtu::THREADS;
-  g_last_blocks = (int)blocks;
-  g_last_kernel = "hopf_union_tmg_kernel<l2>";
-  return check_launch("hopf_union_tmg_kernel");
-}
-
 // ---------------------------------------------------------------- NEXT-4 helpers
 // istar = 0 where the first solve is valid, -1 on invalid points
 __global__ void hopf_istar_init_kernel(int64_t M, const int32_t *iters, int32_t *istar) {
@@ -323,10 +228,11 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   static const char *tm_env = getenv("HOPF_DIAG_TM");
   if (!ell && !is_union && v->G == 32 && v->CPL == 32 && !(tm_env && strcmp(tm_env, "0") == 0))
     return launch_diag_tm(p, h, stream);
-  if (!ell && !is_union)
-    if (const TmgVariant *tv = pick_tmg(p.n)) return launch_diag_tmg(p, h, tv, stream);
-  if (is_union && h == HOPF_H_L2 && p.dist == nullptr)
-    if (const TmuVariant *uv = pick_tmu(p)) return launch_union_tmg(p, uv, stream);
+  {   // grouped TMEM kernels (tmg_api.cu) where a variant fits
+    bool handled = false;
+    const int rc = tmg_try_launch(p, (int)h, is_union, stream, &handled);
+    if (handled) return rc;
+  }
   KernFn fn = ell ? v->fn[0][0] : v->fn[(int)h][is_union ? 1 : 0];
   // Block size: the one that keeps the most warps resident per SM (register-limited kernels
   // lose whole 256-thread blocks to the allocation granularity); ties go to the larger block.
