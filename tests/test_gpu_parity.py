@@ -811,3 +811,81 @@ def test_union_ragged_widths(hb, n, K, h):
                                              want_phik=True)
     o = oracle.eval_union(X, t, Dk, Ck, gk, h, w if h == "wl1" else None, want_y=want_y)
     check_union(phi, grad, it, Y if want_y else None, ks, pk, o, t)
+
+
+# ----------------------------------------------------------------- bounds (no compute-sanitizer on the pool)
+def _guarded(shape, fill, pad=256, dtype=None):
+    """A CUDA tensor view of `shape` in the middle of a larger buffer whose margins hold `fill`."""
+    import torch
+    numel = int(np.prod(shape))
+    buf = torch.full((numel + 2 * pad,), fill, dtype=dtype or torch.float32, device="cuda")
+    return buf, buf[pad:pad + numel].view(shape)
+
+
+@pytest.mark.parametrize("family", ["tm", "tmg", "reg", "tmu", "dense"])
+def test_kernels_stay_in_bounds_and_are_deterministic(hb, family):
+    """Inputs sit between NaN margins and outputs between sentinel margins: a kernel that reads
+    outside its rows would pull NaN into a valid result (compared bitwise with a clean run), one
+    that writes outside would change a sentinel.  Two runs must agree bit for bit (races)."""
+    import torch
+    name, M, n = {"tm": ("c3", 700, None), "tmg": ("c2", 3001, None), "reg": ("c2", 3001, 90),
+                  "tmu": ("c5", 1001, None), "dense": ("c4", 1001, None)}[family]
+    wl = inputs.config(name, M=M, n=n)
+    X, t = inputs.points(wl)
+    n = wl.n
+    SENT = 12345.0
+
+    def run(guard):
+        if guard:
+            bx, Xd = _guarded((M, n), float("nan"))
+            bt, td = _guarded((M,), float("nan"))
+            Xd.copy_(torch.from_numpy(X)); td.copy_(torch.from_numpy(t))
+            bp, phi = _guarded((M,), SENT)
+            bg, grad = _guarded((M, n), SENT)
+            bi, it = _guarded((M,), 777, dtype=torch.int32)
+            bufs = [(bp, phi), (bg, grad), (bi, it)]
+        else:
+            Xd, td = dev(X), dev(t)
+            phi, grad = torch.empty(M, device="cuda"), torch.empty((M, n), device="cuda")
+            it = torch.empty(M, dtype=torch.int32, device="cuda")
+            bufs = []
+        if family == "tmu":
+            if guard:
+                by, Y = _guarded((M, n), SENT)
+                bk, ks = _guarded((M,), 777, dtype=torch.int32)
+                bufs += [(by, Y), (bk, ks)]
+            else:
+                Y, ks = torch.empty((M, n), device="cuda"), torch.empty(M, dtype=torch.int32, device="cuda")
+            L = hb.lib()
+            Dk, Ck, gk = dev(wl.Dk), dev(wl.Ck), dev(wl.gammak)
+            rc = L.hopf_eval_union(M, n, wl.K, Xd.data_ptr(), td.data_ptr(), Dk.data_ptr(), Ck.data_ptr(),
+                                   gk.data_ptr(), 2, None, 1.0, 1000, 1e-8, phi.data_ptr(), grad.data_ptr(),
+                                   it.data_ptr(), Y.data_ptr(), ks.data_ptr(), None,
+                                   torch.cuda.current_stream().cuda_stream)
+            assert rc == 0
+            outs = (phi, grad, it, Y, ks)
+        elif family == "dense":
+            plan = hb.DensePlan(wl.Q, wl.Lam)
+            hb.eval_dense(Xd, td, plan, wl.gamma, "l1", out=(phi, grad, it))
+            outs = (phi, grad, it)
+        else:
+            hb.eval_diag(Xd, td, dev(wl.D), dev(wl.c), wl.gamma, wl.h, dev(wl.w), out=(phi, grad, it))
+            outs = (phi, grad, it)
+        torch.cuda.synchronize()
+        kern = hb.last_kernel()
+        for buf, view in bufs:
+            pad = (buf.numel() - view.numel()) // 2
+            margin = torch.cat([buf[:pad], buf[pad + view.numel():]])
+            want = SENT if buf.dtype == torch.float32 else 777
+            assert torch.all(margin == want), f"{family}: write outside the output ({kern})"
+        return [o.clone() for o in outs], kern
+
+    a, ka = run(True)
+    b, kb = run(False)
+    c, _ = run(True)
+    expect = {"tm": "hopf_diag_tm_kernel", "tmg": "hopf_diag_tmg_kernel", "reg": "hopf_diag_kernel",
+              "tmu": "hopf_union_tmg_kernel", "dense": "hopf_dense_tc3_kernel"}[family]
+    assert ka.startswith(expect) and kb.startswith(expect), (ka, kb)
+    for u, v, w in zip(a, b, c):
+        assert torch.equal(u.nan_to_num(0.25), v.nan_to_num(0.25)), f"{family}: guarded run differs"
+        assert torch.equal(u.nan_to_num(0.25), w.nan_to_num(0.25)), f"{family}: nondeterministic"
