@@ -7,7 +7,7 @@
 // and arithmetic as hopf_diag_kernel (diag_kernel.cuh) and hopf_diag_tm_kernel (diag_tm.cuh);
 // only the storage and the control flow differ:
 //
-//   registers : d, b (u between l2 trips) — 2 x CPL floats per lane
+//   registers : l1 / wl1: a = d - b and b; l2: -d and the pending u — 2 x CPL floats per lane
 //   TMEM      : x_hat (columns 0-31), v (32-63), kappa / -kappa (64-95), tau_i (96-127, wl1)
 //
 // A group of G lanes owns a point, lane gl of the group owns coordinates gl + G j (j < CPL).
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       for (int q = 0; q < NP; q++) {
         const float2 xt = d[q];
         if (L2) { d[q] = make_float2(-xt.x, -xt.y); b[q] = xt; }   // -d^0, pending u
-        else b[q] = splat2(0.f);                                    // d^0 = x - c, b^0 = 0
+        else b[q] = splat2(0.f);                                    // a^0 = d^0 = x - c, b^0 = 0
       }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;");
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
     if (stop) {
 #pragma unroll
       for (int q = 0; q < NP; q++) {
-        const float2 g = L2 ? make_float2(-d[q].x, -d[q].y) : d[q];
+        const float2 g = L2 ? make_float2(-d[q].x, -d[q].y) : add2(d[q], b[q]);   // l1: d = a + b
         my_g[G * (2 * q)] = spec == 2 ? __int_as_float(0x7fc00000) : g.x;
         my_g[G * (2 * q + 1)] = spec == 2 ? __int_as_float(0x7fc00000) : g.y;
       }
@@ -423,15 +423,16 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
             c0 = fma2(dv, dv, c0);
             r0 = fma2(b[q], b[q], r0);
           } else {
-            const float2 a = sub2(d[q], b[q]);
-            vn = fma2(kq, a, xh);                                   // (3.4a): v^k
+            // l1 / wl1 state: d[q] holds a = d - b (what (3.4a) consumes), b[q] = b; both are
+            // updated in place (no register moves of loop-carried values)
+            vn = fma2(kq, d[q], xh);                                // (3.4a): v^k = x_hat + kappa a
             const float2 dv = sub2(vn, v);                          // v^k - v^{k-1}
             const float2 u = add2(vn, b[q]);
             const float2 tq = WL1 ? make_float2(ch[WL1 ? 3 : 0][2 * e2], ch[WL1 ? 3 : 0][2 * e2 + 1]) : tP;
-            b[q] = clamp2(u, tq);                                   // projection (Moreau)
-            const float2 dn = sub2(u, b[q]);                        // (3.4b) shrink_1
-            const float2 dd = sub2(dn, d[q]);                       // d^k - d^{k-1}
-            d[q] = dn;
+            const float2 t = sub2(vn, d[q]);                        // v^k - a^{k-1}
+            b[q] = clamp2(u, tq);                                   // b^k: projection (Moreau)
+            d[q] = fma2(b[q], splat2(-2.f), u);                     // a^k = d^k - b^k, d^k = u - b^k
+            const float2 dd = sub2(t, b[q]);                        // d^k - d^{k-1} = v^k - b^k - a^{k-1}
             a0 = fma2(dd, dd, a0); c0 = fma2(dv, dv, c0);
           }
           ch[2][2 * e2] = vn.x;
@@ -492,7 +493,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
           wait_ld(vv);
 #pragma unroll
           for (int e2 = 0; e2 < SZ / 2; e2++) {
-            const float2 dmv = sub2(d[4 * c + e2], make_float2(vv[0][2 * e2], vv[0][2 * e2 + 1]));
+            const float2 dk = L2 ? d[4 * c + e2] : add2(d[4 * c + e2], b[4 * c + e2]);   // d^k = a + b
+            const float2 dmv = sub2(dk, make_float2(vv[0][2 * e2], vv[0][2 * e2 + 1]));
             if (e2 & 1) sb3 = fma2(dmv, dmv, sb3);
             else sb2 = fma2(dmv, dmv, sb2);
           }
