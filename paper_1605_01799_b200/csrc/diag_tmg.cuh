@@ -308,17 +308,23 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
         bulk_load(smem_u32(xbuf + grp * PITCH), p.X + (pt + ngroups) * (int64_t)n, row_bytes, my_bar);
     }
     const float tl = tt / lam;
+    // the chunk stores are warp-collective: lanes that keep their point write back what they
+    // read; when every lane starts a point or has none left (the lockstep case), nothing is read
+#ifndef HOPF_TMG_SKIPLOAD
+#define HOPF_TMG_SKIPLOAD 0   // skipping the reads when every lane is new measured slower (C2 1.265 vs 1.231 ms)
+#endif
+    const bool keep_any = !HOPF_TMG_SKIPLOAD || __any_sync(0xffffffffu, have && !fresh);
     for_chunks<CPL>([&](auto ci, auto szc) {
       constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
       float ch[3][8];
-      ldn<SZ, C_XH + 8 * c>(tl0, ch[0]);
-      ldn<SZ, C_V + 8 * c>(tl0, ch[1]);
-      if constexpr (WL1) ldn<SZ, C_TAU + 8 * c>(tl0, ch[2]);
-      else {
 #pragma unroll
-        for (int e = 0; e < 8; e++) ch[2][e] = 0.f;
+      for (int e = 0; e < 8; e++) ch[0][e] = ch[1][e] = ch[2][e] = 0.f;
+      if (keep_any) {
+        ldn<SZ, C_XH + 8 * c>(tl0, ch[0]);
+        ldn<SZ, C_V + 8 * c>(tl0, ch[1]);
+        if constexpr (WL1) ldn<SZ, C_TAU + 8 * c>(tl0, ch[2]);
+        wait_ld(ch);
       }
-      wait_ld(ch);
       if (fresh) {
 #pragma unroll
         for (int e = 0; e < SZ; e++) {

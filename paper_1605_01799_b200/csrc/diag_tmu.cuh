@@ -138,13 +138,20 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   auto set_setup = [&](bool fresh) {
     const float *xr = xrow(xs) + gl;
     const float2 *dc = DC_s + kset * (G * CPL) + gl;
+    // lanes that keep their set write back what they read; in the lockstep case (every lane
+    // starts a set or has no point left) nothing is read
+    const bool keep_any = __any_sync(0xffffffffu, have && !fresh);
     for_chunks<CPL>([&](auto ci, auto szc) {
       constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
       float ch[3][8];
-      ldn<SZ, C_XH + 8 * c>(tl0, ch[0]);
-      ldn<SZ, C_V + 8 * c>(tl0, ch[1]);
-      ldn<SZ, C_K + 8 * c>(tl0, ch[2]);
-      wait_ld(ch);
+#pragma unroll
+      for (int e = 0; e < 8; e++) ch[0][e] = ch[1][e] = ch[2][e] = 0.f;
+      if (keep_any) {
+        ldn<SZ, C_XH + 8 * c>(tl0, ch[0]);
+        ldn<SZ, C_V + 8 * c>(tl0, ch[1]);
+        ldn<SZ, C_K + 8 * c>(tl0, ch[2]);
+        wait_ld(ch);
+      }
       if (fresh) {
 #pragma unroll
         for (int e = 0; e < SZ; e++) {
