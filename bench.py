@@ -443,18 +443,27 @@ def main():
                "h2d_bytes_per_step": int(Xp.numel() * 4 + tp.numel() * 4),
                "d2h_bytes_per_step": int(M * 4 + M * n * 4 + M * 4),
                "api": "hopf_eval_diag_host (pinned host buffers, chunked H2D/kernel/D2H pipeline)"}
-    elif not args.no_e2e and wl.kind in ("normsq", "ella"):
-        # no host-buffer entry point: pinned H2D of x and t, the call, D2H of phi, grad, iters
+    elif not args.no_e2e:
+        # no host-buffer entry point for these kinds: pinned H2D of x and t, the call, D2H of every
+        # result the call writes (phi, grad, iters; union: + y, k*; maxh: + winner; distance: its six)
         Xp = torch.from_numpy(Xh).pin_memory()
         tp = torch.from_numpy(th).pin_memory()
-        outh = (torch.empty(M, pin_memory=True), torch.empty((M, n), pin_memory=True),
-                torch.empty(M, dtype=torch.int32, pin_memory=True))
+
+        def results():
+            if wl.kind == "union":
+                return [phi, grad, iters, Y, kst]
+            if wl.kind == "maxh":
+                return list(mres["r"])
+            if wl.kind == "distance":
+                return list(dres["r"])
+            return list(out)
+        outh = [torch.empty(r.shape, dtype=r.dtype, pin_memory=True) for r in results()]
 
         def e2e_step():
             X.copy_(Xp, non_blocking=True)
             t.copy_(tp, non_blocking=True)
             step()
-            for hbuf, dbuf in zip(outh, out):
+            for hbuf, dbuf in zip(outh, results()):
                 hbuf.copy_(dbuf, non_blocking=True)
             torch.cuda.synchronize(dev)
         for _ in range(2):
@@ -470,11 +479,13 @@ def main():
             tm = torch.tensor([el], device=dev, dtype=torch.float64)
             dist.all_reduce(tm, op=dist.ReduceOp.MAX)
             el = float(tm.item())
+        api = {"normsq": "hopf_eval_normsq", "ella": "hopf_eval_diag_A", "union": "hopf_eval_union",
+               "maxh": "hopf_eval_maxh", "distance": "hopf_distance_union",
+               "dense": "hopf_eval_dense"}.get(wl.kind, wl.kind)
         e2e = {"value": M * ws * ksteps / el, "unit": UNIT,
                "h2d_bytes_per_step": int(Xp.numel() * 4 + tp.numel() * 4),
-               "d2h_bytes_per_step": int(M * 4 + M * n * 4 + M * 4),
-               "api": f"{'hopf_eval_normsq' if wl.kind == 'normsq' else 'hopf_eval_diag_A'} "
-                      "with torch pinned copies on the same stream"}
+               "d2h_bytes_per_step": int(sum(h.numel() * h.element_size() for h in outh)),
+               "api": f"{api} with torch pinned copies on the same stream"}
 
     if rank != 0:
         if ws > 1:
