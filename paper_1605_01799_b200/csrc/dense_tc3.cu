@@ -509,12 +509,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           g4[0] = make_float4(gout[0], gout[1], gout[2], gout[3]);
           g4[1] = make_float4(gout[4], gout[5], gout[6], gout[7]);
         }
+        // U^{k+1} first: its K block is released to the MMA thread before the stopping sums of
+        // this stage are formed (they are not on the MMA -> epilogue -> MMA chain)
         uint32_t hw[4], lw[4];
+        float2 dOs[4], dns[4];
 #pragma unroll
         for (int i2 = 0; i2 < 4; i2++) {
           const int i = 4 * s + i2;                 // coordinate pair index 0..15
           const float2 v = make_float2(va[2 * i2], va[2 * i2 + 1]);
-          const float2 vp = make_float2(vpa[2 * i2], vpa[2 * i2 + 1]);
           const float2 x = make_float2(xa[2 * i2], xa[2 * i2 + 1]);
           const float2 wv = (HK == HK_WL1) ? *reinterpret_cast<const float2 *>(w_s + cb + 2 * i)
                                            : splat2(1.f);
@@ -522,24 +524,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const float2 tauo = (HK == HK_WL1) ? mul2(splat2(told), wv) : splat2(told);
           const float2 u = us[i];
           const float2 bo = clamp2(u, tauo);               // b^{k-1}
-          const float2 dO = sub2(u, bo);                   // d^{k-1}
+          dOs[i2] = sub2(u, bo);                           // d^{k-1}
           const float2 un = add2(v, bo);                   // argument of (3.4b): v^k + b^{k-1}
           const float2 bn = clamp2(un, tau);               // b^k (projection, Moreau)
           const float2 dn = sub2(un, bn);                  // d^k = shrink_1
-          const float2 ed = sub2(dn, dO);
-          asd = fma2(ed, ed, asd);
-          const float2 fd = sub2(dn, v);
-          asb = fma2(fd, fd, asb);
-          const float2 gd = sub2(v, vp);
-          asv = fma2(gd, gd, asv);
+          dns[i2] = dn;
           const float2 U = fma2(splat2(lam), sub2(dn, bn), x);   // U^{k+1} = x + lambda (d - b)
           us[i] = un;
           split2(U, hw[i2], lw[i2]);
-        }
-        if (s < 3 && r > 0) {
-          tmem_ld8(tbuf + 8 * (s + 1), va);
-          tmem_ld8(tpbuf + 8 * (s + 1), vpa);
-          tmem_ld8(t_x + 8 * (s + 1), xa);
         }
         // U^{k+1} of coordinates cb + 8 s .. + 8 -> its K' block: one 16-byte row chunk (hi, lo)
         const uint32_t off = kmaj(pl, 64 * s + 32 * h + 8 * j);
@@ -553,7 +545,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (rank == 0) mbar_arrive_local(bar_stage0 + 8 * s);
           else mbar_arrive_remote(stage_remote + 8 * s);
         }
-        if (s < 3 && r > 0) tmem_wait_ld3(va, vpa, xa);
+        // the paper's three stopping sums of this stage, off the MMA chain
+#pragma unroll
+        for (int i2 = 0; i2 < 4; i2++) {
+          const float2 v = make_float2(va[2 * i2], va[2 * i2 + 1]);
+          const float2 vp = make_float2(vpa[2 * i2], vpa[2 * i2 + 1]);
+          const float2 ed = sub2(dns[i2], dOs[i2]);
+          asd = fma2(ed, ed, asd);
+          const float2 fd = sub2(dns[i2], v);
+          asb = fma2(fd, fd, asb);
+          const float2 gd = sub2(v, vp);
+          asv = fma2(gd, gd, asv);
+        }
+        if (s < 3 && r > 0) {
+          tmem_ld8(tbuf + 8 * (s + 1), va);
+          tmem_ld8(tpbuf + 8 * (s + 1), vpa);
+          tmem_ld8(t_x + 8 * (s + 1), xa);
+          tmem_wait_ld3(va, vpa, xa);
+        }
       }
       // ---- partial sums of this round -> red[r & 1]; released through bar_red ---------------
       {
