@@ -119,7 +119,12 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   int wstatus = 0, it = 0, lim = 0, spec = 0, kset = 0;
   float tt = 0.f, tauS = 0.f, s_cur = 1.f;
   bool sv_ok = false;
-  float tpre = have ? __ldg(p.t + pt) : 0.f;
+  // distance mode (NEXT-1): non-null p.dist; the point is the query y, evaluated at
+  // s_0 = 0 and then at the Newton iterates s_l (p.t is not read)
+  const bool DIST = p.dist != nullptr;
+  float tpre = (have && !DIST) ? __ldg(p.t + pt) : 0.f;
+  int nn = 0;               // Newton evaluations at s > 0 so far
+  float s_lo = 0.f, s_hi = 0.f;   // bracket of the root (R25)
   uint32_t xph = 0;        // parity bits of the two x-row mbarriers
   int xs = 0;              // x row of the current point
   int cand = 0;            // grad row that receives the next stopped set's d (the other is the best)
@@ -185,10 +190,11 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   auto point_start = [&](bool fresh) {
     bool bad = false;
     if (fresh) {
-      tt = tpre;
+      tt = DIST ? 0.f : tpre;   // distance mode starts at s_0 = 0 (R24)
       bad = !(tt >= 0.f) || !finite_f(tt);
       const int64_t nx = pt + ngroups;
-      tpre = nx < M ? __ldg(p.t + nx) : 0.f;
+      tpre = (nx < M && !DIST) ? __ldg(p.t + nx) : 0.f;
+      nn = 0;
       dtg::mbar_wait(dtg::smem_u32(bars + xs), (xph >> xs) & 1u);
       xph ^= 1u << xs;
       float fin = 0.f;   // x * 0 accumulates NaN iff some x is NaN or infinite
@@ -361,6 +367,36 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
       }
       point_done = spec == 2 || kset + 1 >= K;
     }
+    bool restart = false;   // distance mode: the K sets again at the next Newton iterate
+    if (DIST && point_done && spec != 2 && bestk >= 0) {
+      // psi(y,s) = best, ||grad psi|| = bgn; Newton in s with d psi/dt = -||grad psi|| (eq.
+      // Newton_zero), the same step / stop / safeguard order as the oracle (R24-R26)
+      const float s0 = tt;
+      bool fin = false;
+      if (nn == 0 && s0 == 0.f) {
+        if (!(best > 0.f)) fin = true;                  // y in Omega: dist 0, proj y
+        else { s_lo = 0.f; s_hi = __int_as_float(0x7f800000); }
+      } else if (best > 0.f) {
+        s_lo = s0;
+      } else {
+        s_hi = s0;
+      }
+      if (!fin && (nn >= p.max_newton || !(bgn > 0.f))) fin = true;
+      if (!fin) {
+        float sn = s0 + best / bgn;
+        if (fabsf(sn - s0) <= p.stol * fmaxf(1.f, s0)) {
+          fin = true;                                   // R26: keep the evaluated s
+        } else {
+          if (!(sn > s_lo && sn < s_hi)) sn = 0.5f * (s_lo + s_hi);   // R25
+          point_done = false;
+          restart = true;
+          nn++;
+          tt = sn;
+          tauS = sn / lam;
+          spec = 0;
+        }
+      }
+    }
     // ---- the point's outputs (groups whose last set finished) ---------------------------------
     if (__any_sync(0xffffffffu, point_done)) {
       float *const br = grow_s(cand ^ 1) + gl;   // best grad row
@@ -372,15 +408,18 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
 #pragma unroll
         for (int j = 0; j < CPL; j++) {
           const float g = br[G * j];
-          // y = x - t grad / ||grad||, c_k* if grad = 0 (R18)
-          const float y = bgn > 0.f ? yr[G * j] - tt * (g * ign) : dck[G * j].y;
+          // y = x - t grad / ||grad||, c_k* if grad = 0 (R18); distance mode:
+          // pi = y - s grad / ||grad|| at the evaluated s, y itself inside
+          const float y = DIST ? ((tt > 0.f && bgn > 0.f) ? yr[G * j] - tt * (g * ign) : yr[G * j])
+                               : (bgn > 0.f ? yr[G * j] - tt * (g * ign) : dck[G * j].y);
           br[G * j] = nanpt ? gnan : g;
           yr[G * j] = nanpt ? gnan : y;
         }
         if (gl == 0) {
           p.phi[pt] = nanpt ? gnan : best;
-          p.iters[pt] = nanpt ? INT32_MIN : bestit;
+          p.iters[pt] = nanpt ? INT32_MIN : (DIST ? nn : bestit);
           if (p.kstar) p.kstar[pt] = nanpt ? -1 : bestk;
+          if (DIST) p.dist[pt] = nanpt ? gnan : tt;
         }
       }
       dtg::fence_proxy_async();
@@ -397,8 +436,15 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
       }
     }
     // ---- next set, or next point --------------------------------------------------------------
-    const bool next_set = done && !point_done;
+    const bool next_set = done && !point_done && !restart;
     if (next_set) kset++;
+    if (restart) {
+      kset = 0;
+      best = __int_as_float(0x7f800000);
+      bestk = -1;
+      bestit = 0;
+      bgn = 0.f;
+    }
     if (point_done) {
       pt += ngroups;
       have = pt < M;
@@ -412,7 +458,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
     }
     const bool started = point_done && have;
     if (__any_sync(0xffffffffu, started)) point_start(started);
-    if (__any_sync(0xffffffffu, next_set || started)) set_setup(next_set || started);
+    if (__any_sync(0xffffffffu, next_set || started || restart)) set_setup(next_set || started || restart);
     any_have = __any_sync(0xffffffffu, have);
   }
   if (gl == 0) dtg::bulk_wait_all();

@@ -371,7 +371,8 @@ int hopf_distance_union(int64_t M, int32_t n, int32_t K, const float *Y, const f
   p.phi = psi; p.grad = grad; p.iters = newton; p.Y = proj; p.kstar = kstar; p.phik = nullptr;
   p.dist = dist; p.max_newton = max_newton; p.stol = stol;
   int rc = launch_diag_like(p, HOPF_H_L2, true, (cudaStream_t)stream);
-  if (rc == HOPF_OK) g_last_kernel = "hopf_diag_kernel<union, distance>";
+  if (rc == HOPF_OK && strcmp(g_last_kernel, "hopf_diag_kernel<union>") == 0)
+    g_last_kernel = "hopf_diag_kernel<union, distance>";
   return rc;
 }
 

@@ -104,7 +104,10 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
                     : (h == HOPF_H_WL1 ? "hopf_diag_tmg_kernel<wl1>" : "hopf_diag_tmg_kernel<l1>");
     return check_launch("hopf_diag_tmg_kernel");
   }
-  if (h != HOPF_H_L2 || p.dist != nullptr || (p.Y && ((uintptr_t)p.Y & 15) != 0)) return HOPF_OK;
+  // union (l2), also in distance mode (NEXT-1: p.dist non-null, p.Y = the projections)
+  static const char *denv = getenv("HOPF_DIST_TMG");
+  if (p.dist && denv && strcmp(denv, "0") == 0) return HOPF_OK;
+  if (h != HOPF_H_L2 || (p.Y && ((uintptr_t)p.Y & 15) != 0)) return HOPF_OK;
   int idx = 0;
   const TmuVariant *v = pick_tmu(p, &idx);
   if (!v) return HOPF_OK;
@@ -119,7 +122,7 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   g_launches += 1;
   g_last_threads = dtu::THREADS;
   g_last_blocks = (int)blocks;
-  g_last_kernel = "hopf_union_tmg_kernel<l2>";
+  g_last_kernel = p.dist ? "hopf_union_tmg_kernel<l2, distance>" : "hopf_union_tmg_kernel<l2>";
   return check_launch("hopf_union_tmg_kernel");
 }
 
