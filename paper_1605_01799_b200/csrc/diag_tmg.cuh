@@ -185,13 +185,14 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   static_assert(G >= 2 && G <= 16 && (G & (G - 1)) == 0, "G in {2, 4, 8, 16}");
   static_assert(CPL % 2 == 0 && CPL <= 32 && (CPL % 8 == 0 || CPL % 8 == 2 || CPL % 8 == 4),
                 "CPL = 8 a + {0, 2, 4}, at most 32");
-  static_assert(HK == HK_L1 || HK == HK_WL1 || HK == HK_L2, "l1, wl1, l2");
+  static_assert(HK == HK_L1 || HK == HK_WL1 || HK == HK_L2 || HK == HK_ELL || HK == HK_LINF, "l1, wl1, l2, ell, linf");
   static_assert(smem_bytes<G, CPL>() <= (size_t)DYN_SMEM, "shared buffers exceed the budget");
   constexpr int NP = CPL / 2;
   constexpr int GPW = 32 / G, GPB = THREADS / G;
   constexpr int PITCH = row_pitch(G * CPL, G);
   constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMG_WAIT8 / 8) > 0 ? (GPW * HOPF_TMG_WAIT8 / 8) : 1;
-  constexpr bool L2 = HK == HK_L2, WL1 = HK == HK_WL1;
+  constexpr bool L2 = HK == HK_L2, WL1 = HK == HK_WL1, ELL = HK == HK_ELL, LINF = HK == HK_LINF;
+  constexpr bool WTAB = WL1 || ELL;   // per-coordinate weights in the tables
   extern __shared__ __align__(16) uint8_t dyn_smem[];
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   for (int i = threadIdx.x; i < G * CPL; i += THREADS) {
     const bool real = i < n;
     const float Dv = real ? __ldg(p.D + i) : 1.f;
-    const float wv = (WL1 && real) ? __ldg(p.w + i) : 0.f;
+    const float wv = (WTAB && real) ? __ldg(p.w + i) : (ELL ? 1.f : 0.f);   // ELL pads with w = 1
     const float cv = (p.c && real) ? __ldg(p.c + i) : 0.f;
     A_s[i] = make_float4(1.f / (Dv + lam), wv, cv, 0.f);
     B_s[i] = make_float4(Dv + lam, wv, -0.5f * Dv, 1.f / Dv);
@@ -251,7 +252,19 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       kv[e] = (e < SZ && j < jmax) ? ksign * my_A[G * j].x : 0.f;
     }
     stn<SZ, C_K + 8 * c>(tl0, kv);
+    if constexpr (ELL) {   // w_i of this lane's slots (padded slots: w = 1, their u is 0)
+      float wv8[8];
+#pragma unroll
+      for (int e = 0; e < 8; e++) wv8[e] = e < SZ ? my_A[G * (8 * c + e)].y : 1.f;
+      stn<SZ, C_TAU + 8 * c>(tl0, wv8);
+    }
   });
+  // ELL: min_i w_i, the scale of the Newton stopping test on mu
+  float wmin = 1.f;
+  if constexpr (ELL) {
+    wmin = __int_as_float(0x7f800000);
+    for (int i = 0; i < n; i++) wmin = fminf(wmin, A_s[i].y);
+  }
 
   float2 d[NP], b[NP];
   int64_t pt = gid;
@@ -266,6 +279,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   int spec = 0;           // 0 normal, 1 t == 0, 2 invalid
   float s_cur = 1.f;      // l2: shrink factor of the pending (3.4b)
   bool sv_ok = false;     // l2: ||v^k - v^{k-1}||^2 <= tol of the pending iteration
+  float mu = 0.f;         // ELL / LINF: multiplier of the last projection (warm start of the next)
 #pragma unroll
   for (int q = 0; q < NP; q++) d[q] = b[q] = splat2(0.f);
   if (bulk && gl == 0 && have) bulk_load(smem_u32(xbuf + grp * PITCH), p.X + pt * (int64_t)n, row_bytes, my_bar);
@@ -356,6 +370,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       lim = spec ? 0 : p.max_iter;
       tauS = tt / lam;
       it = 0;
+      mu = 0.f;
       s_cur = 1.f;
       sv_ok = false;
       waiting = false;
@@ -374,7 +389,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
     if (stop) {
 #pragma unroll
       for (int q = 0; q < NP; q++) {
-        const float2 g = L2 ? make_float2(-d[q].x, -d[q].y) : add2(d[q], b[q]);   // l1: d = a + b
+        const float2 g = L2 ? make_float2(-d[q].x, -d[q].y)
+                            : ((ELL || LINF) ? d[q] : add2(d[q], b[q]));   // l1 / wl1: d = a + b
         my_g[G * (2 * q)] = spec == 2 ? __int_as_float(0x7fc00000) : g.x;
         my_g[G * (2 * q + 1)] = spec == 2 ? __int_as_float(0x7fc00000) : g.y;
       }
@@ -447,12 +463,197 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
         stn<SZ, C_V + 8 * c>(tl0, ch[2]);
       });
     };
+    bool conv = false;
+    int kdone;
+    if constexpr (ELL || LINF) {
+      // (3.4a), u = v + b for every coordinate (b holds u until the projection is known), fused
+      // with the first evaluation of the projection's sums at the warm-start mu
+      float2 s1 = splat2(0.f), s2 = s1;
+      {
+        const float2 muP = splat2(mu);
+        for_chunks<CPL>([&](auto ci, auto szc) {
+          constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
+          float ch[4][8];   // kappa, x_hat, v, w
+          ldn<SZ, C_K + 8 * c>(tl0, ch[0]);
+          ldn<SZ, C_XH + 8 * c>(tl0, ch[1]);
+          ldn<SZ, C_V + 8 * c>(tl0, ch[2]);
+          if constexpr (ELL) ldn<SZ, C_TAU + 8 * c>(tl0, ch[3]);
+          else {
+#pragma unroll
+            for (int e = 0; e < 8; e++) ch[3][e] = 0.f;
+          }
+          wait_ld(ch);
+#pragma unroll
+          for (int e2 = 0; e2 < SZ / 2; e2++) {
+            const int q = 4 * c + e2;
+            const float2 kq = make_float2(ch[0][2 * e2], ch[0][2 * e2 + 1]);
+            const float2 xh = make_float2(ch[1][2 * e2], ch[1][2 * e2 + 1]);
+            const float2 v = make_float2(ch[2][2 * e2], ch[2][2 * e2 + 1]);
+            const float2 a = sub2(d[q], b[q]);
+            const float2 vn = fma2(kq, a, xh);                    // (3.4a): v^k
+            const float2 dv = sub2(vn, v);
+            c0 = fma2(dv, dv, c0);
+            const float2 u = add2(vn, b[q]);
+            b[q] = u;
+            if constexpr (ELL) {   // S1 = sum w u^2/(w + mu)^2, S2 = sum w u^2/(w + mu)^3
+              const float2 w = make_float2(ch[3][2 * e2], ch[3][2 * e2 + 1]);
+              const float2 ee = add2(w, muP);
+              const float2 r = make_float2(rcp_approx(ee.x), rcp_approx(ee.y));
+              const float2 hh = __fmul2_rn(u, r);
+              const float2 wh2 = __fmul2_rn(__fmul2_rn(w, hh), hh);
+              s1 = add2(s1, wh2);
+              s2 = fma2(wh2, r, s2);
+            } else {               // S1 = sum max(|u| - mu, 0), S2 = #{|u| > mu}
+              const float ex = fabsf(u.x) - mu, ey = fabsf(u.y) - mu;
+              s1.x += fmaxf(ex, 0.f);
+              s1.y += fmaxf(ey, 0.f);
+              s2.x += ex > 0.f ? 1.f : 0.f;
+              s2.y += ey > 0.f ? 1.f : 0.f;
+            }
+            ch[2][2 * e2] = vn.x;
+            ch[2][2 * e2 + 1] = vn.y;
+          }
+          stn<SZ, C_V + 8 * c>(tl0, ch[2]);
+        });
+      }
+      float S1, S2;
+      bool ok_sv;
+      group_reduce3<G>(s1.x + s1.y, s2.x + s2.y, c0.x + c0.y, tol, S1, S2, ok_sv);
+      bool act = live && spec == 0;
+      int nit = 0;
+      if constexpr (ELL) {
+        // the dual-ellipsoid projection's multiplier by Newton on 1/sqrt(S1) - 1/tau, warm start,
+        // clamp at 0 (the inside case), a step below 1e-3 (mu + min w) accepted (reading R27;
+        // the same scheme as the register kernel)
+        const float itau = rcp_approx(tauS);
+        for (;;) {
+          if (act) {
+            const float mun = S2 > 0.f ? fmaxf(fmaf(S1 * rcp_approx(S2), fmaf(sqrtf(S1), itau, -1.f), mu), 0.f)
+                                       : 0.f;   // u = 0: d' = 0
+            act = !(fabsf(mun - mu) <= 1e-3f * (mun + wmin)) && ++nit < 30;
+            mu = mun;
+          }
+          if (!__any_sync(0xffffffffu, act)) break;
+          float2 t1 = splat2(0.f), t2 = splat2(0.f);
+          const float2 muP = splat2(mu);
+          for_chunks<CPL>([&](auto ci, auto szc) {
+            constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
+            float wv[1][8];
+            ldn<SZ, C_TAU + 8 * c>(tl0, wv[0]);
+            wait_ld(wv);
+#pragma unroll
+            for (int e2 = 0; e2 < SZ / 2; e2++) {
+              const float2 w = make_float2(wv[0][2 * e2], wv[0][2 * e2 + 1]);
+              const float2 ee = add2(w, muP);
+              const float2 r = make_float2(rcp_approx(ee.x), rcp_approx(ee.y));
+              const float2 hh = __fmul2_rn(b[4 * c + e2], r);
+              const float2 wh2 = __fmul2_rn(__fmul2_rn(w, hh), hh);
+              t1 = add2(t1, wh2);
+              t2 = fma2(wh2, r, t2);
+            }
+          });
+          S1 = group_sum<G>(t1.x + t1.y);
+          S2 = group_sum<G>(t2.x + t2.y);
+        }
+        // (3.4b): d' = mu u / (w + mu); (3.4c): b' = u - d'
+        const float2 muP = splat2(mu);
+        for_chunks<CPL>([&](auto ci, auto szc) {
+          constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
+          float wv[1][8];
+          ldn<SZ, C_TAU + 8 * c>(tl0, wv[0]);
+          wait_ld(wv);
+#pragma unroll
+          for (int e2 = 0; e2 < SZ / 2; e2++) {
+            const int q = 4 * c + e2;
+            const float2 w = make_float2(wv[0][2 * e2], wv[0][2 * e2 + 1]);
+            const float2 ee = add2(w, muP);
+            const float2 r = make_float2(rcp_approx(ee.x), rcp_approx(ee.y));
+            const float2 u = b[q];
+            const float2 dn = __fmul2_rn(__fmul2_rn(muP, u), r);
+            b[q] = sub2(u, dn);
+            const float2 dd = sub2(dn, d[q]);
+            d[q] = dn;
+            a0 = fma2(dd, dd, a0);
+          }
+        });
+      } else {
+        // the l1-ball multiplier by active-set Newton, exact acceptance when no |u_i| lies between
+        // two iterates (reading R28; the same scheme as the register kernel)
+        float mu_e = mu;
+        for (;;) {
+          float mun = mu_e;
+          if (act) mun = S2 > 0.f ? fmaxf(mu_e + __fdividef(S1 - tauS, S2), 0.f) : 0.f;
+          bool cross = false;
+#pragma unroll
+          for (int q = 0; q < NP; q++) {
+            const float ax = fabsf(b[q].x), ay = fabsf(b[q].y);
+            cross |= ((ax > mu_e) != (ax > mun)) || ((ay > mu_e) != (ay > mun));
+          }
+          cross = group_any<G>(cross);
+          const bool tiny = fabsf(mun - mu_e) <= HOPF_TINY_STEP * fmaxf(mun, 1e-30f);
+          if (act && (!cross || tiny || ++nit >= 64)) { mu = mun; act = false; }
+          if (!__any_sync(0xffffffffu, act)) break;
+          if (act) mu_e = mun;
+          float2 ta = splat2(0.f), tn = ta;
+#pragma unroll
+          for (int q = 0; q < NP; q++) {
+            const float ex = fabsf(b[q].x) - mu_e, ey = fabsf(b[q].y) - mu_e;
+            ta.x += fmaxf(ex, 0.f);
+            ta.y += fmaxf(ey, 0.f);
+            tn.x += ex > 0.f ? 1.f : 0.f;
+            tn.y += ey > 0.f ? 1.f : 0.f;
+          }
+          S1 = group_sum<G>(ta.x + ta.y);
+          S2 = group_sum<G>(tn.x + tn.y);
+        }
+        // (3.4b): d' = u - shrink_1(u, mu) = clamp(u, -mu, mu); (3.4c): b' = u - d'
+        const float2 muP = splat2(mu);
+#pragma unroll
+        for (int q = 0; q < NP; q++) {
+          const float2 u = b[q];
+          const float2 dn = clamp2(u, muP);
+          b[q] = sub2(u, dn);
+          const float2 dd = sub2(dn, d[q]);
+          d[q] = dn;
+          a0 = fma2(dd, dd, a0);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+      if (live) it++;
+      kdone = it;
+      // ||v^k - v^{k-1}||^2 came with the projection sums; ||d^k - d^{k-1}||^2 now;
+      // ||d^k - v^k||^2 only where both pass (v^k from TMEM)
+      const float sd = group_sum<G>(a0.x + a0.y);
+      const bool need = live && spec == 0 && ok_sv && sd <= tol;
+      if (__any_sync(0xffffffffu, need)) {
+        float2 sb2 = splat2(0.f);
+        for_chunks<CPL>([&](auto ci, auto szc) {
+          constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
+          float vv[1][8];
+          ldn<SZ, C_V + 8 * c>(tl0, vv[0]);
+          wait_ld(vv);
+#pragma unroll
+          for (int e2 = 0; e2 < SZ / 2; e2++) {
+            const float2 dmv = sub2(d[4 * c + e2], make_float2(vv[0][2 * e2], vv[0][2 * e2 + 1]));
+            sb2 = fma2(dmv, dmv, sb2);
+          }
+        });
+        const float sb = group_sum<G>(sb2.x + sb2.y);
+        conv = need && sb <= tol;
+      }
+      const bool stop = live && (spec != 0 || conv || kdone >= lim);
+      if (!__any_sync(0xffffffffu, stop)) continue;
+      if (stop) {
+        waiting = true;
+        wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -lim));
+        if (spec == 0) my_iters += (unsigned)kdone;
+      }
+      stash(stop);
+    } else {
     if (full_test) trip(std::true_type{});
     else trip(std::false_type{});
     asm volatile("tcgen05.wait::st.sync.aligned;");
 
-    bool conv = false;
-    int kdone;
     if constexpr (L2) {
       const float psd = a0.x + a0.y, psb = b0.x + b0.y, psv = c0.x + c0.y, pr2 = r0.x + r0.y;
       float r2;
@@ -499,7 +700,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
           wait_ld(vv);
 #pragma unroll
           for (int e2 = 0; e2 < SZ / 2; e2++) {
-            const float2 dk = L2 ? d[4 * c + e2] : add2(d[4 * c + e2], b[4 * c + e2]);   // d^k = a + b
+            const float2 dk = (L2 || ELL || LINF) ? d[4 * c + e2] : add2(d[4 * c + e2], b[4 * c + e2]);   // l1: d^k = a + b
             const float2 dmv = sub2(dk, make_float2(vv[0][2 * e2], vv[0][2 * e2 + 1]));
             if (e2 & 1) sb3 = fma2(dmv, dmv, sb3);
             else sb2 = fma2(dmv, dmv, sb2);
@@ -517,6 +718,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       }
       stash(stop);
     }
+    }   // H in {l1, wl1, l2}
     {
       const unsigned gbit = (gl == 0) ? 1u : 0u;
       const int nwait = __popc(__ballot_sync(0xffffffffu, waiting && gbit));
@@ -565,6 +767,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
         qs = fmaf(xt, dq, qs);
         qs = fmaf(B.z * dq, dq, qs);
         if (L2) hs = fmaf(dq, dq, hs);
+        else if (ELL) hs = fmaf(B.y * dq, dq, hs);
+        else if (LINF) hs = fmaxf(hs, fabsf(dq));
         else if (WL1) hs = fmaf(B.y, fabsf(dq), hs);
         else hs += fabsf(dq);
         if (!bulk && done && j < jmax) grow[G * j] = dq;
@@ -576,9 +780,9 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       if (done && gl == 0) bulk_store(grow - gl, smem_u32(gbuf + grp * PITCH), row_bytes);
     }
     const float qs = group_sum<G>(qs0 + qs1);
-    const float hsum = group_sum<G>(hs0 + hs1);
+    const float hsum = LINF ? group_max<G>(fmaxf(hs0, hs1)) : group_sum<G>(hs0 + hs1);
     if (done && gl == 0) {
-      float phiv = (spec == 1) ? qs + p.gamma : qs - tt * (L2 ? sqrtf(hsum) : hsum) + p.gamma;
+      float phiv = (spec == 1) ? qs + p.gamma : qs - tt * ((L2 || ELL) ? sqrtf(hsum) : hsum) + p.gamma;
       if (spec == 2) phiv = gnan;
       p.phi[pt] = phiv;
       p.iters[pt] = wstatus;

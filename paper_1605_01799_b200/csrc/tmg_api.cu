@@ -84,12 +84,12 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   static const char *benv = getenv("HOPF_TMG_BULK");
   if (!aligned || (benv && strcmp(benv, "0") == 0)) return HOPF_OK;
   if (!is_union) {
-    if (h != HOPF_H_L1 && h != HOPF_H_WL1 && h != HOPF_H_L2) return HOPF_OK;
+    if (h < HOPF_H_L1 || h > HOPF_H_LINF) return HOPF_OK;
     int idx = 0;
     const TmgVariant *v = pick_tmg(p.n, &idx);
-    if (!v) return HOPF_OK;
+    if (!v || !v->fn[h]) return HOPF_OK;
     TmgFn fn = v->fn[h];
-    ensure_smem_attr(fn, 3 * idx + h, dtg::DYN_SMEM);
+    ensure_smem_attr(fn, 5 * idx + h, dtg::DYN_SMEM);
     const int per_block = dtg::THREADS / v->G;   // points in flight per block
     int64_t blocks = (int64_t)num_sms() * 4;
     const int64_t need = (p.M + per_block - 1) / per_block;
@@ -100,8 +100,10 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
     g_launches += 1;
     g_last_threads = dtg::THREADS;
     g_last_blocks = (int)blocks;
-    g_last_kernel = h == HOPF_H_L2 ? "hopf_diag_tmg_kernel<l2>"
-                    : (h == HOPF_H_WL1 ? "hopf_diag_tmg_kernel<wl1>" : "hopf_diag_tmg_kernel<l1>");
+    static const char *names[5] = {"hopf_diag_tmg_kernel<l1>", "hopf_diag_tmg_kernel<wl1>",
+                                   "hopf_diag_tmg_kernel<l2>", "hopf_diag_tmg_kernel<ell>",
+                                   "hopf_diag_tmg_kernel<linf>"};
+    g_last_kernel = names[h];
     return check_launch("hopf_diag_tmg_kernel");
   }
   // union (l2), also in distance mode (NEXT-1: p.dist non-null, p.Y = the projections)
@@ -111,7 +113,7 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   int idx = 0;
   const TmuVariant *v = pick_tmu(p, &idx);
   if (!v) return HOPF_OK;
-  ensure_smem_attr(v->fn, 200 + idx, dtu::DYN_SMEM);
+  ensure_smem_attr(v->fn, 240 + idx, dtu::DYN_SMEM);
   const int per_block = dtu::THREADS / v->G;
   int64_t blocks = (int64_t)num_sms() * dtu::BLOCKS_PER_SM;
   const int64_t need = (p.M + per_block - 1) / per_block;

@@ -11,7 +11,7 @@ namespace hopf {
 using TmgFn = void (*)(const DiagParams);
 struct TmgVariant {
   int G, CPL;
-  TmgFn fn[3];   // [h kind]: l1, wl1, l2 (bulk row copies)
+  TmgFn fn[5];   // [h kind]: l1, wl1, l2, ell, linf (bulk row copies; null = not instantiated)
 };
 struct TmuVariant {
   int G, CPL;

@@ -4,9 +4,9 @@
 
 namespace hopf {
 extern const TmgVariant kTmgG16[] = {
-    {16, 20, {dtg::hopf_diag_tmg_kernel<16, 20, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_L2, true>}},
-    {16, 24, {dtg::hopf_diag_tmg_kernel<16, 24, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_L2, true>}},
-    {16, 28, {dtg::hopf_diag_tmg_kernel<16, 28, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_L2, true>}},
-    {16, 32, {dtg::hopf_diag_tmg_kernel<16, 32, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_L2, true>}}};
+    {16, 20, {dtg::hopf_diag_tmg_kernel<16, 20, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_L2, true>, nullptr, nullptr}},
+    {16, 24, {dtg::hopf_diag_tmg_kernel<16, 24, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_L2, true>, nullptr, nullptr}},
+    {16, 28, {dtg::hopf_diag_tmg_kernel<16, 28, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_L2, true>, nullptr, nullptr}},
+    {16, 32, {dtg::hopf_diag_tmg_kernel<16, 32, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_L2, true>, nullptr, nullptr}}};
 extern const int kTmgG16Count = 4;
 }  // namespace hopf

@@ -4,9 +4,9 @@
 
 namespace hopf {
 extern const TmgVariant kTmgG8[] = {
-    {8, 20, {dtg::hopf_diag_tmg_kernel<8, 20, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 20, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 20, HK_L2, true>}},
-    {8, 24, {dtg::hopf_diag_tmg_kernel<8, 24, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 24, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 24, HK_L2, true>}},
-    {8, 28, {dtg::hopf_diag_tmg_kernel<8, 28, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 28, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 28, HK_L2, true>}},
-    {8, 32, {dtg::hopf_diag_tmg_kernel<8, 32, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 32, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 32, HK_L2, true>}}};
+    {8, 20, {dtg::hopf_diag_tmg_kernel<8, 20, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 20, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 20, HK_L2, true>, nullptr, nullptr}},
+    {8, 24, {dtg::hopf_diag_tmg_kernel<8, 24, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 24, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 24, HK_L2, true>, nullptr, nullptr}},
+    {8, 28, {dtg::hopf_diag_tmg_kernel<8, 28, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 28, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 28, HK_L2, true>, nullptr, nullptr}},
+    {8, 32, {dtg::hopf_diag_tmg_kernel<8, 32, HK_L1, true>, dtg::hopf_diag_tmg_kernel<8, 32, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<8, 32, HK_L2, true>, nullptr, nullptr}}};
 extern const int kTmgG8Count = 4;
 }  // namespace hopf
