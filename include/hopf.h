@@ -97,7 +97,8 @@ int hopf_eval_diag(int64_t M, int32_t n, const float *X, const float *t, const f
  *   iters[i] = the winning set's status.
  *   Y [M*n] or NULL   closest (Hopf-Lax terminal) point y = x - t grad/||grad||
  *                     (P:1049-1051), y = c_k* if grad == 0 (R18); HOPF_H_L2 only.
- *   kstar [M] or NULL winning set index;  phi_k [M*K] or NULL every phi_k.
+ *   kstar [M] or NULL winning set index;  phi_k [M*K] or NULL every phi_k (an invalid point:
+ *   NaN for every k, kstar -1).
  *   Constraints: 1 <= K <= 64, n <= 256.                                                   */
 int hopf_eval_union(int64_t M, int32_t n, int32_t K, const float *X, const float *t,
                     const float *Dj, const float *C, const float *gamma, hopf_h_kind h,

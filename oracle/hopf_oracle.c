@@ -399,7 +399,10 @@ int oracle_union(int64_t M, int n, int K, const double *X, const double *t, cons
         int it = solve_diag_point(n, x, t[p], Dk + (size_t)k * n, Ck + (size_t)k * n,
                                   gammak[k], h, w, lambda, max_iter, tol, &ph, g, ws);
         if (phik) phik[p * K + k] = ph;
-        if (it == INT32_MIN) { bestk = -1; bestit = INT32_MIN; break; }
+        if (it == INT32_MIN) { /* invalid point: every phi_k is NaN (ABI convention) */
+          if (phik) for (int k2 = 0; k2 < K; k2++) phik[p * K + k2] = NAN;
+          bestk = -1; bestit = INT32_MIN; break;
+        }
         if (ph < best) { /* strict: lowest k wins ties (R19) */
           best = ph;
           bestk = k;

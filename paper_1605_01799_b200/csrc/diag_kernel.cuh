@@ -905,6 +905,8 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
           if (p.kstar) p.kstar[pt] = nanpt ? -1 : bestk;
           if (DIST) p.dist[pt] = nanpt ? __int_as_float(0x7fc00000) : tt;
         }
+        if (nanpt && p.phik)   // an invalid point's phi_k are NaN for every k
+          for (int k = gl; k < p.K; k += G) p.phik[pt * p.K + k] = __int_as_float(0x7fc00000);
         if (nanpt) {   // grad and y of a valid point were written when its best set finished
           float *grow = p.grad + pt * (int64_t)n;
           float *yrow = p.Y ? p.Y + pt * (int64_t)n : nullptr;

@@ -415,6 +415,8 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
           br[G * j] = nanpt ? gnan : g;
           yr[G * j] = nanpt ? gnan : y;
         }
+        if (nanpt && p.phik)   // an invalid point's phi_k are NaN for every k
+          for (int k = gl; k < K; k += G) p.phik[pt * K + k] = gnan;
         if (gl == 0) {
           p.phi[pt] = nanpt ? gnan : best;
           p.iters[pt] = nanpt ? INT32_MIN : (DIST ? nn : bestit);

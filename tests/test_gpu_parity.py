@@ -228,6 +228,17 @@ def check_union(phi, grad, it, Y, ks, pk, o, t):
     phi, grad, it, ks = (a.cpu().numpy() for a in (phi, grad, it, ks))
     pk = pk.cpu().numpy()
     Yg = Y.cpu().numpy() if Y is not None else None
+    # invalid points: the same set on both sides, every output NaN, k* = -1
+    bad = it_o == oracle.INVALID
+    assert np.array_equal(it == oracle.INVALID, bad)
+    assert np.all(np.isnan(phi[bad])) and np.all(np.isnan(grad[bad])) and np.all(ks[bad] == -1)
+    assert np.all(np.isnan(pk[bad]))
+    if Yg is not None:
+        assert np.all(np.isnan(Yg[bad]))
+    ok = ~bad
+    phi, grad, it, ks, pk, phi_o, grad_o, ks_o, pk_o, t = (a[ok] for a in (phi, grad, it, ks, pk, phi_o, grad_o, ks_o, pk_o, t))
+    if Yg is not None:
+        Yg, Y_o = Yg[ok], Y_o[ok]
     # every phi_k matches
     assert np.max(np.abs(pk - pk_o) / np.maximum(1, np.abs(pk_o))) <= PHI_RTOL
     assert np.max(np.abs(phi - phi_o) / np.maximum(1, np.abs(phi_o))) <= PHI_RTOL
@@ -889,3 +900,61 @@ def test_kernels_stay_in_bounds_and_are_deterministic(hb, family):
     for u, v, w in zip(a, b, c):
         assert torch.equal(u.nan_to_num(0.25), v.nan_to_num(0.25)), f"{family}: guarded run differs"
         assert torch.equal(u.nan_to_num(0.25), w.nan_to_num(0.25)), f"{family}: nondeterministic"
+
+
+# ----------------------------------------------------------------- every grouped-TMEM instance
+# n chosen so that each K1g instance (G x CPL) runs: 4x{8,10,12,16,20,24,26,28,32},
+# 8x{20,24,28,32}, 16x{20,24,28,32}; multiples of 4 (bulk rows)
+TMG_N = [28, 40, 48, 60, 80, 96, 100, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512]
+
+
+@pytest.mark.parametrize("n", TMG_N)
+@pytest.mark.parametrize("h", ["l1", "wl1", "l2", "ell", "linf"])
+def test_tmg_every_instance(hb, n, h):
+    """K1g parity at every compiled width with a shifted centre, lambda != 1, t == 0 and an
+    invalid point; the ELL / LINF kinds are instantiated for G = 4 (n <= 128)."""
+    rng = np.random.default_rng(3 * n + len(h))
+    M = 203
+    D = rng.uniform(0.5, 2.0, n).astype(np.float32)
+    c = rng.normal(size=n).astype(np.float32)
+    w = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    X = rng.normal(scale=2.0, size=(M, n)).astype(np.float32)
+    t = rng.uniform(0.0, 2.0, M).astype(np.float32)
+    t[1] = 0.0
+    X[2, n // 2] = np.nan
+    lam = 0.8
+    g = hb.eval_diag(dev(X), dev(t), dev(D), dev(c), -0.5, h, dev(w), lam=lam)
+    kern = hb.last_kernel()
+    if h in ("ell", "linf") and n > 128:
+        assert not kern.startswith("hopf_diag_tmg"), kern
+    else:
+        assert kern.startswith("hopf_diag_tmg_kernel"), kern
+    o = oracle.eval_diag(X, t, D, c, -0.5, h, w, lam=lam)
+    check(*g, *o)
+
+
+@pytest.mark.parametrize("n,K", [(32, 5), (44, 9), (48, 3), (64, 16), (56, 24)])
+def test_tmu_every_instance(hb, n, K):
+    """K4g (union, l2) at its widths 4x{8, 12, 16}: phi, grad, y, k*, phi_k against the oracle,
+    with t == 0 and an invalid point; and its distance mode against the oracle's Newton."""
+    rng = np.random.default_rng(n * 11 + K)
+    Ck = (rng.standard_normal((K, n)) * 2.0).astype(np.float32)
+    a = rng.uniform(0.5, 2.0, (K, n))
+    Dk = (a * a).astype(np.float32)
+    gk = rng.uniform(-0.7, -0.3, K).astype(np.float32)
+    M = 230
+    X = (rng.standard_normal((M, n)) * 2.5).astype(np.float32)
+    t = rng.uniform(0, 2, M).astype(np.float32)
+    t[0] = 0.0
+    X[3, 1] = np.inf
+    phi, grad, it, Y, ks, pk = hb.eval_union(dev(X), dev(t), dev(Dk), dev(Ck), dev(gk), "l2",
+                                             want_phik=True)
+    assert hb.last_kernel() == "hopf_union_tmg_kernel<l2>", hb.last_kernel()
+    o = oracle.eval_union(X, t, Dk, Ck, gk, "l2")
+    check_union(phi, grad, it, Y, ks, pk, o, t)
+    Yq = X[:60].copy()
+    Yq[5] = Ck[1] + 0.01          # inside a set: distance 0, projection = the query
+    g = hb.distance_union(dev(Yq), dev(Dk), dev(Ck), dev(gk))
+    assert hb.last_kernel() == "hopf_union_tmg_kernel<l2, distance>", hb.last_kernel()
+    od = oracle.distance_union(Yq, Dk, Ck, gk)
+    check_distance(g, od, Yq, Dk, Ck, gk)
