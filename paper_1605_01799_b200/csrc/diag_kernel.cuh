@@ -660,6 +660,15 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
       for (;;) {
         float mun = mu_e;
         if (act) mun = S2 > 0.f ? fmaxf(mu_e + __fdividef(S1 - tauS, S2), 0.f) : 0.f;
+        // empty active set at mu_e (a warm start above every |u_i|): step to the root of the top
+        // piece, max |u| - tau, at or left of the root, instead of falling back to 0
+        if (__any_sync(0xffffffffu, act && S2 == 0.f)) {
+          float um = 0.f;
+#pragma unroll
+          for (int q = 0; q < NP; q++) um = fmaxf(um, fmaxf(fabsf(b[q].x), fabsf(b[q].y)));
+          um = group_max<G>(um);
+          if (act && S2 == 0.f) mun = fmaxf(um - tauS, 0.f);
+        }
         bool cross = false;
 #pragma unroll
         for (int q = 0; q < NP; q++) {

@@ -69,6 +69,18 @@ __device__ __forceinline__ float active_set_root(const float (&z)[CPL], float a,
       const float F = fmaf(a, sa, -fmaf(c, me, e));
       mn = den > 0.f ? fmaxf(me + __fdividef(F, den), 0.f) : 0.f;
     }
+    // an evaluation point above every |z_i| (empty active set; the warm start can overshoot
+    // there when the root sits within a few ulps of max |z_i|, e.g. tiny t): the Newton step
+    // would fall to 0 and climb back through every breakpoint.  Step instead to the root of the
+    // top piece's extension, m = (a max|z| - e) / (a + c), which is at or left of the root
+    // (F is convex and decreasing), so the iteration proceeds monotonically from there
+    if (__any_sync(0xffffffffu, act && na == 0.f)) {
+      float zm = 0.f;
+#pragma unroll
+      for (int j = 0; j < CPL; j++) zm = fmaxf(zm, fabsf(z[j]));
+      zm = group_max<G>(zm);
+      if (act && na == 0.f) mn = fmaxf(__fdividef(fmaf(a, zm, -e), a + c), 0.f);
+    }
     bool cross = false;
 #pragma unroll
     for (int j = 0; j < CPL; j++) {

@@ -958,3 +958,22 @@ def test_tmu_every_instance(hb, n, K):
     assert hb.last_kernel() == "hopf_union_tmg_kernel<l2, distance>", hb.last_kernel()
     od = oracle.distance_union(Yq, Dk, Ck, gk)
     check_distance(g, od, Yq, Dk, Ck, gk)
+
+
+def test_normsq_tiny_t_linf_multiplier_regression(hb):
+    """Tiny t with H = l_inf (tools/fuzz_gpu.py case seed 79273243312: J = 1/2||.||_1^2, n = 48,
+    lambda = 0.5): the warm-started l1-ball multiplier can start above every |u_i| (empty active
+    set); its Newton step must then go to the top piece's root, not to 0 (which left the point
+    at max_iter with phi 44 % off).  All points against the oracle, plus t -> 0: phi -> J(x)."""
+    rng = np.random.default_rng(79273243312)
+    rng.choice(8); rng.choice(4); M = int(rng.integers(1, 400))
+    n = int(rng.integers(1, 65)); rng.choice(2); rng.choice(4)
+    X = rng.uniform(-10, 10, (M, n)).astype(np.float32)
+    t = rng.uniform(0, 10, M).astype(np.float32)
+    assert (M, n) == (195, 48) and abs(t[34] - 1.19e-5) < 1e-7
+    check_normsq(hb, X, t, "l1sq", "linf", lam=0.5)
+    t2 = np.full(64, 1e-5, np.float32)
+    for h in ("linf", "l1"):
+        g = hb.eval_normsq(dev(X[:64]), dev(t2), "l1sq", 0.0, h, lam=0.5)
+        J = 0.5 * np.abs(X[:64].astype(np.float64)).sum(axis=1) ** 2
+        assert np.max(np.abs(g[0].cpu().numpy() - J) / J) < 1e-4

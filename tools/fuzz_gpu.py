@@ -16,12 +16,16 @@ import paper_1605_01799_b200 as hb  # noqa: E402
 import test_gpu_parity as T  # noqa: E402
 
 
-def case(rng):
+def case(rng, force=None):
     kind = rng.choice(["diag", "diag", "union", "normsq", "ella", "dense", "distance", "maxh"])
+    if force:
+        kind = force
     lam = float(rng.choice([1.0, 1.0, 0.5, 2.0]))
     M = int(rng.integers(1, 400))
     if kind == "diag":
         n = int(rng.integers(1, 1025))
+        if rng.random() < 0.5:   # half the cases on 16-byte rows: the grouped TMEM kernels
+            n = 4 * int(rng.integers(7, 129))
         h = str(rng.choice(["l1", "wl1", "l2", "ell", "linf"]))
         D = rng.uniform(0.3, 3.0, n).astype(np.float32)
         c = rng.normal(size=n).astype(np.float32) if rng.random() < 0.5 else None
@@ -35,6 +39,8 @@ def case(rng):
         return f"diag n={n} M={M} h={h} lam={lam}"
     if kind == "union":
         n = int(rng.integers(1, 257))
+        if rng.random() < 0.5:   # the TMEM union kernel (l2, n = 25..64 on 16-byte rows)
+            n = 4 * int(rng.integers(7, 17))
         K = int(rng.integers(1, 17))
         h = str(rng.choice(["l1", "wl1", "l2"]))
         Ck = (rng.standard_normal((K, n)) * 2).astype(np.float32)
@@ -71,6 +77,8 @@ def case(rng):
         return f"dense n={n} M={M} h={h} lam={lam}"
     if kind == "distance":
         n = int(rng.integers(1, 129))
+        if rng.random() < 0.5:
+            n = 4 * int(rng.integers(7, 17))
         K = int(rng.integers(1, 9))
         Ck = (rng.standard_normal((K, n)) * 3).astype(np.float32)
         Dk = (rng.uniform(0.5, 2.0, (K, n)) ** 2).astype(np.float32)
@@ -82,6 +90,8 @@ def case(rng):
         return f"distance n={n} K={K} M={M}"
     if kind == "maxh":
         n = int(rng.integers(1, 300))
+        if rng.random() < 0.5:
+            n = 4 * int(rng.integers(7, 75))
         K = int(rng.integers(1, 4))
         kinds = [str(k) for k in rng.choice(["l1", "wl1", "l2", "ell", "linf"], K)]
         a = rng.uniform(0.5, 2.0, K).astype(np.float32)
@@ -122,10 +132,19 @@ def case(rng):
 
 if __name__ == "__main__":
     secs = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
-    rng = np.random.default_rng(int(time.time()) % 100000)
+    only = sys.argv[2] if len(sys.argv) > 2 else None      # replay: a case seed, or a kind
+    base = int(time.time()) % 100000
     t0, k = time.time(), 0
     while time.time() - t0 < secs:
-        desc = case(rng)
+        seed = int(only) if (only and only.isdigit()) else base * 1000003 + k
+        rng = np.random.default_rng(seed)   # one generator per case: a failure replays by seed
+        try:
+            desc = case(rng, only if (only and not only.isdigit()) else None)
+        except Exception:
+            print(f"FAILED case seed {seed}", flush=True)
+            raise
         k += 1
-        print("ok", desc, flush=True)
+        print("ok", desc, hb.last_kernel(), flush=True)
+        if only and only.isdigit():
+            break
     print(f"fuzz: {k} cases passed")
