@@ -964,7 +964,7 @@ def test_normsq_tiny_t_linf_multiplier_regression(hb):
     """Tiny t with H = l_inf (tools/fuzz_gpu.py case seed 79273243312: J = 1/2||.||_1^2, n = 48,
     lambda = 0.5): the warm-started l1-ball multiplier can start above every |u_i| (empty active
     set); its Newton step must then go to the top piece's root, not to 0 (which left the point
-    at max_iter with phi 44 % off).  All points against the oracle, plus t -> 0: phi -> J(x)."""
+    at max_iter with phi 44 % off).  All points against the oracle, and 64 points at t = 1e-5."""
     rng = np.random.default_rng(79273243312)
     rng.choice(8); rng.choice(4); M = int(rng.integers(1, 400))
     n = int(rng.integers(1, 65)); rng.choice(2); rng.choice(4)
@@ -974,6 +974,4 @@ def test_normsq_tiny_t_linf_multiplier_regression(hb):
     check_normsq(hb, X, t, "l1sq", "linf", lam=0.5)
     t2 = np.full(64, 1e-5, np.float32)
     for h in ("linf", "l1"):
-        g = hb.eval_normsq(dev(X[:64]), dev(t2), "l1sq", 0.0, h, lam=0.5)
-        J = 0.5 * np.abs(X[:64].astype(np.float64)).sum(axis=1) ** 2
-        assert np.max(np.abs(g[0].cpu().numpy() - J) / J) < 1e-4
+        check_normsq(hb, X[:64], t2, "l1sq", h, lam=0.5, max_iter=5000)
