@@ -133,15 +133,17 @@ def case(rng, force=None):
 if __name__ == "__main__":
     secs = float(sys.argv[1]) if len(sys.argv) > 1 else 60.0
     only = sys.argv[2] if len(sys.argv) > 2 else None      # replay: a case seed, or a kind
+    kind_arg = sys.argv[3] if len(sys.argv) > 3 else None  # with a seed: the kind that was forced
     base = int(time.time()) % 100000
     t0, k = time.time(), 0
     while time.time() - t0 < secs:
         seed = int(only) if (only and only.isdigit()) else base * 1000003 + k
         rng = np.random.default_rng(seed)   # one generator per case: a failure replays by seed
         try:
-            desc = case(rng, only if (only and not only.isdigit()) else None)
+            desc = case(rng, only if (only and not only.isdigit()) else kind_arg)
         except Exception:
-            print(f"FAILED case seed {seed}", flush=True)
+            print(f"FAILED case seed {seed} (replay: python tools/fuzz_gpu.py 1 {seed}"
+                  f"{' ' + only if only and not only.isdigit() else ''})", flush=True)
             raise
         k += 1
         print("ok", desc, hb.last_kernel(), flush=True)
