@@ -242,10 +242,18 @@ def main():
     import paper_1605_01799_b200 as hb
 
     ws, rank, local = dist_env()
+    if os.environ.get("HOPF_BENCH_BACKEND", "nccl") != "nccl":
+        local = local % torch.cuda.device_count()   # the gloo test: ranks may share a GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # HOPF_BENCH_BACKEND=gloo: a test of the multi-rank code paths with several ranks on one GPU
+        # (NCCL refuses two ranks on one device); the timed numbers of such a run mean nothing
+        backend = os.environ.get("HOPF_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     L = hb.lib()
 
     # ---- inputs: this rank's shard of the global points (generated by global index) ----------

@@ -31,6 +31,11 @@ def gather_results(tensors, group=None, dst_all=True):
     rank 0 gets the data and other ranks get None)."""
     import torch
     import torch.distributed as dist
+    if dist.get_backend(group) == "gloo" and tensors[0].is_cuda:
+        # gloo gathers host tensors: round-trip through the host (tests, CPU fallbacks of the
+        # process group; the GPU path is NCCL)
+        out = gather_results([t.cpu() for t in tensors], group, dst_all)
+        return [None if o is None else o.to(tensors[0].device) for o in out]
     world = dist.get_world_size(group)
     dev = tensors[0].device
     n_local = torch.tensor([tensors[0].shape[0]], device=dev, dtype=torch.int64)
@@ -67,6 +72,7 @@ def eval_gather_pipelined(eval_chunk, n_local, chunk, outs_full, group=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    host = dist.get_backend(group) == "gloo"   # gloo gathers host copies
     pending = []
 
     def land(item):
@@ -75,15 +81,16 @@ def eval_gather_pipelined(eval_chunk, n_local, chunk, outs_full, group=None):
             w.wait()
         for full, buf in zip(outs_full, bufs):
             full.view((world, n_local) + tuple(full.shape[1:]))[:, lo:hi] = \
-                buf.view((world, hi - lo) + tuple(buf.shape[1:]))
+                buf.view((world, hi - lo) + tuple(buf.shape[1:])).to(full.device)
 
     for lo in range(0, n_local, chunk):
         hi = min(n_local, lo + chunk)
         res = eval_chunk(lo, hi)
         works, bufs = [], []
         for t in res:
-            buf = torch.empty((world * (hi - lo),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-            works.append(dist.all_gather_into_tensor(buf, t.contiguous(), group=group, async_op=True))
+            src = t.cpu() if host else t.contiguous()
+            buf = torch.empty((world * (hi - lo),) + tuple(t.shape[1:]), dtype=t.dtype, device=src.device)
+            works.append(dist.all_gather_into_tensor(buf, src.contiguous(), group=group, async_op=True))
             bufs.append(buf)
         pending.append((lo, hi, works, bufs))
         if len(pending) > 1:
