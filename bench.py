@@ -555,6 +555,9 @@ def main():
                 "algorithmic_flops_per_launch": flops,
                 "executed_tensor_flops_per_launch": 3 * flops if tc else None,
                 "executed_frac": 3 * achieved / peak if tc else None,
+                # the target's own metric, from the committed ncu capture of this build
+                "tensor_pipe_active_frac_ncu": (load_traffic("_tensor_pipe_active_pct") or {}).get(wl.name, 0) / 100
+                if tc else None,
                 "mean_iters": float(conv.mean()) if conv.size else None}
     cpu = None
     if not args.no_cpu_baseline and ws == 1:

@@ -176,12 +176,12 @@ __host__ __device__ constexpr size_t smem_bytes() {
 #define HOPF_TMG_WAIT8 8  // finalize when this many eighths of the warp's groups wait
 #endif                    // (C2, 8 groups: 2 -> 1.65 ms, 4 -> 1.54, 5 -> 1.66, 6 -> 1.50, 7 -> 1.38, 8 -> 1.26)
 
-// bulk = the rows of X and grad are 16-byte aligned (n % 4 == 0, aligned bases): x of a group's
-// next point is prefetched into shared memory by a bulk copy one point ahead, and grad leaves
-// through a shared buffer by a bulk store; otherwise plain strided loads / stores.
+// The rows of X and grad must be 16-byte aligned (n % 4 == 0, aligned bases; the dispatcher in
+// tmg_api.cu checks): x of a group's next point is prefetched into shared memory by a bulk copy
+// one point ahead, and grad leaves through a shared buffer by a bulk store.
 template <int G, int CPL, int HK, bool BULK>
 __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagParams p) {
-  constexpr bool bulk = BULK;
+  static_assert(BULK, "instantiated with bulk row copies only (unaligned rows use the register kernel)");
   static_assert(G >= 2 && G <= 16 && (G & (G - 1)) == 0, "G in {2, 4, 8, 16}");
   static_assert(CPL % 2 == 0 && CPL <= 32 && (CPL % 8 == 0 || CPL % 8 == 2 || CPL % 8 == 4),
                 "CPL = 8 a + {0, 2, 4}, at most 32");
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
     A_s[i] = make_float4(1.f / (Dv + lam), wv, cv, 0.f);
     B_s[i] = make_float4(Dv + lam, wv, -0.5f * Dv, 1.f / Dv);
   }
-  if (bulk && gl == 0) mbar_init(my_bar, 1);
+  if (gl == 0) mbar_init(my_bar, 1);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  :: "r"((uint32_t)__cvta_generic_to_shared(&tmem_slot)), "r"(TMEM_COLS));
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   float mu = 0.f;         // ELL / LINF: multiplier of the last projection (warm start of the next)
 #pragma unroll
   for (int q = 0; q < NP; q++) d[q] = b[q] = splat2(0.f);
-  if (bulk && gl == 0 && have) bulk_load(smem_u32(xbuf + grp * PITCH), p.X + pt * (int64_t)n, row_bytes, my_bar);
+  if (gl == 0 && have) bulk_load(smem_u32(xbuf + grp * PITCH), p.X + pt * (int64_t)n, row_bytes, my_bar);
 
   // ---- start the point pt of the groups with `fresh` set (collective: every lane executes the
   // TMEM chunk traffic; other lanes write back what they read).  Setup: x_hat = (x - c)/(D + lambda),
@@ -294,33 +294,22 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       bad = !(tt >= 0.f) || !finite_f(tt);
       const int64_t nx = pt + ngroups;
       tpre = nx < M ? __ldg(p.t + nx) : 0.f;
-      if (bulk) {
-        mbar_wait(my_bar, xph);
-        xph ^= 1u;
+      mbar_wait(my_bar, xph);
+      xph ^= 1u;
 #pragma unroll
-        for (int q = 0; q < NP; q++) {   // x from the prefetched row (padding slots read 0 below)
-          const int j0 = 2 * q, j1 = 2 * q + 1;
-          d[q] = make_float2(j0 < jmax ? my_x[G * j0] : 0.f, j1 < jmax ? my_x[G * j1] : 0.f);
-        }
-      } else {
-        const float *xrow = p.X + pt * (int64_t)n + gl;
-#pragma unroll
-        for (int q = 0; q < NP; q++) {   // x into d (all loads in flight together)
-          const int j0 = 2 * q, j1 = 2 * q + 1;
-          d[q] = make_float2(j0 < jmax ? __ldg(xrow + G * j0) : 0.f, j1 < jmax ? __ldg(xrow + G * j1) : 0.f);
-        }
+      for (int q = 0; q < NP; q++) {   // x from the prefetched row (padding slots read 0 below)
+        const int j0 = 2 * q, j1 = 2 * q + 1;
+        d[q] = make_float2(j0 < jmax ? my_x[G * j0] : 0.f, j1 < jmax ? my_x[G * j1] : 0.f);
       }
       float2 fin = splat2(0.f);   // x * 0 accumulates NaN iff some x is NaN or infinite
 #pragma unroll
       for (int q = 0; q < NP; q++) fin = fma2(d[q], splat2(0.f), fin);
       bad |= !(fin.x == 0.f && fin.y == 0.f);
     }
-    if (bulk) {
-      // the group's row has been read: its leader prefetches the following point's x into it
-      __syncwarp();
-      if (fresh && gl == 0 && pt + ngroups < M)
-        bulk_load(smem_u32(xbuf + grp * PITCH), p.X + (pt + ngroups) * (int64_t)n, row_bytes, my_bar);
-    }
+    // the group's row has been read: its leader prefetches the following point's x into it
+    __syncwarp();
+    if (fresh && gl == 0 && pt + ngroups < M)
+      bulk_load(smem_u32(xbuf + grp * PITCH), p.X + (pt + ngroups) * (int64_t)n, row_bytes, my_bar);
     const float tl = tt / lam;
     // the chunk stores are warp-collective: lanes that keep their point write back what they
     // read; when every lane starts a point or has none left (the lockstep case), nothing is read
@@ -382,10 +371,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   // invalid point): the group then keeps iterating harmlessly until the warp finalizes, so the
   // trip needs no per-slot select to freeze d.  Collective; `stop` marks the stopping groups.
   auto stash = [&](bool stop) {
-    if (bulk) {   // the group's previous grad row has left the buffer
-      if (stop && gl == 0) bulk_wait_read();
-      __syncwarp();
-    }
+    if (stop && gl == 0) bulk_wait_read();   // the group's previous grad row has left the buffer
+    __syncwarp();
     if (stop) {
 #pragma unroll
       for (int q = 0; q < NP; q++) {
@@ -780,14 +767,11 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
         else if (LINF) hs = fmaxf(hs, fabsf(dq));
         else if (WL1) hs = fmaf(B.y, fabsf(dq), hs);
         else hs += fabsf(dq);
-        if (!bulk && done && j < jmax) grow[G * j] = dq;
       }
     });
-    if (bulk) {
-      fence_proxy_async();
-      __syncwarp();
-      if (done && gl == 0) bulk_store(grow - gl, smem_u32(gbuf + grp * PITCH), row_bytes);
-    }
+    fence_proxy_async();
+    __syncwarp();
+    if (done && gl == 0) bulk_store(grow - gl, smem_u32(gbuf + grp * PITCH), row_bytes);
     const float qs = group_sum<G>(qs0 + qs1);
     const float hsum = LINF ? group_max<G>(fmaxf(hs0, hs1)) : group_sum<G>(hs0 + hs1);
     if (done && gl == 0) {
@@ -810,7 +794,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
     refill(done && have);
     any_have = __any_sync(0xffffffffu, have);
   }
-  if (bulk && gl == 0) bulk_wait_all();
+  if (gl == 0) bulk_wait_all();
   if (p.iter_total && gl == 0 && my_iters) atomicAdd(p.iter_total, (unsigned long long)my_iters);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
