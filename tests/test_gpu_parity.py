@@ -933,9 +933,10 @@ def test_tmg_every_instance(hb, n, h):
     check(*g, *o)
 
 
-@pytest.mark.parametrize("n,K", [(32, 5), (44, 9), (48, 3), (64, 16), (56, 24)])
+@pytest.mark.parametrize("n,K", [(32, 5), (44, 9), (48, 3), (64, 16), (56, 24), (100, 8), (128, 4),
+                                 (200, 3), (256, 2)])
 def test_tmu_every_instance(hb, n, K):
-    """K4g (union, l2) at its widths 4x{8, 12, 16}: phi, grad, y, k*, phi_k against the oracle,
+    """K4g (union, l2) at its widths 4x{8, 12, 16}, 8x16, 16x16: phi, grad, y, k*, phi_k against the oracle,
     with t == 0 and an invalid point; and its distance mode against the oracle's Newton."""
     rng = np.random.default_rng(n * 11 + K)
     Ck = (rng.standard_normal((K, n)) * 2.0).astype(np.float32)
