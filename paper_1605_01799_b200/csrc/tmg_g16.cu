@@ -1,12 +1,12 @@
-// tmg_g16.cu — instances of the grouped TMEM kernel (diag_tmg.cuh) with 16 lanes per point.
+// tmg_g16.cu — instances of the grouped TMEM kernel (diag_tmg.cuh) with 16 lanes per point, every H kind.
 #include "diag_tmg.cuh"
 #include "tmg_api.h"
 
 namespace hopf {
 extern const TmgVariant kTmgG16[] = {
-    {16, 20, {dtg::hopf_diag_tmg_kernel<16, 20, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_L2, true>, nullptr, nullptr}},
-    {16, 24, {dtg::hopf_diag_tmg_kernel<16, 24, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_L2, true>, nullptr, nullptr}},
-    {16, 28, {dtg::hopf_diag_tmg_kernel<16, 28, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_L2, true>, nullptr, nullptr}},
-    {16, 32, {dtg::hopf_diag_tmg_kernel<16, 32, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_L2, true>, nullptr, nullptr}}};
+    {16, 20, {dtg::hopf_diag_tmg_kernel<16, 20, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_L2, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_ELL, true>, dtg::hopf_diag_tmg_kernel<16, 20, HK_LINF, true>}},
+    {16, 24, {dtg::hopf_diag_tmg_kernel<16, 24, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_L2, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_ELL, true>, dtg::hopf_diag_tmg_kernel<16, 24, HK_LINF, true>}},
+    {16, 28, {dtg::hopf_diag_tmg_kernel<16, 28, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_L2, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_ELL, true>, dtg::hopf_diag_tmg_kernel<16, 28, HK_LINF, true>}},
+    {16, 32, {dtg::hopf_diag_tmg_kernel<16, 32, HK_L1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_WL1, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_L2, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_ELL, true>, dtg::hopf_diag_tmg_kernel<16, 32, HK_LINF, true>}}};
 extern const int kTmgG16Count = 4;
 }  // namespace hopf

@@ -1,4 +1,4 @@
-// tmg_g4.cu — instances of the grouped TMEM kernel (diag_tmg.cuh) with 4 lanes per point (H = ellipsoidal norm and l_inf too).
+// tmg_g4.cu — instances of the grouped TMEM kernel (diag_tmg.cuh) with 4 lanes per point, every H kind.
 #include "diag_tmg.cuh"
 #include "tmg_api.h"
 
