@@ -70,6 +70,8 @@ struct DiagParams {
   float tscale = 1.f;
   int max_newton = 0;
   float stol = 0.f;
+  // K1g / K4g: the launch's point counter (zeroed before the launch; points claimed per warp)
+  unsigned long long *claim = nullptr;
 };
 
 template <int G>

@@ -172,15 +172,14 @@ __host__ __device__ constexpr size_t smem_bytes() {
          (size_t)(THREADS / G) * 8;
 }
 
-#ifndef HOPF_TMG_WAIT8
-#define HOPF_TMG_WAIT8 8  // finalize when this many eighths of the warp's groups wait
-#endif                    // (C2, 8 groups: 2 -> 1.65 ms, 4 -> 1.54, 5 -> 1.66, 6 -> 1.50, 7 -> 1.38, 8 -> 1.26)
-
 // The rows of X and grad must be 16-byte aligned (n % 4 == 0, aligned bases; the dispatcher in
 // tmg_api.cu checks): x of a group's next point is prefetched into shared memory by a bulk copy
 // one point ahead, and grad leaves through a shared buffer by a bulk store.
 template <int G, int CPL, int HK, bool BULK>
-__global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagParams p) {
+#ifndef HOPF_TMG_MINB
+#define HOPF_TMG_MINB 4
+#endif
+__global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(const DiagParams p) {
   static_assert(BULK, "instantiated with bulk row copies only (unaligned rows use the register kernel)");
   static_assert(G >= 2 && G <= 16 && (G & (G - 1)) == 0, "G in {2, 4, 8, 16}");
   static_assert(CPL % 2 == 0 && CPL <= 32 && (CPL % 8 == 0 || CPL % 8 == 2 || CPL % 8 == 4),
@@ -190,7 +189,6 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   constexpr int NP = CPL / 2;
   constexpr int GPW = 32 / G, GPB = THREADS / G;
   constexpr int PITCH = row_pitch(G * CPL, G);
-  constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMG_WAIT8 / 8) > 0 ? (GPW * HOPF_TMG_WAIT8 / 8) : 1;
   constexpr bool L2 = HK == HK_L2, WL1 = HK == HK_WL1, ELL = HK == HK_ELL, LINF = HK == HK_LINF;
   constexpr bool WTAB = WL1 || ELL;   // per-coordinate weights in the tables
   extern __shared__ __align__(16) uint8_t dyn_smem[];
@@ -267,7 +265,12 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
   }
 
   float2 d[NP], b[NP];
+  // points: generations 0 and 1 static (gid, gid + ngroups), later ones claimed by the warp from
+  // p.claim one generation ahead (GPW consecutive points, one per group), so warps that drew
+  // cheap points take more of them and the launch ends within about one generation
   int64_t pt = gid;
+  int64_t pnext = gid + ngroups;
+  unsigned long long wclaim = 0;   // lane 0: the claim made at the last refill
   bool have = pt < M;
   bool waiting = false;   // the solve stopped; d frozen until the warp finalizes
   int wstatus = 0;
@@ -292,8 +295,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
     if (fresh) {
       tt = p.tscale * tpre;
       bad = !(tt >= 0.f) || !finite_f(tt);
-      const int64_t nx = pt + ngroups;
-      tpre = nx < M ? __ldg(p.t + nx) : 0.f;
+      tpre = pnext < M ? __ldg(p.t + pnext) : 0.f;
       mbar_wait(my_bar, xph);
       xph ^= 1u;
 #pragma unroll
@@ -308,8 +310,11 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
     }
     // the group's row has been read: its leader prefetches the following point's x into it
     __syncwarp();
-    if (fresh && gl == 0 && pt + ngroups < M)
-      bulk_load(smem_u32(xbuf + grp * PITCH), p.X + (pt + ngroups) * (int64_t)n, row_bytes, my_bar);
+    if (fresh && gl == 0 && pnext < M)
+      bulk_load(smem_u32(xbuf + grp * PITCH), p.X + pnext * (int64_t)n, row_bytes, my_bar);
+    // the generation after next (consumed at the next finalize: the atomic's latency is hidden)
+    const bool any_fresh = __any_sync(0xffffffffu, fresh);
+    if (lane == 0 && any_fresh) wclaim = atomicAdd(p.claim, (unsigned long long)GPW);
     const float tl = tt / lam;
     // the chunk stores are warp-collective: lanes that keep their point write back what they
     // read; when every lane starts a point or has none left (the lockstep case), nothing is read
@@ -646,9 +651,31 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       }
       stash(stop);
     } else {
-    if (full_test) trip(std::true_type{});
-    else trip(std::false_type{});
-    asm volatile("tcgen05.wait::st.sync.aligned;");
+    constexpr unsigned LEADERS = G == 2 ? 0x55555555u : G == 4 ? 0x11111111u : G == 8 ? 0x01010101u : 0x00010001u;
+    unsigned ev = 0;
+    if constexpr (L2) {
+      if (full_test) trip(std::true_type{});
+      else trip(std::false_type{});
+      asm volatile("tcgen05.wait::st.sync.aligned;");
+    } else {
+      // l1 / wl1: trips until some group may stop.  Exact prefilter: a group total <= tol needs
+      // every lane's (non-negative) partial <= tol; t == 0 / invalid points (lim = 0) and
+      // max_iter are forced events.  Two trips per pass of the loop.
+      auto fast = [&]() -> bool {
+        a0 = c0 = splat2(0.f);
+        trip(std::false_type{});
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+        it += live ? 1 : 0;
+        const float psd = a0.x + a0.y, psv = c0.x + c0.y;
+        const bool lane_ev = live && ((psd <= tol && psv <= tol) || it >= lim);
+        ev = __ballot_sync(0xffffffffu, lane_ev);
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) ev &= ev >> o;   // bit base of a group: all G lanes set
+        return (ev & LEADERS) != 0u;
+      };
+      while (!fast() && !fast()) {
+      }
+    }
 
     if constexpr (L2) {
       const float psd = a0.x + a0.y, psb = b0.x + b0.y, psv = c0.x + c0.y, pr2 = r0.x + r0.y;
@@ -671,17 +698,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       }
       stash(stop);
     } else {
-      it += live ? 1 : 0;
       kdone = it;
-      // exact prefilter: a group total <= tol needs every lane's (non-negative) partial <= tol;
-      // t == 0 / invalid points (lim = 0) and max_iter are forced events
       const float psd = a0.x + a0.y, psv = c0.x + c0.y;
-      const bool lane_ev = live && ((psd <= tol && psv <= tol) || kdone >= lim);
-      unsigned ev = __ballot_sync(0xffffffffu, lane_ev);
-#pragma unroll
-      for (int o = 1; o < G; o <<= 1) ev &= ev >> o;   // bit base of a group: all G lanes set
-      constexpr unsigned LEADERS = G == 2 ? 0x55555555u : G == 4 ? 0x11111111u : G == 8 ? 0x01010101u : 0x00010001u;
-      if ((ev & LEADERS) == 0u) continue;   // the common trip: no group can stop
       const bool cand = (ev >> base) & 1u;
       bool ok_sd, ok_sv;
       group_test2<G>(psd, psv, tol, ok_sd, ok_sv);
@@ -720,7 +738,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       const int nwait = __popc(__ballot_sync(0xffffffffu, waiting && gbit));
       if (nwait == 0) continue;
       const int nhave = __popc(__ballot_sync(0xffffffffu, have && gbit));
-      if (nwait < WAIT_THRESHOLD && nwait < nhave) continue;
+      if (nwait < nhave) continue;   // lockstep generations: finalize when every group waits
+                                     // (C2: half the groups 1.65 ms, three quarters 1.50, all 1.26)
     }
 
     // ============ finalize the waiting groups (all lanes compute, waiting groups store) ========
@@ -781,8 +800,10 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tmg_kernel(const DiagPar
       p.iters[pt] = wstatus;
     }
     // ---- refill: the next point of each finalized group --------------------------------------
+    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * ngroups + (lane / G);
     if (done) {
-      pt += ngroups;
+      pt = pnext;
+      pnext = claimed;
       have = pt < M;
       if (!have) {
         waiting = false;

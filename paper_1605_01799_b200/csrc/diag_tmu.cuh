@@ -113,7 +113,11 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   auto grow_s = [&](int s) { return xrow0 + (2 + s) * PITCH; };
 
   float2 d[NP], b[NP];   // -d, pending u (l2 storage of the trip)
-  int64_t pt = gid;
+  // points: the first three of a group static (gid + r ngroups, r < 3), later ones claimed by
+  // the group from p.claim one point ahead (the atomic's latency is hidden by a whole point), so
+  // groups that drew cheap points take more of them and the launch ends within about one point
+  int64_t pt = gid, p1 = gid + ngroups, p2 = gid + 2 * ngroups;
+  unsigned long long gclaim = 0;   // group lane 0: the claim made at the last point start
   bool have = pt < M;
   bool waiting = false;
   int wstatus = 0, it = 0, lim = 0, spec = 0, kset = 0;
@@ -134,8 +138,8 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   for (int q = 0; q < NP; q++) d[q] = b[q] = splat2(0.f);
   if (gl == 0 && have) {
     dtg::bulk_load(dtg::smem_u32(xrow(0)), p.X + pt * (int64_t)n, row_bytes, dtg::smem_u32(bars));
-    if (pt + ngroups < M)
-      dtg::bulk_load(dtg::smem_u32(xrow(1)), p.X + (pt + ngroups) * (int64_t)n, row_bytes, dtg::smem_u32(bars + 1));
+    if (p1 < M)
+      dtg::bulk_load(dtg::smem_u32(xrow(1)), p.X + p1 * (int64_t)n, row_bytes, dtg::smem_u32(bars + 1));
   }
 
   // ---- set k of the current point for the groups with `fresh` (collective): x_hat = (x - c_k) /
@@ -192,8 +196,8 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
     if (fresh) {
       tt = DIST ? 0.f : tpre;   // distance mode starts at s_0 = 0 (R24)
       bad = !(tt >= 0.f) || !finite_f(tt);
-      const int64_t nx = pt + ngroups;
-      tpre = (nx < M && !DIST) ? __ldg(p.t + nx) : 0.f;
+      tpre = (p1 < M && !DIST) ? __ldg(p.t + p1) : 0.f;
+      if (gl == 0) gclaim = atomicAdd(p.claim, 1ull);
       nn = 0;
       dtg::mbar_wait(dtg::smem_u32(bars + xs), (xph >> xs) & 1u);
       xph ^= 1u << xs;
@@ -430,10 +434,9 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
         dtg::bulk_store(p.grad + pt * (int64_t)n, dtg::smem_u32(br - gl), row_bytes);
         if (p.Y) dtg::bulk_store(p.Y + pt * (int64_t)n, dtg::smem_u32(yr - gl), row_bytes);
         // the x row is free once y has left it: the point after the next one goes there
-        const int64_t nn2 = pt + 2 * ngroups;
-        if (nn2 < M) {
+        if (p2 < M) {
           dtg::bulk_wait_read();
-          dtg::bulk_load(dtg::smem_u32(yr - gl), p.X + nn2 * (int64_t)n, row_bytes, dtg::smem_u32(bars + xs));
+          dtg::bulk_load(dtg::smem_u32(yr - gl), p.X + p2 * (int64_t)n, row_bytes, dtg::smem_u32(bars + xs));
         }
       }
     }
@@ -447,8 +450,11 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
       bestit = 0;
       bgn = 0.f;
     }
+    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, gclaim, lane & ~(G - 1)) + 3 * ngroups;
     if (point_done) {
-      pt += ngroups;
+      pt = p1;
+      p1 = p2;
+      p2 = claimed;
       have = pt < M;
       xs ^= 1;
       if (!have) {

@@ -95,7 +95,12 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
     const int64_t need = (p.M + per_block - 1) / per_block;
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
-    fn<<<(unsigned)blocks, dtg::THREADS, dtg::DYN_SMEM, stream>>>(p);
+    DiagParams q = p;
+    int rc = scratch_alloc((void **)&q.claim, sizeof(unsigned long long), stream);
+    if (rc != HOPF_OK) return rc;
+    cudaMemsetAsync(q.claim, 0, sizeof(unsigned long long), stream);
+    fn<<<(unsigned)blocks, dtg::THREADS, dtg::DYN_SMEM, stream>>>(q);
+    scratch_free(q.claim, stream);
     *handled = true;
     g_launches += 1;
     g_last_threads = dtg::THREADS;
@@ -119,7 +124,12 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   const int64_t need = (p.M + per_block - 1) / per_block;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  v->fn<<<(unsigned)blocks, dtu::THREADS, dtu::DYN_SMEM, stream>>>(p);
+  DiagParams q = p;
+  int rc = scratch_alloc((void **)&q.claim, sizeof(unsigned long long), stream);
+  if (rc != HOPF_OK) return rc;
+  cudaMemsetAsync(q.claim, 0, sizeof(unsigned long long), stream);
+  v->fn<<<(unsigned)blocks, dtu::THREADS, dtu::DYN_SMEM, stream>>>(q);
+  scratch_free(q.claim, stream);
   *handled = true;
   g_launches += 1;
   g_last_threads = dtu::THREADS;
