@@ -157,7 +157,11 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   }
 
   float2 d[NP], b[NP];
-  int64_t pt = gid;
+  // points: the first two of a warp static (gid, gid + ngroups), later ones claimed from p.claim
+  // one point ahead, so warps that drew cheap points take more and the launch ends within
+  // about one point
+  int64_t pt = gid, pnext = gid + ngroups;
+  unsigned long long wclaim = 0;   // lane 0: the claim made at the last point start
   bool have = pt < p.M;
   int it = 0;
   float tt = 0.f, tauS = 0.f;
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     if (active) {
       tt = p.tscale * __ldg(p.t + pt);
       bad = !(tt >= 0.f) || !finite_f(tt);
+      if (lane == 0) wclaim = atomicAdd(p.claim, 1ull);
     }
     const float *xrow = p.X + (active ? pt : 0) * (int64_t)n;
 #pragma unroll
@@ -390,7 +395,9 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     float phiv = (spec == 1) ? qs + p.gamma : qs - tt * (HK == HK_L2 ? sqrtf(hsum) : hsum) + p.gamma;
     if (spec == 2) phiv = __int_as_float(0x7fc00000);
     if (gl == 0) { p.phi[pt] = phiv; p.iters[pt] = wstatus; }
-    pt += ngroups;
+    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * ngroups;
+    pt = pnext;
+    pnext = claimed;
     have = pt < p.M;
     if (have) start_point(true);
   }

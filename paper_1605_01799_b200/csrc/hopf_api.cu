@@ -185,7 +185,12 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
   const int64_t need = (p.M + 3) / 4;   // 4 points (warps) per block
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  fn<<<(unsigned)blocks, THREADS, DYN_SMEM, stream>>>(p);
+  DiagParams q = p;
+  int rc = scratch_alloc((void **)&q.claim, sizeof(unsigned long long), stream);
+  if (rc != HOPF_OK) return rc;
+  cudaMemsetAsync(q.claim, 0, sizeof(unsigned long long), stream);
+  fn<<<(unsigned)blocks, THREADS, DYN_SMEM, stream>>>(q);
+  scratch_free(q.claim, stream);
   g_launches += 1;
   g_last_threads = THREADS;
   g_last_blocks = (int)blocks;
