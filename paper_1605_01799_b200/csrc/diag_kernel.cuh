@@ -74,6 +74,25 @@ struct DiagParams {
   unsigned long long *claim = nullptr;
 };
 
+// Dynamic point claims (one atomic on the launch's counter per claim).  `zero_lanes` is a shared
+// array of zeros written at kernel start; reading it at a lane-dependent address outside the
+// claiming lane's branch keeps the counter address non-uniform in the compiler's view, so a
+// single lane's atomic is not turned into a warp-aggregated one whose result is shuffled at
+// once (that would expose the atomic's latency; here the result is consumed one point later).
+__device__ __forceinline__ void zero_lanes_init(unsigned *zero_lanes) {
+  if (threadIdx.x < 32) {
+    unsigned z;
+    asm volatile("mov.u32 %0, 0;" : "=r"(z));
+    zero_lanes[threadIdx.x] = z;
+  }
+}
+__device__ __forceinline__ unsigned lane_zero(const unsigned *zero_lanes, int lane) {
+  unsigned z;
+  asm volatile("ld.shared.u32 %0, [%1];"
+               : "=r"(z) : "r"((uint32_t)__cvta_generic_to_shared(zero_lanes + lane)));
+  return z;
+}
+
 template <int G>
 __device__ __forceinline__ float group_sum(float v) {
 #pragma unroll

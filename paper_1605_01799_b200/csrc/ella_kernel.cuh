@@ -26,6 +26,7 @@ struct EllAParams {
   float *phi, *grad;
   int *iters;
   unsigned long long *iter_total;
+  unsigned long long *claim;   // the launch's point counter (zeroed before the launch)
 };
 
 constexpr int ELLA_WARPS = 4;
@@ -109,7 +110,23 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
 
   const int64_t nslots = (int64_t)gridDim.x * ELLA_WARPS * GPW;
   unsigned my_iters = 0;
-  for (int64_t base = ((int64_t)blockIdx.x * ELLA_WARPS + wib) * GPW; base < p.M; base += nslots) {
+  // batches of GPW points: the first two of a warp static, later ones claimed from p.claim one
+  // batch ahead (warps that drew cheap batches take more; the launch ends within one batch)
+  __shared__ unsigned zero_lanes[32];
+  zero_lanes_init(zero_lanes);
+  __syncthreads();
+  int64_t bnext = ((int64_t)blockIdx.x * ELLA_WARPS + wib) * GPW + nslots;
+  unsigned long long wclaim = 0;   // lane 0: the claim made at the current batch's start
+  auto next_batch = [&]() {
+    const int64_t nb = bnext;
+    bnext = (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * nslots;
+    return nb;
+  };
+  for (int64_t base = ((int64_t)blockIdx.x * ELLA_WARPS + wib) * GPW; base < p.M; base = next_batch()) {
+    {
+      const unsigned zoff = lane_zero(zero_lanes, lane);
+      if (lane == 0) wclaim = atomicAdd(p.claim + zoff, (unsigned long long)GPW);
+    }
     const int64_t pt = base + sub;
     const bool have = pt < p.M;
     const float tt = have ? __ldg(p.t + pt) : 1.f;

@@ -8,15 +8,11 @@
 #include <cstdlib>
 
 #include "../../include/hopf.h"
+#include "common.cuh"
 #include "normsq_kernel.cuh"
 
 namespace hopf {
-int set_error(int code, const char *fmt, ...);
-int check_launch(const char *what);
-int num_sms();
-extern thread_local int32_t g_launches;
 extern thread_local int32_t g_last_threads, g_last_blocks;
-extern thread_local const char *g_last_kernel;
 extern thread_local unsigned long long *g_iter_counter;
 
 using NormsqFn = void (*)(const NormsqParams);
@@ -78,7 +74,11 @@ extern "C" int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const floa
   const int64_t need = (M * v->G + threads - 1) / threads;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
+  int rc = scratch_alloc((void **)&p.claim, sizeof(unsigned long long), (cudaStream_t)stream);
+  if (rc != HOPF_OK) return rc;
+  cudaMemsetAsync(p.claim, 0, sizeof(unsigned long long), (cudaStream_t)stream);
   fn<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(p);
+  scratch_free(p.claim, (cudaStream_t)stream);
   g_launches = 1;
   g_last_threads = threads;
   g_last_blocks = (int)blocks;
@@ -134,7 +134,11 @@ extern "C" int hopf_eval_diag_A(int64_t M, int32_t n, const float *X, const floa
   int64_t blocks = (int64_t)num_sms() * per_sm;
   const int64_t need = (M + ELLA_WARPS * gpw - 1) / (ELLA_WARPS * gpw);
   if (blocks > need) blocks = need;
+  int rc = scratch_alloc((void **)&p.claim, sizeof(unsigned long long), (cudaStream_t)stream);
+  if (rc != HOPF_OK) return rc;
+  cudaMemsetAsync(p.claim, 0, sizeof(unsigned long long), (cudaStream_t)stream);
   fn<<<(unsigned)blocks, 32 * ELLA_WARPS, smem, (cudaStream_t)stream>>>(p);
+  scratch_free(p.claim, (cudaStream_t)stream);
   g_launches = 1;
   g_last_threads = 32 * ELLA_WARPS;
   g_last_blocks = (int)blocks;

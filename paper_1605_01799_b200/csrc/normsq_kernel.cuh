@@ -42,6 +42,7 @@ struct NormsqParams {
   float *phi, *grad;
   int *iters;
   unsigned long long *iter_total;
+  unsigned long long *claim;   // the launch's point counter (zeroed before the launch)
 };
 
 // Root m >= 0 of a S(m) - c m - e (see above) for the values |z_i| of this lane's CPL slots;
@@ -111,7 +112,14 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
   const int HKr = p.h;
 
   float x[CPL], d[CPL], b[CPL], v[CPL], wr[CPL];
-  int64_t pt = gid;
+  // points: the first two of a group static (gid, gid + ngroups), later ones claimed by the
+  // group from p.claim one point ahead.  Iteration counts vary widely here (Table 5: 30 to
+  // max_iter), so a static assignment leaves long tails of nearly idle warps.
+  __shared__ unsigned zero_lanes[32];
+  zero_lanes_init(zero_lanes);
+  __syncthreads();
+  int64_t pt = gid, pnext = gid + ngroups;
+  unsigned long long gclaim = 0;   // group lane 0: the claim made at the last point start
   bool have = pt < p.M;
   int it = 0, spec = 0;
   float tt = 0.f, tau = 0.f, beta = 0.f, mu = 0.f;
@@ -120,7 +128,9 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
 
   auto load = [&](bool active) {
     bool bad = false;
+    const unsigned zoff = lane_zero(zero_lanes, lane);
     if (active) {
+      if (gl == 0) gclaim = atomicAdd(p.claim + zoff, 1ull);
       tt = __ldg(p.t + pt);
       bad = !(tt >= 0.f) || !finite_f(tt);
       const float *xrow = p.X + pt * (int64_t)n;
@@ -249,6 +259,7 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
 #pragma unroll
     for (int j = 0; j < CPL; j++) cnt += (j < jmax && fabsf(x[j]) == mx) ? 1.f : 0.f;
     cnt = group_sum<G>(cnt);
+    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, gclaim, lane & ~(G - 1)) + 2 * ngroups;
     if (done) {
       float phiv, g[CPL];
       if (spec == 2) {
@@ -276,7 +287,8 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
 #pragma unroll
       for (int j = 0; j < CPL; j++)
         if (j < jmax) grow[gl + G * j] = g[j];
-      pt += ngroups;
+      pt = pnext;
+      pnext = claimed;
       have = pt < p.M;
     }
     load(done && have);   // collective
