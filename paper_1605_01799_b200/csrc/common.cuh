@@ -19,4 +19,11 @@ int num_sms();
 // never share scratch; the pool's event tracking orders reuse across streams.
 int scratch_alloc(void **ptr, size_t bytes, cudaStream_t stream);
 void scratch_free(void *ptr, cudaStream_t stream);
+// Dynamic point claims pay when each resident group (or warp batch) processes many points; for
+// short launches (about 3 points per group: the paper-protocol lines at n <= 16) the counter's
+// memset and the claims cost more than the balance gains (p4_id_l1 0.026 -> 0.039 ms), and the
+// kernels keep the static stride.  *ctr = a zeroed stream-ordered counter (free it with
+// scratch_free after the launch) or null; returns HOPF_OK or the allocation error.
+// HOPF_CLAIMS=1 / 0 forces the counter on / off (tests, A/B runs).
+int claim_counter(int64_t M, int64_t resident, cudaStream_t stream, unsigned long long **ctr);
 }  // namespace hopf

@@ -70,7 +70,7 @@ struct DiagParams {
   float tscale = 1.f;
   int max_newton = 0;
   float stol = 0.f;
-  // K1g / K4g: the launch's point counter (zeroed before the launch; points claimed per warp)
+  // the launch's point counter (zeroed before the launch); null: static point stride
   unsigned long long *claim = nullptr;
 };
 
@@ -359,7 +359,30 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
     for (int i = 0; i < n; i++) wmin = fminf(wmin, w_s[i]);
   }
 
-  int64_t pt = gid;
+  // points: the first two of a group static (gid, gid + ngroups); later ones claimed from
+  // p.claim, one claim per event for all groups that start a point (lane 0 adds their count; a
+  // group's index is base + its rank), resolved at the warp's next event and used at the
+  // group's next start, so the atomic's latency is off the critical path.  Not for a thread per
+  // point (G = 1: n <= 16, launches of about 3 points per thread, where the claims cost more
+  // than they balance: p16_id_l2 0.064 -> 0.076 ms); the host passes no counter there.
+  constexpr bool CLAIMS = G > 1;
+  __shared__ unsigned zero_lanes[CLAIMS ? 32 : 1];
+  if constexpr (CLAIMS) {
+    zero_lanes_init(zero_lanes);
+    __syncthreads();
+  }
+  int64_t pt = gid, pn = gid + ngroups, pc = 0;   // current, next, resolved claim
+  unsigned long long wclaim = 0;                 // lane 0: base of the last claim
+  bool pend = false;                             // this group's claim is not resolved yet
+  unsigned rk = 0;                               // its rank in that claim
+  const unsigned gbase = (unsigned)(lane & ~(G - 1));
+  auto claim = [&](bool start) {   // collective: the groups with `start` set claim one point each
+    if constexpr (!CLAIMS) return;
+    const unsigned cm = __ballot_sync(0xffffffffu, gl == 0 && start);
+    if (start) { pend = true; rk = __popc(cm & ((1u << gbase) - 1u)); }
+    const unsigned zoff = lane_zero(zero_lanes, lane);
+    if (lane == 0 && cm && p.claim) wclaim = atomicAdd(p.claim + zoff, (unsigned long long)__popc(cm));
+  };
   bool have = pt < p.M;
   bool waiting = false; // the current solve stopped; d is frozen until the warp finalizes
   int wstatus = 0;      // its status (iteration, 0, -max_iter or INT32_MIN)
@@ -467,6 +490,7 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
   };
 
   load_point(have);
+  claim(have);
   if (have) {
     setup_solve();
     if (UNION) { best = __int_as_float(0x7f800000); bestk = -1; bestit = 0; }
@@ -970,11 +994,17 @@ __global__ void __launch_bounds__(128, ((HK >= 3 || UNION) && CPL <= 16) ? 4 : 3
       }
     }
     // ---- refill: the next set of the point (union) or the next point of this group ---------
+    if constexpr (CLAIMS) {
+      const unsigned long long wb = __shfl_sync(0xffffffffu, wclaim, 0);   // the last claim's base
+      if (pend) { pc = (int64_t)wb + 2 * ngroups + rk; pend = false; }
+    }
     if (point_done) {
-      pt += ngroups;
+      pt = pn;
+      pn = (CLAIMS && p.claim) ? pc : pn + ngroups;   // no counter: static stride
       have = pt < p.M;
     }
     load_point(point_done && have);   // collective (ballot inside): all lanes call it
+    claim(point_done && have);
     if (done) {
       if (have) {
         kset = (point_done || restart) ? 0 : kset + 1;

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     if (active) {
       tt = p.tscale * __ldg(p.t + pt);
       bad = !(tt >= 0.f) || !finite_f(tt);
-      if (lane == 0) wclaim = atomicAdd(p.claim, 1ull);
+      if (lane == 0 && p.claim) wclaim = atomicAdd(p.claim, 1ull);
     }
     const float *xrow = p.X + (active ? pt : 0) * (int64_t)n;
 #pragma unroll
@@ -395,7 +395,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     float phiv = (spec == 1) ? qs + p.gamma : qs - tt * (HK == HK_L2 ? sqrtf(hsum) : hsum) + p.gamma;
     if (spec == 2) phiv = __int_as_float(0x7fc00000);
     if (gl == 0) { p.phi[pt] = phiv; p.iters[pt] = wstatus; }
-    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * ngroups;
+    const int64_t claimed = p.claim ? (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * ngroups
+                                    : pnext + ngroups;   // no counter: static stride
     pt = pnext;
     pnext = claimed;
     have = pt < p.M;

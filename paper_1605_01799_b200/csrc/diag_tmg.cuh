@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
       bulk_load(smem_u32(xbuf + grp * PITCH), p.X + pnext * (int64_t)n, row_bytes, my_bar);
     // the generation after next (consumed at the next finalize: the atomic's latency is hidden)
     const bool any_fresh = __any_sync(0xffffffffu, fresh);
-    if (lane == 0 && any_fresh) wclaim = atomicAdd(p.claim, (unsigned long long)GPW);
+    if (lane == 0 && any_fresh && p.claim) wclaim = atomicAdd(p.claim, (unsigned long long)GPW);
     const float tl = tt / lam;
     // the chunk stores are warp-collective: lanes that keep their point write back what they
     // read; when every lane starts a point or has none left (the lockstep case), nothing is read
@@ -800,7 +800,8 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
       p.iters[pt] = wstatus;
     }
     // ---- refill: the next point of each finalized group --------------------------------------
-    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * ngroups + (lane / G);
+    const int64_t claimed = p.claim ? (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * ngroups + (lane / G)
+                                    : pnext + ngroups;   // no counter: static stride
     if (done) {
       pt = pnext;
       pnext = claimed;

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
       tt = DIST ? 0.f : tpre;   // distance mode starts at s_0 = 0 (R24)
       bad = !(tt >= 0.f) || !finite_f(tt);
       tpre = (p1 < M && !DIST) ? __ldg(p.t + p1) : 0.f;
-      if (gl == 0) gclaim = atomicAdd(p.claim, 1ull);
+      if (gl == 0 && p.claim) gclaim = atomicAdd(p.claim, 1ull);
       nn = 0;
       dtg::mbar_wait(dtg::smem_u32(bars + xs), (xph >> xs) & 1u);
       xph ^= 1u << xs;
@@ -450,7 +450,8 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
       bestit = 0;
       bgn = 0.f;
     }
-    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, gclaim, lane & ~(G - 1)) + 3 * ngroups;
+    const int64_t claimed = p.claim ? (int64_t)__shfl_sync(0xffffffffu, gclaim, lane & ~(G - 1)) + 3 * ngroups
+                                    : p2 + ngroups;   // no counter: static stride
     if (point_done) {
       pt = p1;
       p1 = p2;

@@ -26,7 +26,7 @@ struct EllAParams {
   float *phi, *grad;
   int *iters;
   unsigned long long *iter_total;
-  unsigned long long *claim;   // the launch's point counter (zeroed before the launch)
+  unsigned long long *claim;   // the launch's point counter (zeroed before the launch); null: static
 };
 
 constexpr int ELLA_WARPS = 4;
@@ -119,13 +119,13 @@ __global__ void __launch_bounds__(32 * ELLA_WARPS) hopf_ella_kernel(const EllAPa
   unsigned long long wclaim = 0;   // lane 0: the claim made at the current batch's start
   auto next_batch = [&]() {
     const int64_t nb = bnext;
-    bnext = (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * nslots;
+    bnext = p.claim ? (int64_t)__shfl_sync(0xffffffffu, wclaim, 0) + 2 * nslots : bnext + nslots;
     return nb;
   };
   for (int64_t base = ((int64_t)blockIdx.x * ELLA_WARPS + wib) * GPW; base < p.M; base = next_batch()) {
     {
       const unsigned zoff = lane_zero(zero_lanes, lane);
-      if (lane == 0) wclaim = atomicAdd(p.claim + zoff, (unsigned long long)GPW);
+      if (lane == 0 && p.claim) wclaim = atomicAdd(p.claim + zoff, (unsigned long long)GPW);
     }
     const int64_t pt = base + sub;
     const bool have = pt < p.M;

@@ -92,6 +92,18 @@ void scratch_free(void *ptr, cudaStream_t stream) {
   if (ptr) cudaFreeAsync(ptr, stream);
 }
 
+int claim_counter(int64_t M, int64_t resident, cudaStream_t stream, unsigned long long **ctr) {
+  *ctr = nullptr;
+  // HOPF_CLAIMS=0 / 1: never / always (tests and A/B runs); default: M >= 8 x resident
+  const char *env = getenv("HOPF_CLAIMS");   // read per launch: tests switch it
+  const int mode = env ? atoi(env) : -1;
+  if (mode == 0 || (mode != 1 && M < 8 * resident)) return HOPF_OK;
+  const int rc = scratch_alloc((void **)ctr, sizeof(unsigned long long), stream);
+  if (rc != HOPF_OK) return rc;
+  cudaMemsetAsync(*ctr, 0, sizeof(unsigned long long), stream);
+  return HOPF_OK;
+}
+
 // ---------------------------------------------------------------- diag / union variants
 using KernFn = void (*)(const DiagParams);
 
@@ -186,9 +198,8 @@ static int launch_diag_tm(const DiagParams &p, hopf_h_kind h, cudaStream_t strea
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   DiagParams q = p;
-  int rc = scratch_alloc((void **)&q.claim, sizeof(unsigned long long), stream);
+  int rc = claim_counter(p.M, blocks * (THREADS / 32), stream, &q.claim);
   if (rc != HOPF_OK) return rc;
-  cudaMemsetAsync(q.claim, 0, sizeof(unsigned long long), stream);
   fn<<<(unsigned)blocks, THREADS, DYN_SMEM, stream>>>(q);
   scratch_free(q.claim, stream);
   g_launches += 1;
@@ -288,7 +299,11 @@ static int launch_diag_like(const DiagParams &p_in, hopf_h_kind h, bool is_union
   int64_t blocks = (int64_t)num_sms() * cached.per_sm;
   if (blocks > blocks_needed) blocks = blocks_needed;
   if (blocks < 1) blocks = 1;
-  fn<<<(unsigned)blocks, threads, dyn, stream>>>(p);
+  DiagParams q = p;
+  int rc = v->G > 1 ? claim_counter(p.M, blocks * threads / v->G, stream, &q.claim) : HOPF_OK;   // (G = 1: static)
+  if (rc != HOPF_OK) return rc;
+  fn<<<(unsigned)blocks, threads, dyn, stream>>>(q);
+  scratch_free(q.claim, stream);
   g_launches += 1;
   g_last_threads = threads;
   g_last_blocks = (int)blocks;

@@ -74,9 +74,8 @@ extern "C" int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const floa
   const int64_t need = (M * v->G + threads - 1) / threads;
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  int rc = scratch_alloc((void **)&p.claim, sizeof(unsigned long long), (cudaStream_t)stream);
+  int rc = claim_counter(M, blocks * threads / v->G, (cudaStream_t)stream, &p.claim);
   if (rc != HOPF_OK) return rc;
-  cudaMemsetAsync(p.claim, 0, sizeof(unsigned long long), (cudaStream_t)stream);
   fn<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(p);
   scratch_free(p.claim, (cudaStream_t)stream);
   g_launches = 1;
@@ -134,9 +133,8 @@ extern "C" int hopf_eval_diag_A(int64_t M, int32_t n, const float *X, const floa
   int64_t blocks = (int64_t)num_sms() * per_sm;
   const int64_t need = (M + ELLA_WARPS * gpw - 1) / (ELLA_WARPS * gpw);
   if (blocks > need) blocks = need;
-  int rc = scratch_alloc((void **)&p.claim, sizeof(unsigned long long), (cudaStream_t)stream);
+  int rc = claim_counter(M, blocks * ELLA_WARPS * gpw, (cudaStream_t)stream, &p.claim);
   if (rc != HOPF_OK) return rc;
-  cudaMemsetAsync(p.claim, 0, sizeof(unsigned long long), (cudaStream_t)stream);
   fn<<<(unsigned)blocks, 32 * ELLA_WARPS, smem, (cudaStream_t)stream>>>(p);
   scratch_free(p.claim, (cudaStream_t)stream);
   g_launches = 1;

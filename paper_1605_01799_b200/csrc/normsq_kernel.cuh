@@ -42,7 +42,7 @@ struct NormsqParams {
   float *phi, *grad;
   int *iters;
   unsigned long long *iter_total;
-  unsigned long long *claim;   // the launch's point counter (zeroed before the launch)
+  unsigned long long *claim;   // the launch's point counter (zeroed before the launch); null: static
 };
 
 // Root m >= 0 of a S(m) - c m - e (see above) for the values |z_i| of this lane's CPL slots;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
     bool bad = false;
     const unsigned zoff = lane_zero(zero_lanes, lane);
     if (active) {
-      if (gl == 0) gclaim = atomicAdd(p.claim + zoff, 1ull);
+      if (gl == 0 && p.claim) gclaim = atomicAdd(p.claim + zoff, 1ull);
       tt = __ldg(p.t + pt);
       bad = !(tt >= 0.f) || !finite_f(tt);
       const float *xrow = p.X + pt * (int64_t)n;
@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
 #pragma unroll
     for (int j = 0; j < CPL; j++) cnt += (j < jmax && fabsf(x[j]) == mx) ? 1.f : 0.f;
     cnt = group_sum<G>(cnt);
-    const int64_t claimed = (int64_t)__shfl_sync(0xffffffffu, gclaim, lane & ~(G - 1)) + 2 * ngroups;
+    const int64_t claimed = p.claim ? (int64_t)__shfl_sync(0xffffffffu, gclaim, lane & ~(G - 1)) + 2 * ngroups
+                                    : pnext + ngroups;   // no counter: static stride
     if (done) {
       float phiv, g[CPL];
       if (spec == 2) {

@@ -96,9 +96,8 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
     if (blocks > need) blocks = need;
     if (blocks < 1) blocks = 1;
     DiagParams q = p;
-    int rc = scratch_alloc((void **)&q.claim, sizeof(unsigned long long), stream);
+    int rc = claim_counter(p.M, blocks * per_block, stream, &q.claim);
     if (rc != HOPF_OK) return rc;
-    cudaMemsetAsync(q.claim, 0, sizeof(unsigned long long), stream);
     fn<<<(unsigned)blocks, dtg::THREADS, dtg::DYN_SMEM, stream>>>(q);
     scratch_free(q.claim, stream);
     *handled = true;
@@ -125,9 +124,8 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   if (blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   DiagParams q = p;
-  int rc = scratch_alloc((void **)&q.claim, sizeof(unsigned long long), stream);
+  int rc = claim_counter(p.M, blocks * per_block, stream, &q.claim);
   if (rc != HOPF_OK) return rc;
-  cudaMemsetAsync(q.claim, 0, sizeof(unsigned long long), stream);
   v->fn<<<(unsigned)blocks, dtu::THREADS, dtu::DYN_SMEM, stream>>>(q);
   scratch_free(q.claim, stream);
   *handled = true;

@@ -973,3 +973,64 @@ def test_normsq_tiny_t_linf_multiplier_regression(hb):
     t2 = np.full(64, 1e-5, np.float32)
     for h in ("linf", "l1"):
         check_normsq(hb, X[:64], t2, "l1sq", h, lam=0.5, max_iter=5000)
+
+
+# ----------------------------------------------------------------- dynamic point claims
+def _claims_case(hb, family, rng):
+    """One call of a kernel family on a modest batch; returns (outputs, expected kernel prefix)."""
+    M = 3000
+    if family in ("reg_g2", "reg_unaligned", "tmg", "tm"):
+        n = {"reg_g2": 20, "reg_unaligned": 41, "tmg": 100, "tm": 700}[family]
+        h = {"reg_g2": "l1", "reg_unaligned": "wl1", "tmg": "wl1", "tm": "l2"}[family]
+        X = rng.normal(scale=2.0, size=(M, n)).astype(np.float32)
+        t = rng.uniform(0.0, 2.0, M).astype(np.float32)
+        t[7] = 0.0
+        X[11, 0] = np.nan
+        D = rng.uniform(0.5, 2.0, n).astype(np.float32)
+        w = rng.uniform(0.5, 1.5, n).astype(np.float32)
+        kern = {"reg_g2": "hopf_diag_kernel", "reg_unaligned": "hopf_diag_kernel",
+                "tmg": "hopf_diag_tmg_kernel", "tm": "hopf_diag_tm_kernel"}[family]
+        return (lambda: hb.eval_diag(dev(X), dev(t), dev(D), None, -0.5, h, dev(w))), kern
+    if family in ("union_tmg", "union_reg", "distance"):
+        n = 65 if family == "union_reg" else 64
+        K = 5
+        Ck = (rng.standard_normal((K, n)) * 2.0).astype(np.float32)
+        Dk = (rng.uniform(0.5, 2.0, (K, n)) ** 2).astype(np.float32)
+        gk = rng.uniform(-0.7, -0.3, K).astype(np.float32)
+        X = (rng.standard_normal((M, n)) * 3.0).astype(np.float32)
+        t = rng.uniform(0.0, 2.0, M).astype(np.float32)
+        if family == "distance":
+            return (lambda: hb.distance_union(dev(X[:1000]), dev(Dk), dev(Ck), dev(gk))), "hopf_union_tmg_kernel<l2, distance>"
+        kern = "hopf_diag_kernel<union>" if family == "union_reg" else "hopf_union_tmg_kernel<l2>"
+        return (lambda: hb.eval_union(dev(X), dev(t), dev(Dk), dev(Ck), dev(gk), "l2", want_phik=True)), kern
+    if family == "normsq":
+        X = rng.uniform(-10, 10, (M, 16)).astype(np.float32)
+        t = rng.uniform(0, 10, M).astype(np.float32)
+        return (lambda: hb.eval_normsq(dev(X), dev(t), "l1sq", 0.0, "linf")), "hopf_normsq_kernel"
+    assert family == "ella"
+    n = 16
+    X = rng.uniform(-10, 10, (M, n)).astype(np.float32)
+    t = rng.uniform(0, 10, M).astype(np.float32)
+    D = (1.0 + np.arange(n) / (n - 1)).astype(np.float32)
+    A = np.eye(n) + np.ones((n, n))
+    Lam, Q = np.linalg.eigh(A)
+    return (lambda: hb.eval_diag_A(dev(X), dev(t), dev(D), None, 0.0, dev(Q), dev(Lam))), "hopf_ella_kernel"
+
+
+@pytest.mark.parametrize("family", ["reg_g2", "reg_unaligned", "tmg", "tm", "union_tmg", "union_reg",
+                                    "distance", "normsq", "ella"])
+def test_point_claims_match_static(hb, family, monkeypatch):
+    """Dynamic point claims (a launch counter; HOPF_CLAIMS=1 forces them at any size) hand the
+    points to other groups than the static stride (HOPF_CLAIMS=0) does, but every point's solve
+    is the same arithmetic: the outputs must be bitwise identical, with every point written."""
+    import torch
+    rng = np.random.default_rng(hash(family) % 2**32)
+    call, kern = _claims_case(hb, family, rng)
+    monkeypatch.setenv("HOPF_CLAIMS", "0")
+    a = [x.clone() for x in call()]
+    assert hb.last_kernel().startswith(kern), hb.last_kernel()
+    monkeypatch.setenv("HOPF_CLAIMS", "1")
+    b = [x.clone() for x in call()]
+    assert hb.last_kernel().startswith(kern), hb.last_kernel()
+    for u, v in zip(a, b):   # (the static path itself is parity-tested against the oracle)
+        assert torch.equal(u.nan_to_num(0.25), v.nan_to_num(0.25)), family
