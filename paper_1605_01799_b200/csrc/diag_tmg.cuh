@@ -383,8 +383,8 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
       for (int q = 0; q < NP; q++) {
         const float2 g = L2 ? make_float2(-d[q].x, -d[q].y)
                             : ((ELL || LINF) ? d[q] : add2(d[q], b[q]));   // l1 / wl1: d = a + b
-        my_g[G * (2 * q)] = spec == 2 ? __int_as_float(0x7fc00000) : g.x;
-        my_g[G * (2 * q + 1)] = spec == 2 ? __int_as_float(0x7fc00000) : g.y;
+        my_g[G * (2 * q)] = g.x;   // (an invalid point's row is set to NaN at finalize)
+        my_g[G * (2 * q + 1)] = g.y;
       }
     }
   };
@@ -714,7 +714,8 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
           wait_ld(vv);
 #pragma unroll
           for (int e2 = 0; e2 < SZ / 2; e2++) {
-            const float2 dk = (L2 || ELL || LINF) ? d[4 * c + e2] : add2(d[4 * c + e2], b[4 * c + e2]);   // l1: d^k = a + b
+            const int q = 4 * c + e2;
+            const float2 dk = (L2 || ELL || LINF) ? d[q] : add2(d[q], b[q]);   // l1: d^k = a + b
             const float2 dmv = sub2(dk, make_float2(vv[0][2 * e2], vv[0][2 * e2 + 1]));
             if (e2 & 1) sb3 = fma2(dmv, dmv, sb3);
             else sb2 = fma2(dmv, dmv, sb2);
@@ -761,6 +762,12 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
           }
         }
       });
+    }
+    if (__any_sync(0xffffffffu, done && spec == 2)) {   // rare: invalid points, grad = NaN
+      if (done && spec == 2) {
+#pragma unroll
+        for (int j = 0; j < CPL; j++) my_g[G * j] = gnan;
+      }
     }
     // the grad rows (stashed at stop) are read back for phi; non-finalized lanes read their own
     // (irrelevant) buffer contents
