@@ -168,7 +168,7 @@ __host__ __device__ constexpr int row_pitch(int w, int G) {
 }
 template <int G, int CPL>
 __host__ __device__ constexpr size_t smem_bytes() {
-  return (size_t)2 * G * CPL * 16 + (size_t)2 * (THREADS / G) * row_pitch(G * CPL, G) * 4 +
+  return (size_t)2 * G * CPL * 16 + (size_t)2 * (THREADS / G) * row_pitch(G * CPL + 4, G) * 4 +
          (size_t)(THREADS / G) * 8;
 }
 
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
   static_assert(smem_bytes<G, CPL>() <= (size_t)DYN_SMEM, "shared buffers exceed the budget");
   constexpr int NP = CPL / 2;
   constexpr int GPW = 32 / G, GPB = THREADS / G;
-  constexpr int PITCH = row_pitch(G * CPL, G);
+  constexpr int PITCH = row_pitch(G * CPL + 4, G);   // a row starts at offset (r n) mod 4 in its buffer
   constexpr bool L2 = HK == HK_L2, WL1 = HK == HK_WL1, ELL = HK == HK_ELL, LINF = HK == HK_LINF;
   constexpr bool WTAB = WL1 || ELL;   // per-coordinate weights in the tables
   extern __shared__ __align__(16) uint8_t dyn_smem[];
@@ -212,12 +212,15 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
   float *const xbuf = reinterpret_cast<float *>(B_s + G * CPL);
   float *const gbuf = xbuf + GPB * PITCH;
   uint64_t *const xbar = reinterpret_cast<uint64_t *>(gbuf + GPB * PITCH);
-  float *const my_x = xbuf + grp * PITCH + gl;   // + G j: this lane's slot j
-  float *const my_g = gbuf + grp * PITCH + gl;
+  // this lane's slot j of the current point's x / grad row: my_x[G j], my_g[G j].  Element i of
+  // row r sits at buffer offset (r n) mod 4 + i, so that the row's 16-byte aligned part maps to
+  // 16-byte aligned shared memory (bulk copies need both ends aligned); set at each refill
+  float *my_x = xbuf + grp * PITCH + gl;
+  float *my_g = gbuf + grp * PITCH + gl;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
   const float4 *const my_A = A_s + gl;
   const float4 *const my_B = B_s + gl;
   const uint32_t my_bar = smem_u32(xbar + grp);
-  const uint32_t row_bytes = (uint32_t)n * 4u;
   for (int i = threadIdx.x; i < G * CPL; i += THREADS) {
     const bool real = i < n;
     const float Dv = real ? __ldg(p.D + i) : 1.f;
@@ -285,7 +288,17 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
   float mu = 0.f;         // ELL / LINF: multiplier of the last projection (warm start of the next)
 #pragma unroll
   for (int q = 0; q < NP; q++) d[q] = b[q] = splat2(0.f);
-  if (gl == 0 && have) bulk_load(smem_u32(xbuf + grp * PITCH), p.X + pt * (int64_t)n, row_bytes, my_bar);
+  // x row of point r: its 16-byte aligned part [a0, a1) by one bulk copy (leader), the last
+  // (r n + n) mod 4 floats by plain loads of lanes gl < that count into xtail (stored into the
+  // buffer at the refill); with n % 4 == 0 the whole row is one bulk copy
+  auto prefetch_x = [&](int64_t r) {
+    const int64_t off = r * (int64_t)n, a0 = off & ~(int64_t)3, a1 = (off + n) & ~(int64_t)3;
+    if (gl == 0) bulk_load(smem_u32(xbuf + grp * PITCH), p.X + a0, (uint32_t)(a1 - a0) * 4u, my_bar);
+    const int64_t e = off + n;
+    const int tl = (int)(e & 3);
+    return gl < tl ? __ldg(p.X + (e - tl) + gl) : 0.f;
+  };
+  float xtail = have ? prefetch_x(pt) : 0.f;
 
   // ---- start the point pt of the groups with `fresh` set (collective: every lane executes the
   // TMEM chunk traffic; other lanes write back what they read).  Setup: x_hat = (x - c)/(D + lambda),
@@ -298,6 +311,15 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
       tpre = pnext < M ? __ldg(p.t + pnext) : 0.f;
       mbar_wait(my_bar, xph);
       xph ^= 1u;
+      {
+        const int64_t off = pt * (int64_t)n;
+        const int o = (int)(off & 3), tl = (int)((off + n) & 3);
+        float *const xr = xbuf + grp * PITCH + o;   // element i at xr[i]
+        if (gl < tl) xr[n - tl + gl] = xtail;
+        __syncwarp(gmask);
+        my_x = xr + gl;
+        my_g = gbuf + grp * PITCH + o + gl;
+      }
 #pragma unroll
       for (int q = 0; q < NP; q++) {   // x from the prefetched row (padding slots read 0 below)
         const int j0 = 2 * q, j1 = 2 * q + 1;
@@ -308,10 +330,11 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
       for (int q = 0; q < NP; q++) fin = fma2(d[q], splat2(0.f), fin);
       bad |= !(fin.x == 0.f && fin.y == 0.f);
     }
-    // the group's row has been read: its leader prefetches the following point's x into it
+    // the group's row has been read (and its tail written): its leader prefetches the following
+    // point's x into it (generic-proxy accesses ordered before the async-proxy copy)
+    if (fresh) fence_proxy_async();
     __syncwarp();
-    if (fresh && gl == 0 && pnext < M)
-      bulk_load(smem_u32(xbuf + grp * PITCH), p.X + pnext * (int64_t)n, row_bytes, my_bar);
+    if (fresh && pnext < M) xtail = prefetch_x(pnext);
     // the generation after next (consumed at the next finalize: the atomic's latency is hidden)
     const bool any_fresh = __any_sync(0xffffffffu, fresh);
     if (lane == 0 && any_fresh && p.claim) wclaim = atomicAdd(p.claim, (unsigned long long)GPW);
@@ -772,7 +795,6 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
     // the grad rows (stashed at stop) are read back for phi; non-finalized lanes read their own
     // (irrelevant) buffer contents
     float qs0 = 0.f, qs1 = 0.f, hs0 = 0.f, hs1 = 0.f;
-    float *const grow = p.grad + pt * (int64_t)n + gl;
     for_chunks<CPL>([&](auto ci, auto szc) {
       constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
       float xh8[1][8];
@@ -797,7 +819,14 @@ __global__ void __launch_bounds__(THREADS, HOPF_TMG_MINB) hopf_diag_tmg_kernel(c
     });
     fence_proxy_async();
     __syncwarp();
-    if (done && gl == 0) bulk_store(grow - gl, smem_u32(gbuf + grp * PITCH), row_bytes);
+    if (done) {   // the row's aligned interior by a bulk store, up to 3 floats at each end by lanes
+      const int64_t off = pt * (int64_t)n;
+      const int o = (int)(off & 3), h = (4 - o) & 3, e = (int)(((off + n) & ~(int64_t)3) - off);
+      const float *const gr = gbuf + grp * PITCH + o;   // element i at gr[i]
+      if (gl == 0) bulk_store(p.grad + off + h, smem_u32(gr + h), (uint32_t)(e - h) * 4u);
+      if (gl < h) p.grad[off + gl] = gr[gl];
+      if (gl < n - e) p.grad[off + e + gl] = gr[e + gl];
+    }
     const float qs = group_sum<G>(qs0 + qs1);
     const float hsum = LINF ? group_max<G>(fmaxf(hs0, hs1)) : group_sum<G>(hs0 + hs1);
     if (done && gl == 0) {

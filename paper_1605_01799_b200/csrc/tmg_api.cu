@@ -1,7 +1,7 @@
 // tmg_api.cu — variant choice and launch of the grouped TMEM kernels (K1g, K4g).
-// A variant applies when it holds n (G * CPL >= n) with at most a quarter of padding, the rows of
-// X, grad (and Y) are 16-byte aligned with n % 4 == 0 (bulk row copies), and, for the union, the
-// per-set tables fit the block's shared memory.  HOPF_DIAG_TMG=0 / HOPF_UNION_TMG=0 select the
+// A variant applies when it holds n (G * CPL >= n) with at most a quarter of padding, the bases of
+// X, grad (and Y) are 16-byte aligned (bulk row copies; the union also needs n % 4 == 0), and, for
+// the union, the per-set tables fit the block's shared memory.  HOPF_DIAG_TMG=0 / HOPF_UNION_TMG=0 select the
 // register kernels (A/B experiments).
 #include <atomic>
 #include <cstdint>
@@ -80,9 +80,11 @@ const TmuVariant *tmu_variants(int *count) {
 
 int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t stream, bool *handled) {
   *handled = false;
-  const bool aligned = p.n % 4 == 0 && (((uintptr_t)p.X | (uintptr_t)p.grad) & 15) == 0;
+  // bulk row copies: 16-byte aligned bases; K1g handles any n (a row's unaligned ends move by
+  // plain loads / stores), K4g needs n % 4 == 0
+  const bool bases = (((uintptr_t)p.X | (uintptr_t)p.grad) & 15) == 0;
   static const char *benv = getenv("HOPF_TMG_BULK");
-  if (!aligned || (benv && strcmp(benv, "0") == 0)) return HOPF_OK;
+  if (!bases || (benv && strcmp(benv, "0") == 0)) return HOPF_OK;
   if (!is_union) {
     if (h < HOPF_H_L1 || h > HOPF_H_LINF) return HOPF_OK;
     int idx = 0;
@@ -113,7 +115,7 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   // union (l2), also in distance mode (NEXT-1: p.dist non-null, p.Y = the projections)
   static const char *denv = getenv("HOPF_DIST_TMG");
   if (p.dist && denv && strcmp(denv, "0") == 0) return HOPF_OK;
-  if (h != HOPF_H_L2 || (p.Y && ((uintptr_t)p.Y & 15) != 0)) return HOPF_OK;
+  if (h != HOPF_H_L2 || p.n % 4 != 0 || (p.Y && ((uintptr_t)p.Y & 15) != 0)) return HOPF_OK;
   int idx = 0;
   const TmuVariant *v = pick_tmu(p, &idx);
   if (!v) return HOPF_OK;

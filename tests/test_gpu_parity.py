@@ -833,14 +833,14 @@ def _guarded(shape, fill, pad=256, dtype=None):
     return buf, buf[pad:pad + numel].view(shape)
 
 
-@pytest.mark.parametrize("family", ["tm", "tmg", "reg", "tmu", "dense"])
+@pytest.mark.parametrize("family", ["tm", "tmg", "tmg_unaligned", "reg", "tmu", "dense"])
 def test_kernels_stay_in_bounds_and_are_deterministic(hb, family):
     """Inputs sit between NaN margins and outputs between sentinel margins: a kernel that reads
     outside its rows would pull NaN into a valid result (compared bitwise with a clean run), one
     that writes outside would change a sentinel.  Two runs must agree bit for bit (races)."""
     import torch
-    name, M, n = {"tm": ("c3", 700, None), "tmg": ("c2", 3001, None), "reg": ("c2", 3001, 90),
-                  "tmu": ("c5", 1001, None), "dense": ("c4", 1001, None)}[family]
+    name, M, n = {"tm": ("c3", 700, None), "tmg": ("c2", 3001, None), "tmg_unaligned": ("c2", 3001, 90),
+                  "reg": ("c2", 3001, 22), "tmu": ("c5", 1001, None), "dense": ("c4", 1001, None)}[family]
     wl = inputs.config(name, M=M, n=n)
     X, t = inputs.points(wl)
     n = wl.n
@@ -894,8 +894,8 @@ def test_kernels_stay_in_bounds_and_are_deterministic(hb, family):
     a, ka = run(True)
     b, kb = run(False)
     c, _ = run(True)
-    expect = {"tm": "hopf_diag_tm_kernel", "tmg": "hopf_diag_tmg_kernel", "reg": "hopf_diag_kernel",
-              "tmu": "hopf_union_tmg_kernel", "dense": "hopf_dense_tc3_kernel"}[family]
+    expect = {"tm": "hopf_diag_tm_kernel", "tmg": "hopf_diag_tmg_kernel", "tmg_unaligned": "hopf_diag_tmg_kernel",
+              "reg": "hopf_diag_kernel", "tmu": "hopf_union_tmg_kernel", "dense": "hopf_dense_tc3_kernel"}[family]
     assert ka.startswith(expect) and kb.startswith(expect), (ka, kb)
     for u, v, w in zip(a, b, c):
         assert torch.equal(u.nan_to_num(0.25), v.nan_to_num(0.25)), f"{family}: guarded run differs"
@@ -927,6 +927,29 @@ def test_tmg_every_instance(hb, n, h):
     kern = hb.last_kernel()
     assert kern.startswith("hopf_diag_tmg_kernel"), kern
     o = oracle.eval_diag(X, t, D, c, -0.5, h, w, lam=lam)
+    check(*g, *o)
+
+
+@pytest.mark.parametrize("n", [25, 27, 33, 61, 99, 101, 127, 203, 255, 257, 381, 509, 511])
+@pytest.mark.parametrize("h", ["l1", "wl1", "l2", "ell", "linf"])
+def test_tmg_unaligned_rows(hb, n, h):
+    """K1g with n % 4 != 0: each row's 16-byte aligned part moves by bulk copies and its up to 3
+    unaligned floats at either end by plain loads / stores (row r starts at float r n).  Every
+    point against the oracle (so every combination of head and tail lengths is covered)."""
+    rng = np.random.default_rng(7 * n + len(h))
+    M = 203
+    D = rng.uniform(0.5, 2.0, n).astype(np.float32)
+    c = rng.normal(size=n).astype(np.float32)
+    w = rng.uniform(0.5, 1.5, n).astype(np.float32)
+    X = rng.normal(scale=2.0, size=(M, n)).astype(np.float32)
+    t = rng.uniform(0.0, 2.0, M).astype(np.float32)
+    t[1] = 0.0
+    X[2, n - 1] = np.nan   # in a row's tail
+    X[5, 0] = np.inf       # in a row's head
+    g = hb.eval_diag(dev(X), dev(t), dev(D), dev(c), -0.5, h, dev(w), lam=0.8)
+    kern = hb.last_kernel()
+    assert kern.startswith("hopf_diag_tmg_kernel"), kern
+    o = oracle.eval_diag(X, t, D, c, -0.5, h, w, lam=0.8)
     check(*g, *o)
 
 
@@ -979,16 +1002,16 @@ def test_normsq_tiny_t_linf_multiplier_regression(hb):
 def _claims_case(hb, family, rng):
     """One call of a kernel family on a modest batch; returns (outputs, expected kernel prefix)."""
     M = 3000
-    if family in ("reg_g2", "reg_unaligned", "tmg", "tm"):
-        n = {"reg_g2": 20, "reg_unaligned": 41, "tmg": 100, "tm": 700}[family]
-        h = {"reg_g2": "l1", "reg_unaligned": "wl1", "tmg": "wl1", "tm": "l2"}[family]
+    if family in ("reg_g2", "tmg_unaligned", "tmg", "tm"):
+        n = {"reg_g2": 20, "tmg_unaligned": 41, "tmg": 100, "tm": 700}[family]
+        h = {"reg_g2": "l1", "tmg_unaligned": "wl1", "tmg": "wl1", "tm": "l2"}[family]
         X = rng.normal(scale=2.0, size=(M, n)).astype(np.float32)
         t = rng.uniform(0.0, 2.0, M).astype(np.float32)
         t[7] = 0.0
         X[11, 0] = np.nan
         D = rng.uniform(0.5, 2.0, n).astype(np.float32)
         w = rng.uniform(0.5, 1.5, n).astype(np.float32)
-        kern = {"reg_g2": "hopf_diag_kernel", "reg_unaligned": "hopf_diag_kernel",
+        kern = {"reg_g2": "hopf_diag_kernel", "tmg_unaligned": "hopf_diag_tmg_kernel",
                 "tmg": "hopf_diag_tmg_kernel", "tm": "hopf_diag_tm_kernel"}[family]
         return (lambda: hb.eval_diag(dev(X), dev(t), dev(D), None, -0.5, h, dev(w))), kern
     if family in ("union_tmg", "union_reg", "distance"):
@@ -1017,7 +1040,7 @@ def _claims_case(hb, family, rng):
     return (lambda: hb.eval_diag_A(dev(X), dev(t), dev(D), None, 0.0, dev(Q), dev(Lam))), "hopf_ella_kernel"
 
 
-@pytest.mark.parametrize("family", ["reg_g2", "reg_unaligned", "tmg", "tm", "union_tmg", "union_reg",
+@pytest.mark.parametrize("family", ["reg_g2", "tmg_unaligned", "tmg", "tm", "union_tmg", "union_reg",
                                     "distance", "normsq", "ella"])
 def test_point_claims_match_static(hb, family, monkeypatch):
     """Dynamic point claims (a launch counter; HOPF_CLAIMS=1 forces them at any size) hand the
