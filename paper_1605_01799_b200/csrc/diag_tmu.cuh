@@ -46,17 +46,20 @@ constexpr int BLOCKS_PER_SM = HOPF_TMU_BLOCKS;
 constexpr int DYN_SMEM = (226 * 1024) / BLOCKS_PER_SM - 1024;
 
 // shared-memory bytes for K sets: (D, c) tables, gamma, 4 rows per group, 2 mbarriers per group
-template <int G, int CPL>
+// (UNAL: rows start at offset (r n) mod 4 in their buffers, 3 floats more)
+template <int G, int CPL, bool UNAL>
 __host__ __device__ constexpr size_t smem_bytes(int K) {
   return (size_t)K * G * CPL * 8 + (((size_t)K * 4 + 15) & ~(size_t)15) +
-         (size_t)4 * (THREADS / G) * dtg::row_pitch(G * CPL, G) * 4 + (size_t)(THREADS / G) * 16;
+         (size_t)4 * (THREADS / G) * dtg::row_pitch(G * CPL + (UNAL ? 4 : 0), G) * 4 + (size_t)(THREADS / G) * 16;
 }
 
 #ifndef HOPF_TMU_WAIT8
 #define HOPF_TMU_WAIT8 8  // run the event when this many eighths of the warp's groups wait
 #endif                    // (C5, 8 groups: 2 -> 11.75 ms, 3 -> 12.38, 4 -> 11.04, 5 -> 13.98, 6 -> 12.53, 7 -> 11.39, 8 -> 9.79)
 
-template <int G, int CPL>
+// UNAL: n % 4 != 0 (rows do not all start on a 16-byte boundary; a separate instance keeps the
+// aligned case's code as it was: the unaligned bookkeeping cost C5 ~4 % when shared)
+template <int G, int CPL, bool UNAL>
 __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(const DiagParams p) {
   constexpr int C_XH = Cols<CPL>::XH, C_V = Cols<CPL>::V, C_K = Cols<CPL>::K, TMEM_COLS = Cols<CPL>::ALLOC;
   static_assert(G >= 2 && G <= 16 && (G & (G - 1)) == 0, "G in {2, 4, 8, 16}");
@@ -64,7 +67,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
                 "CPL = 8 a + {0, 2, 4}, at most 32");
   constexpr int NP = CPL / 2;
   constexpr int GPW = 32 / G, GPB = THREADS / G;
-  constexpr int PITCH = dtg::row_pitch(G * CPL, G);
+  constexpr int PITCH = dtg::row_pitch(G * CPL + (UNAL ? 4 : 0), G);   // UNAL: rows at offset (r n) mod 4
   constexpr int WAIT_THRESHOLD = (GPW * HOPF_TMU_WAIT8 / 8) > 0 ? (GPW * HOPF_TMU_WAIT8 / 8) : 1;
   using dtg::ldn;
   using dtg::stn;
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   float *const rows = reinterpret_cast<float *>(dyn_smem + (((size_t)K * G * CPL * 8 + (size_t)K * 4 + 15) & ~(size_t)15));
   float *const xrow0 = rows + (size_t)(4 * grp) * PITCH;   // x rows 0, 1; grad rows 2, 3
   uint64_t *const bars = reinterpret_cast<uint64_t *>(rows + (size_t)4 * GPB * PITCH) + 2 * grp;
-  const uint32_t row_bytes = (uint32_t)n * 4u;
+  const unsigned gmask = ((1u << G) - 1u) << (lane & ~(G - 1));
   for (int e = threadIdx.x; e < K * G * CPL; e += THREADS) {
     const int k = e / (G * CPL), i = e % (G * CPL);
     const bool real = i < n;
@@ -136,16 +139,33 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   int bestk = -1, bestit = 0;
 #pragma unroll
   for (int q = 0; q < NP; q++) d[q] = b[q] = splat2(0.f);
-  if (gl == 0 && have) {
-    dtg::bulk_load(dtg::smem_u32(xrow(0)), p.X + pt * (int64_t)n, row_bytes, dtg::smem_u32(bars));
-    if (p1 < M)
-      dtg::bulk_load(dtg::smem_u32(xrow(1)), p.X + p1 * (int64_t)n, row_bytes, dtg::smem_u32(bars + 1));
-  }
+  // x row of point r into row buffer sb: the 16-byte aligned part by a bulk copy (leader) at
+  // buffer offset (r n) mod 4, the last (r n + n) mod 4 floats by 4-byte cp.async of lanes
+  // gl < that count (no registers held; waited for when the point starts) -- as K1g, diag_tmg.cuh
+  auto prefetch_x = [&](int64_t r, int sb) {
+    const int64_t off = r * (int64_t)n;
+    if constexpr (!UNAL) {
+      if (gl == 0) dtg::bulk_load(dtg::smem_u32(xrow(sb)), p.X + off, (uint32_t)n * 4u, dtg::smem_u32(bars + sb));
+    } else {
+      const int64_t a0 = off & ~(int64_t)3, a1 = (off + n) & ~(int64_t)3;
+      if (gl == 0)
+        dtg::bulk_load(dtg::smem_u32(xrow(sb)), p.X + a0, (uint32_t)(a1 - a0) * 4u, dtg::smem_u32(bars + sb));
+      const int tl = (int)((off + n) & 3);
+      if (gl < tl)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;"
+                     :: "r"(dtg::smem_u32(xrow(sb) + (off & 3) + n - tl + gl)), "l"(p.X + (off + n - tl) + gl) : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
+  if (have) prefetch_x(pt, 0);
+  if (have && p1 < M) prefetch_x(p1, 1);
+  // (pt n) mod 4: offset of the current point's rows in their buffers (0 unless UNAL)
+  auto xo = [&]() { return UNAL ? (int)((pt * (int64_t)n) & 3) : 0; };
 
   // ---- set k of the current point for the groups with `fresh` (collective): x_hat = (x - c_k) /
   // (D_k + lambda), v^0 = d^0 = x - c_k, b^0 = 0 (R5), -kappa_k = -lambda / (D_k + lambda)
   auto set_setup = [&](bool fresh) {
-    const float *xr = xrow(xs) + gl;
+    const float *xr = xrow(xs) + xo() + gl;
     const float2 *dc = DC_s + kset * (G * CPL) + gl;
     // lanes that keep their set write back what they read; in the lockstep case (every lane
     // starts a set or has no point left) nothing is read
@@ -201,8 +221,14 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
       nn = 0;
       dtg::mbar_wait(dtg::smem_u32(bars + xs), (xph >> xs) & 1u);
       xph ^= 1u << xs;
+      // the row's tail: this lane's cp.async of it (at most the two rows' groups are pending;
+      // waiting for all of them is exact: the other row's tail is in flight at most one point)
+      if constexpr (UNAL) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp(gmask);
+      }
       float fin = 0.f;   // x * 0 accumulates NaN iff some x is NaN or infinite
-      const float *xr = xrow(xs) + gl;
+      const float *xr = xrow(xs) + xo() + gl;
 #pragma unroll
       for (int j = 0; j < CPL; j++)
         if (j < jmax) fin = fmaf(xr[G * j], 0.f, fin);
@@ -227,7 +253,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   // a stopped set parks its d^k (grad := d, R1) in the candidate row; collective
   auto park = [&](bool stop) {
     if (stop) {
-      float *gr = grow_s(cand) + gl;
+      float *gr = grow_s(cand) + xo() + gl;
 #pragma unroll
       for (int q = 0; q < NP; q++) {
         gr[G * (2 * q)] = -d[q].x;
@@ -334,9 +360,10 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
     // ================= event: the parked sets of the waiting groups ===========================
     const bool done = waiting;
     const float gnan = __int_as_float(0x7fc00000);
-    const float *xr = xrow(xs) + gl;
+    const int xoff = xo();
+    const float *xr = xrow(xs) + xoff + gl;
     const float2 *dc = DC_s + kset * (G * CPL) + gl;
-    float *const cr = grow_s(cand) + gl;
+    float *const cr = grow_s(cand) + xoff + gl;
     // t == 0 (R6): the set's grad is grad J_k(x) = D_k^{-1}(x - c_k)
     if (done && spec == 1) {
 #pragma unroll
@@ -403,8 +430,9 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
     }
     // ---- the point's outputs (groups whose last set finished) ---------------------------------
     if (__any_sync(0xffffffffu, point_done)) {
-      float *const br = grow_s(cand ^ 1) + gl;   // best grad row
-      float *const yr = xrow(xs) + gl;           // y formed in place in the x row
+      const int xoff = xo();
+      float *const br = grow_s(cand ^ 1) + xoff + gl;   // best grad row
+      float *const yr = xrow(xs) + xoff + gl;           // y formed in place in the x row
       const bool nanpt = spec == 2 || bestk < 0;
       if (point_done) {
         const float ign = bgn > 0.f ? __fdividef(1.f, bgn) : 0.f;
@@ -428,15 +456,45 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
           if (DIST) p.dist[pt] = nanpt ? gnan : tt;
         }
       }
-      dtg::fence_proxy_async();
-      __syncwarp();
-      if (point_done && gl == 0) {
-        dtg::bulk_store(p.grad + pt * (int64_t)n, dtg::smem_u32(br - gl), row_bytes);
-        if (p.Y) dtg::bulk_store(p.Y + pt * (int64_t)n, dtg::smem_u32(yr - gl), row_bytes);
+      if constexpr (!UNAL) {
+        dtg::fence_proxy_async();
+        __syncwarp();
+        if (point_done && gl == 0) {
+          const int64_t off = pt * (int64_t)n;
+          dtg::bulk_store(p.grad + off, dtg::smem_u32(br - gl), (uint32_t)n * 4u);
+          if (p.Y) dtg::bulk_store(p.Y + off, dtg::smem_u32(yr - gl), (uint32_t)n * 4u);
+          // the x row is free once y has left it: the point after the next one goes there
+          if (p2 < M) {
+            dtg::bulk_wait_read();
+            prefetch_x(p2, xs);
+          }
+        }
+      } else {
+        // rows leave as a bulk store of their 16-byte aligned interior [h, e) plus up to 3 plain
+        // stores at each end (element i of the rows at br - gl + i, yr - gl + i)
+        const int64_t off = pt * (int64_t)n;
+        const int h = (4 - xoff) & 3, e = (int)(((off + n) & ~(int64_t)3) - off);
+        dtg::fence_proxy_async();
+        __syncwarp();
+        if (point_done) {   // (the tail elements were written by other lanes: after the sync)
+          if (gl < h) {
+            p.grad[off + gl] = br[0];
+            if (p.Y) p.Y[off + gl] = yr[0];
+          }
+          if (gl < n - e) {
+            p.grad[off + e + gl] = br[e];
+            if (p.Y) p.Y[off + e + gl] = yr[e];
+          }
+        }
+        if (point_done && gl == 0) {
+          dtg::bulk_store(p.grad + off + h, dtg::smem_u32(br - gl + h), (uint32_t)(e - h) * 4u);
+          if (p.Y) dtg::bulk_store(p.Y + off + h, dtg::smem_u32(yr - gl + h), (uint32_t)(e - h) * 4u);
+        }
         // the x row is free once y has left it: the point after the next one goes there
-        if (p2 < M) {
-          dtg::bulk_wait_read();
-          dtg::bulk_load(dtg::smem_u32(yr - gl), p.X + p2 * (int64_t)n, row_bytes, dtg::smem_u32(bars + xs));
+        if (point_done && p2 < M) {
+          if (gl == 0) dtg::bulk_wait_read();
+          __syncwarp(gmask);
+          prefetch_x(p2, xs);
         }
       }
     }

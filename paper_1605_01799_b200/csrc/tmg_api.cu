@@ -1,7 +1,8 @@
 // tmg_api.cu — variant choice and launch of the grouped TMEM kernels (K1g, K4g).
 // A variant applies when it holds n (G * CPL >= n) with at most a quarter of padding, the bases of
-// X, grad (and Y) are 16-byte aligned (bulk row copies; the union also needs n % 4 == 0), and, for
-// the union, the per-set tables fit the block's shared memory.  HOPF_DIAG_TMG=0 / HOPF_UNION_TMG=0 select the
+// X, grad (and Y) are 16-byte aligned (bulk row copies; rows that do not start on a 16-byte
+// boundary move their ends by plain loads / stores), and, for the union, the per-set tables fit
+// the block's shared memory.  HOPF_DIAG_TMG=0 / HOPF_UNION_TMG=0 select the
 // register kernels (A/B experiments).
 #include <atomic>
 #include <cstdint>
@@ -46,7 +47,7 @@ const TmuVariant *pick_tmu(const DiagParams &p, int *index) {
     const TmuVariant &v = kTmu[i];
     if (v.G * v.CPL >= p.n) {
       *index = i;
-      return (4 * (v.G * v.CPL - p.n) <= v.G * v.CPL && v.smem(p.K) <= (size_t)dtu::DYN_SMEM) ? &v : nullptr;
+      return (4 * (v.G * v.CPL - p.n) <= v.G * v.CPL && v.smem[p.n % 4 != 0](p.K) <= (size_t)dtu::DYN_SMEM) ? &v : nullptr;
     }
   }
   return nullptr;
@@ -80,8 +81,8 @@ const TmuVariant *tmu_variants(int *count) {
 
 int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t stream, bool *handled) {
   *handled = false;
-  // bulk row copies: 16-byte aligned bases; K1g handles any n (a row's unaligned ends move by
-  // plain loads / stores), K4g needs n % 4 == 0
+  // bulk row copies: 16-byte aligned bases; any n (a row's unaligned ends move by plain loads /
+  // stores)
   const bool bases = (((uintptr_t)p.X | (uintptr_t)p.grad) & 15) == 0;
   static const char *benv = getenv("HOPF_TMG_BULK");
   if (!bases || (benv && strcmp(benv, "0") == 0)) return HOPF_OK;
@@ -115,11 +116,12 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   // union (l2), also in distance mode (NEXT-1: p.dist non-null, p.Y = the projections)
   static const char *denv = getenv("HOPF_DIST_TMG");
   if (p.dist && denv && strcmp(denv, "0") == 0) return HOPF_OK;
-  if (h != HOPF_H_L2 || p.n % 4 != 0 || (p.Y && ((uintptr_t)p.Y & 15) != 0)) return HOPF_OK;
+  if (h != HOPF_H_L2 || (p.Y && ((uintptr_t)p.Y & 15) != 0)) return HOPF_OK;
   int idx = 0;
   const TmuVariant *v = pick_tmu(p, &idx);
   if (!v) return HOPF_OK;
-  ensure_smem_attr(v->fn, 240 + idx, dtu::DYN_SMEM);
+  const int un = p.n % 4 != 0;
+  ensure_smem_attr(v->fn[un], 240 + 2 * idx + un, dtu::DYN_SMEM);
   const int per_block = dtu::THREADS / v->G;
   int64_t blocks = (int64_t)num_sms() * dtu::BLOCKS_PER_SM;
   const int64_t need = (p.M + per_block - 1) / per_block;
@@ -128,7 +130,7 @@ int tmg_try_launch(const DiagParams &p, int h, bool is_union, cudaStream_t strea
   DiagParams q = p;
   int rc = claim_counter(p.M, blocks * per_block, stream, &q.claim);
   if (rc != HOPF_OK) return rc;
-  v->fn<<<(unsigned)blocks, dtu::THREADS, dtu::DYN_SMEM, stream>>>(q);
+  v->fn[un]<<<(unsigned)blocks, dtu::THREADS, dtu::DYN_SMEM, stream>>>(q);
   scratch_free(q.claim, stream);
   *handled = true;
   g_launches += 1;

@@ -15,8 +15,8 @@ struct TmgVariant {
 };
 struct TmuVariant {
   int G, CPL;
-  TmgFn fn;              // union, l2
-  size_t (*smem)(int K); // shared-memory bytes for K sets
+  TmgFn fn[2];              // union, l2: [n % 4 != 0]
+  size_t (*smem[2])(int K); // shared-memory bytes for K sets: [n % 4 != 0]
 };
 // tables, ordered by padded width G * CPL
 const TmgVariant *tmg_variants(int *count);

@@ -1,13 +1,13 @@
-// tmu.cu — instances of the grouped TMEM union kernel (diag_tmu.cuh), H = l2.
+// tmu.cu — instances of the grouped TMEM union kernel (diag_tmu.cuh), H = l2: rows on 16-byte
+// boundaries (n % 4 == 0) and not (UNAL).
 #include "diag_tmu.cuh"
 #include "tmg_api.h"
 
 namespace hopf {
-extern const TmuVariant kTmu[] = {
-    {4, 8, dtu::hopf_union_tmg_kernel<4, 8>, dtu::smem_bytes<4, 8>},
-    {4, 12, dtu::hopf_union_tmg_kernel<4, 12>, dtu::smem_bytes<4, 12>},
-    {4, 16, dtu::hopf_union_tmg_kernel<4, 16>, dtu::smem_bytes<4, 16>},
-    {8, 16, dtu::hopf_union_tmg_kernel<8, 16>, dtu::smem_bytes<8, 16>},
-    {16, 16, dtu::hopf_union_tmg_kernel<16, 16>, dtu::smem_bytes<16, 16>}};
+#define HOPF_TMU(G_, C_)                                                                     \
+  {G_, C_, {dtu::hopf_union_tmg_kernel<G_, C_, false>, dtu::hopf_union_tmg_kernel<G_, C_, true>}, \
+   {dtu::smem_bytes<G_, C_, false>, dtu::smem_bytes<G_, C_, true>}}
+extern const TmuVariant kTmu[] = {HOPF_TMU(4, 8), HOPF_TMU(4, 12), HOPF_TMU(4, 16), HOPF_TMU(8, 16),
+                                  HOPF_TMU(16, 16)};
 extern const int kTmuCount = 5;
 }  // namespace hopf

@@ -833,14 +833,14 @@ def _guarded(shape, fill, pad=256, dtype=None):
     return buf, buf[pad:pad + numel].view(shape)
 
 
-@pytest.mark.parametrize("family", ["tm", "tmg", "tmg_unaligned", "reg", "tmu", "dense"])
+@pytest.mark.parametrize("family", ["tm", "tmg", "tmg_unaligned", "reg", "tmu", "tmu_unaligned", "dense"])
 def test_kernels_stay_in_bounds_and_are_deterministic(hb, family):
     """Inputs sit between NaN margins and outputs between sentinel margins: a kernel that reads
     outside its rows would pull NaN into a valid result (compared bitwise with a clean run), one
     that writes outside would change a sentinel.  Two runs must agree bit for bit (races)."""
     import torch
     name, M, n = {"tm": ("c3", 700, None), "tmg": ("c2", 3001, None), "tmg_unaligned": ("c2", 3001, 90),
-                  "reg": ("c2", 3001, 22), "tmu": ("c5", 1001, None), "dense": ("c4", 1001, None)}[family]
+                  "reg": ("c2", 3001, 22), "tmu": ("c5", 1001, None), "tmu_unaligned": ("c5", 1001, 63), "dense": ("c4", 1001, None)}[family]
     wl = inputs.config(name, M=M, n=n)
     X, t = inputs.points(wl)
     n = wl.n
@@ -860,7 +860,7 @@ def test_kernels_stay_in_bounds_and_are_deterministic(hb, family):
             phi, grad = torch.empty(M, device="cuda"), torch.empty((M, n), device="cuda")
             it = torch.empty(M, dtype=torch.int32, device="cuda")
             bufs = []
-        if family == "tmu":
+        if family.startswith("tmu"):
             if guard:
                 by, Y = _guarded((M, n), SENT)
                 bk, ks = _guarded((M,), 777, dtype=torch.int32)
@@ -895,7 +895,7 @@ def test_kernels_stay_in_bounds_and_are_deterministic(hb, family):
     b, kb = run(False)
     c, _ = run(True)
     expect = {"tm": "hopf_diag_tm_kernel", "tmg": "hopf_diag_tmg_kernel", "tmg_unaligned": "hopf_diag_tmg_kernel",
-              "reg": "hopf_diag_kernel", "tmu": "hopf_union_tmg_kernel", "dense": "hopf_dense_tc3_kernel"}[family]
+              "reg": "hopf_diag_kernel", "tmu": "hopf_union_tmg_kernel", "tmu_unaligned": "hopf_union_tmg_kernel", "dense": "hopf_dense_tc3_kernel"}[family]
     assert ka.startswith(expect) and kb.startswith(expect), (ka, kb)
     for u, v, w in zip(a, b, c):
         assert torch.equal(u.nan_to_num(0.25), v.nan_to_num(0.25)), f"{family}: guarded run differs"
@@ -954,10 +954,13 @@ def test_tmg_unaligned_rows(hb, n, h):
 
 
 @pytest.mark.parametrize("n,K", [(32, 5), (44, 9), (48, 3), (64, 16), (56, 24), (100, 8), (128, 4),
-                                 (200, 3), (256, 2)])
+                                 (200, 3), (256, 2),
+                                 # rows that do not start on a 16-byte boundary (every head / tail)
+                                 (25, 4), (45, 7), (63, 16), (97, 5), (99, 3), (127, 6), (201, 2), (255, 3)])
 def test_tmu_every_instance(hb, n, K):
-    """K4g (union, l2) at its widths 4x{8, 12, 16}, 8x16, 16x16: phi, grad, y, k*, phi_k against the oracle,
-    with t == 0 and an invalid point; and its distance mode against the oracle's Newton."""
+    """K4g (union, l2) at its widths 4x{8, 12, 16}, 8x16, 16x16 and at n % 4 != 0: phi, grad, y, k*,
+    phi_k against the oracle, with t == 0 and an invalid point; and its distance mode against the
+    oracle's Newton."""
     rng = np.random.default_rng(n * 11 + K)
     Ck = (rng.standard_normal((K, n)) * 2.0).astype(np.float32)
     a = rng.uniform(0.5, 2.0, (K, n))
