@@ -159,11 +159,12 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // row pitch (floats) of the per-group shared buffers: >= the variant's padded width, a
-// multiple of 4 (16-byte bulk copies) and = G mod 32, so that the strided reads / writes of a
-// warp (lane gl of group g at g * pitch + gl + G j) hit 32 different banks
+// multiple of 4 (16-byte bulk copies) and an odd multiple of G (G >= 4), so that the strided
+// reads / writes of a warp (lane gl of group g at g * pitch + gl + G j) hit 32 different banks:
+// g * pitch mod 32 then runs over the 32 / G distinct multiples of G
 __host__ __device__ constexpr int row_pitch(int w, int G) {
   int r = (w + 3) & ~3;
-  while ((r & 31) != (G & 31)) r += 4;
+  while (r % G != 0 || (r / G) % 2 == 0) r += 4;
   return r;
 }
 template <int G, int CPL>
@@ -172,9 +173,10 @@ __host__ __device__ constexpr size_t smem_bytes() {
          (size_t)(THREADS / G) * 8;
 }
 
-// The rows of X and grad must be 16-byte aligned (n % 4 == 0, aligned bases; the dispatcher in
-// tmg_api.cu checks): x of a group's next point is prefetched into shared memory by a bulk copy
-// one point ahead, and grad leaves through a shared buffer by a bulk store.
+// The bases of X and grad must be 16-byte aligned (the dispatcher in tmg_api.cu checks): x of a
+// group's next point is prefetched into shared memory by a bulk copy one point ahead (plus up to
+// 3 plain loads for a row end off the 16-byte grid), and grad leaves through a shared buffer by a
+// bulk store (plus up to 3 plain stores at each end).
 template <int G, int CPL, int HK, bool BULK>
 #ifndef HOPF_TMG_MINB
 #define HOPF_TMG_MINB 4
