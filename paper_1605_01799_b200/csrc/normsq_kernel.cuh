@@ -50,20 +50,27 @@ struct NormsqParams {
 template <int G, int CPL>
 __device__ __forceinline__ float active_set_root(const float (&z)[CPL], float a, float c, float e,
                                                  float m, bool act) {
-  float me = m;   // evaluation point
-  for (int nit = 0;; nit++) {
-    // S(me) = sum max(|z_i| - me, 0) summed as small terms, and the Newton step in delta form
-    // me + F(me) / (a |A| + c): S_A - |A| me would cancel catastrophically when the root sits
-    // just below a cluster of |z_i| (tiny t / clamped coordinates)
-    float sa = 0.f, na = 0.f;
+  // S(me) = sum max(|z_i| - me, 0) summed as small terms and the active count |A| = #{|z_i| > me}
+  // (group totals).  Both on the FMA pipe (this kernel is ALU-bound): max(x, 0) = (x + |x|) / 2
+  // (exact), and [x > 0] = sat(x 2^126) (exact: under FTZ a positive x is >= 2^-126)
+  auto eval = [&](float me, float &sa, float &na) {
+    float s2 = 0.f, cn = 0.f;
 #pragma unroll
     for (int j = 0; j < CPL; j++) {
       const float ex = fabsf(z[j]) - me;
-      sa += fmaxf(ex, 0.f);
-      na += ex > 0.f ? 1.f : 0.f;
+      s2 += ex + fabsf(ex);
+      cn += __saturatef(ex * 8.50705917e37f);
     }
-    sa = group_sum<G>(sa);
-    na = group_sum<G>(na);
+    sa = 0.5f * group_sum<G>(s2);
+    na = group_sum<G>(cn);
+  };
+  float me = m;   // evaluation point
+  float sa, na;
+  eval(me, sa, na);
+  for (int nit = 0;; nit++) {
+    // Newton step in delta form me + F(me) / (a |A| + c): S_A - |A| me would cancel
+    // catastrophically when the root sits just below a cluster of |z_i| (tiny t / clamped
+    // coordinates)
     float mn = me;
     if (act) {
       const float den = fmaf(a, na, c);
@@ -82,20 +89,19 @@ __device__ __forceinline__ float active_set_root(const float (&z)[CPL], float a,
       zm = group_max<G>(zm);
       if (act && na == 0.f) mn = fmaxf(__fdividef(fmaf(a, zm, -e), a + c), 0.f);
     }
-    bool cross = false;
-#pragma unroll
-    for (int j = 0; j < CPL; j++) {
-      const float az = fabsf(z[j]);
-      cross |= (az > me) != (az > mn);
-    }
-    cross = group_any<G>(cross);
     // a breakpoint at the root (|z_i| = m: coordinates clamped exactly at the multiplier, the
     // typical state of these l1 / l_inf problems near convergence) makes fp32 steps alternate
     // across it; a step within a few ulps of m is accepted as the root
     const bool tiny = fabsf(mn - me) <= HOPF_TINY_STEP * fmaxf(mn, 1e-30f);
-    if (act && (!cross || tiny || nit >= 63)) { m = mn; act = false; }
+    if (act && (tiny || nit >= 63)) { m = mn; act = false; }
     if (!__any_sync(0xffffffffu, act)) break;
-    if (act) me = mn;
+    // the step is exact when no |z_i| lies between me and mn, i.e. when the active count at mn
+    // equals the one at me; otherwise the evaluation at mn is the next Newton evaluation
+    float sn, nn;
+    eval(mn, sn, nn);
+    if (act && nn == na) { m = mn; act = false; }
+    if (!__any_sync(0xffffffffu, act)) break;
+    if (act) { me = mn; sa = sn; na = nn; }
   }
   return m;
 }
