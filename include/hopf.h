@@ -43,6 +43,14 @@
  *    otherwise consists of write-once caches (SM count, kernel attributes per device) and the
  *    per-thread error string / launch statistics.  All device pointers of a call, and a dense
  *    plan, must belong to the CURRENT device (hopf_eval_dense checks the plan's).
+ *  - Point counter: long launches of the persistent kernels hand out points from a 64-bit
+ *    counter in the same stream-ordered scratch (zeroed by a memset on `stream`); the
+ *    environment variable HOPF_CLAIMS=0 / 1 forces the static point stride / the counter.
+ *  - CUDA graphs: every device entry point is purely stream-ordered (scratch allocation and
+ *    free, memsets and kernels on `stream`; no host synchronisation), so a call may be captured
+ *    into a CUDA graph and replayed (make one uncaptured call first: it sets kernel attributes
+ *    and warms the scratch pool).  hopf_eval_diag_host and hopf_dense_plan_create synchronise
+ *    and cannot be captured.
  */
 #ifndef HOPF_H_
 #define HOPF_H_

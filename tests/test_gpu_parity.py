@@ -1064,3 +1064,65 @@ def test_point_claims_match_static(hb, family, monkeypatch):
     assert hb.last_kernel().startswith(kern), hb.last_kernel()
     for u, v in zip(a, b):   # (the static path itself is parity-tested against the oracle)
         assert torch.equal(u.nan_to_num(0.25), v.nan_to_num(0.25)), family
+
+
+# ----------------------------------------------------------------- CUDA graph capture
+@pytest.mark.parametrize("family", ["tmg", "tm", "tmu", "distance", "dense", "normsq", "reg"])
+def test_cuda_graph_capture_and_replay(hb, family, monkeypatch):
+    """Every call of the hot path is stream-ordered (scratch from a stream-ordered pool, a memset
+    for the launch's point counter, the kernels), so it captures into a CUDA graph; replaying the
+    graph on new inputs copied into the captured buffers gives the eager results bit for bit."""
+    import torch
+    monkeypatch.setenv("HOPF_CLAIMS", "1")   # include the counter's memset node
+    rng = np.random.default_rng(hash(family) % 2**32)
+    if family in ("tmg", "tm", "reg"):
+        n, M = {"tmg": (100, 4000), "tm": (700, 600), "reg": (20, 4000)}[family]
+        D = dev(rng.uniform(0.5, 2.0, n).astype(np.float32))
+        w = dev(rng.uniform(0.5, 1.5, n).astype(np.float32))
+        mk = lambda: (rng.normal(scale=2.0, size=(M, n)).astype(np.float32),
+                      rng.uniform(0.0, 2.0, M).astype(np.float32))
+        fn = lambda X, t: hb.eval_diag(X, t, D, None, -0.5, "wl1", w)
+        kern = {"tmg": "hopf_diag_tmg_kernel", "tm": "hopf_diag_tm_kernel", "reg": "hopf_diag_kernel"}[family]
+    elif family in ("tmu", "distance"):
+        n, K, M = 64, 5, 2000
+        Ck = dev((rng.standard_normal((K, n)) * 2.0).astype(np.float32))
+        Dk = dev((rng.uniform(0.5, 2.0, (K, n)) ** 2).astype(np.float32))
+        gk = dev(rng.uniform(-0.7, -0.3, K).astype(np.float32))
+        mk = lambda: ((rng.standard_normal((M, n)) * 3.0).astype(np.float32),
+                      rng.uniform(0.0, 2.0, M).astype(np.float32))
+        if family == "tmu":
+            fn = lambda X, t: hb.eval_union(X, t, Dk, Ck, gk, "l2", want_phik=True)
+            kern = "hopf_union_tmg_kernel<l2>"
+        else:
+            fn = lambda X, t: hb.distance_union(X[:500], Dk, Ck, gk)
+            kern = "hopf_union_tmg_kernel<l2, distance>"
+    elif family == "dense":
+        wl = inputs.config("c4", M=1500)
+        plan = hb.DensePlan(wl.Q, wl.Lam)
+        M, n = 1500, 256
+        mk = lambda: (rng.normal(size=(M, n)).astype(np.float32), rng.uniform(0.1, 1.0, M).astype(np.float32))
+        fn = lambda X, t: hb.eval_dense(X, t, plan, wl.gamma, "l1")
+        kern = "hopf_dense_tc3_kernel"
+    else:
+        M, n = 3000, 16
+        mk = lambda: (rng.uniform(-10, 10, (M, n)).astype(np.float32), rng.uniform(0, 10, M).astype(np.float32))
+        fn = lambda X, t: hb.eval_normsq(X, t, "l1sq", 0.0, "linf")
+        kern = "hopf_normsq_kernel"
+    X1, t1 = mk()
+    X2, t2 = mk()
+    Xd, td = dev(X1), dev(t1)
+    fn(Xd, td)                      # warm-up: function attributes, the scratch pool
+    torch.cuda.synchronize()
+    assert hb.last_kernel().startswith(kern), hb.last_kernel()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        static = fn(Xd, td)
+    Xd.copy_(torch.from_numpy(X2))
+    td.copy_(torch.from_numpy(t2))
+    g.replay()
+    torch.cuda.synchronize()
+    got = [x.clone() for x in static if x is not None]
+    ref = [x.clone() for x in fn(dev(X2), dev(t2)) if x is not None]
+    torch.cuda.synchronize()
+    for u, v in zip(got, ref):
+        assert torch.equal(u.nan_to_num(0.25), v.nan_to_num(0.25)), family
