@@ -18,18 +18,18 @@ extern thread_local unsigned long long *g_iter_counter;
 using NormsqFn = void (*)(const NormsqParams);
 struct NormsqVariant {
   int G, CPL;
-  NormsqFn fn[2];   // [J kind]
+  NormsqFn fn[2][5];   // [J kind][H kind] (no ELL)
 };
-#define HOPF_NSQ_VARIANT(G_, C_) \
-  {G_, C_, {hopf_normsq_kernel<G_, C_, JK_L1SQ>, hopf_normsq_kernel<G_, C_, JK_LINFSQ>}}
+#define HOPF_NSQ_JH(G_, C_, J_)                                                                \
+  {hopf_normsq_kernel<G_, C_, J_, HK_L1>, hopf_normsq_kernel<G_, C_, J_, HK_WL1>,              \
+   hopf_normsq_kernel<G_, C_, J_, HK_L2>, nullptr, hopf_normsq_kernel<G_, C_, J_, HK_LINF>}
+#define HOPF_NSQ_VARIANT(G_, C_) {G_, C_, {HOPF_NSQ_JH(G_, C_, JK_L1SQ), HOPF_NSQ_JH(G_, C_, JK_LINFSQ)}}
 // thread per point up to n = 8, pairs of lanes up to 16 (the paper's Tables 2, 3 and 5 use
 // n = 4..16; at n = 16 (t5): (2, 8) 24.7 ms, (4, 4) 29.5, (1, 16) 31.6, (8, 2) 40.3, (4, 16) 77.5),
 // then groups
 static const NormsqVariant kNormsqVariants[] = {
     HOPF_NSQ_VARIANT(1, 4),  HOPF_NSQ_VARIANT(1, 8),   HOPF_NSQ_VARIANT(2, 8),
-    HOPF_NSQ_VARIANT(4, 16), HOPF_NSQ_VARIANT(16, 16), HOPF_NSQ_VARIANT(32, 16),
-    // alternatives (HOPF_NSQ_VARIANT=G,CPL selects one; experiments)
-    HOPF_NSQ_VARIANT(1, 16), HOPF_NSQ_VARIANT(4, 4),   HOPF_NSQ_VARIANT(8, 2)};
+    HOPF_NSQ_VARIANT(4, 16), HOPF_NSQ_VARIANT(16, 16), HOPF_NSQ_VARIANT(32, 16)};
 }  // namespace hopf
 
 using namespace hopf;
@@ -65,7 +65,7 @@ extern "C" int hopf_eval_normsq(int64_t M, int32_t n, const float *X, const floa
   p.M = M; p.n = n; p.X = X; p.t = t; p.w = h == HOPF_H_WL1 ? w : nullptr;
   p.gamma = gamma; p.lambda = lambda; p.tol = tol; p.max_iter = max_iter; p.h = (int)h;
   p.phi = phi; p.grad = grad; p.iters = iters; p.iter_total = g_iter_counter;
-  NormsqFn fn = v->fn[(int)j];
+  NormsqFn fn = v->fn[(int)j][(int)h];
   const int threads = 128;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0) != cudaSuccess || per_sm < 1)

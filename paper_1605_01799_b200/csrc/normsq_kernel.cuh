@@ -106,7 +106,8 @@ __device__ __forceinline__ float active_set_root(const float (&z)[CPL], float a,
   return m;
 }
 
-template <int G, int CPL, int JK>
+// H is a template parameter (HKr): the loop body carries only its own prox
+template <int G, int CPL, int JK, int HKr>
 __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(const NormsqParams p) {
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
@@ -115,7 +116,6 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
   const int n = p.n;
   const float lam = p.lambda, ilam = 1.f / p.lambda, tol = p.tol;
   const int jmax = (n - gl + G - 1) / G;
-  const int HKr = p.h;
 
   float x[CPL], d[CPL], b[CPL], v[CPL], wr[CPL];
   // points: the first two of a group static (gid, gid + ngroups), later ones claimed by the
@@ -193,12 +193,12 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
     }
     // ---- (3.4b): d' = prox_{(t/lambda) H}(u) ------------------------------------------------
     float s2 = 0.f;
-    if (HKr == HK_L2) {
+    if constexpr (HKr == HK_L2) {
 #pragma unroll
       for (int j = 0; j < CPL; j++) s2 = fmaf(u[j], u[j], s2);
       s2 = group_sum<G>(s2);
     }
-    if (HKr == HK_LINF) {
+    if constexpr (HKr == HK_LINF) {
       const float m0 = fmaxf(mu + dmu, 0.f);
       const float mn = active_set_root<G, CPL>(u, 1.f, 0.f, tau, m0, act);
       if (act) { dmu = mn - mu; mu = mn; }
@@ -208,8 +208,8 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
 #pragma unroll
     for (int j = 0; j < CPL; j++) {
       float dn;
-      if (HKr == HK_L2) dn = sh * u[j];
-      else if (HKr == HK_LINF) dn = fminf(fmaxf(u[j], -mu), mu);
+      if constexpr (HKr == HK_L2) dn = sh * u[j];
+      else if constexpr (HKr == HK_LINF) dn = fminf(fmaxf(u[j], -mu), mu);
       else {
         const float th = (HKr == HK_WL1 ? wr[j] : 1.f) * tau;
         dn = u[j] - fminf(fmaxf(u[j], -th), th);         // shrink_1 (Moreau)
@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(128, CPL <= 8 ? 4 : 3) hopf_normsq_kernel(cons
       sd = fmaf(dd, dd, sd);
       const float dmv = dn - v[j];
       sb = fmaf(dmv, dmv, sb);
-      if (act) { d[j] = dn; b[j] = u[j] - dn; }          // (3.4c): b + v - d' = u - d'
+      d[j] = dn;                                         // (inactive groups: values unused)
+      b[j] = u[j] - dn;                                  // (3.4c): b + v - d' = u - d'
     }
     float r3;
     bool ok_sd, ok_sb, ok_sv;
