@@ -168,6 +168,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   int spec = 0;
   float s_cur = 1.f;
   bool sv_ok = false;
+  bool dfull = true;    // l2: d holds -d_k (else u_k is parked in T_U and s_prev = s_k)
+  float s_prev = 1.f;
 
   // load the point and set up the solve: x_hat, v -> TMEM; d, b -> registers (reading R5).
   // All global loads are issued first (x into d, D into b: both are dead at this point), so
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     it = 0;
     s_cur = 1.f;
     sv_ok = false;
+    dfull = true;
   };
   start_point(have);
 
@@ -240,8 +243,22 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   while (have) {   // one point per warp: `have` is warp-uniform
     float2 a0 = splat2(0.f), b0 = a0, c0 = a0, r0 = a0;   // one packed accumulator per sum
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
-    const float2 nsP = splat2(-s_cur), omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
+    const float2 omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
     const bool full_test = (HK != HK_L2) || sv_ok;   // see hopf_diag_kernel: exact
+    // l2: -d_k = -s_k u_k from the u_k a non-final trip parked in T_U (when a final trip or the
+    // finalize needs it; a non-final trip does not form d: 7 -> 6 packed ops per pair)
+    auto fix_d = [&]() {
+      const float2 ns = splat2(-s_prev);
+      static_for4([&](auto ci) {
+        constexpr int c = decltype(ci)::value;
+        float uk[1][8];
+        ld8o<96 + 8 * c>(tl0, uk[0]);
+        wait_ld(uk);
+#pragma unroll
+        for (int e2 = 0; e2 < 4; e2++)
+          d[4 * c + e2] = __fmul2_rn(ns, make_float2(uk[0][2 * e2], uk[0][2 * e2 + 1]));
+      });
+    };
     auto trip = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
       static_for4([&](auto ci) {
@@ -251,6 +268,11 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         ld8o<0 + 8 * c>(tl0, ch[1]);           // T_XH
         ld8o<32 + 8 * c>(tl0, ch[2]);          // T_V
         if constexpr (HK == HK_WL1) ld8o<96 + 8 * c>(tl0, ch[3]);   // T_TAU
+        if constexpr (HK == HK_L2 && !FULL) {   // u_k of the chunk -> T_U (l2 leaves 96-127 free)
+          const float uk[8] = {b[4 * c].x, b[4 * c].y, b[4 * c + 1].x, b[4 * c + 1].y,
+                               b[4 * c + 2].x, b[4 * c + 2].y, b[4 * c + 3].x, b[4 * c + 3].y};
+          st8o<96 + 8 * c>(tl0, uk);
+        }
         wait_ld(ch);
 #pragma unroll
         for (int e2 = 0; e2 < 4; e2++) {
@@ -268,15 +290,12 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
               d[q] = sub2(d[q], dd);                                // -d_k
               const float2 dmv = add2(d[q], v);                     // v^k - d^k
               a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0);
-            } else {
-              d[q] = __fmul2_rn(nsP, u);                            // -d_k
-            }
-            const float2 bk = __fmul2_rn(omsP, u);                  // b_k
+            }   // non-final trip: u_k went to TMEM (T_U) at the chunk start instead of forming -d_k
             const float2 na = __fmul2_rn(na_sP, u);                 // -(d_k - b_k)
             const float2 vn = fma2(kq, na, xh);                     // (3.4a): v_{k+1}
             const float2 dv = sub2(vn, v);                          // v_{k+1} - v_k
             v = vn;
-            b[q] = add2(v, bk);                                     // u_{k+1} = v_{k+1} + b_k
+            b[q] = fma2(omsP, u, v);                                // u_{k+1} = v_{k+1} + b_k, b_k = (1 - s_k) u_k
             c0 = fma2(dv, dv, c0);          // one packed accumulator per sum: the loop has ample
             r0 = fma2(b[q], b[q], r0);      // independent work, and the serial tail is shorter
           } else {
@@ -299,8 +318,13 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         st8o<32 + 8 * c>(tl0, ch[2]);          // T_V
       });
     };
+    if (HK == HK_L2 && full_test && !dfull) fix_d();
     if (full_test) trip(std::true_type{});
     else trip(std::false_type{});
+    if (HK == HK_L2) {
+      dfull = full_test;
+      if (!full_test) s_prev = s_cur;
+    }
 
     bool conv;
     int kdone;
@@ -346,6 +370,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
 
     // ---- finalize: phi = <x - c, d> - 1/2 <d, D d> - t H(d) + gamma ((3.3) at d, R2); grad ----
     // t == 0: phi = J(x), grad = D^{-1}(x - c) (reading R6); invalid input: NaN (R6)
+    if (HK == HK_L2 && !dfull) fix_d();
     float qs = 0.f, hsum = 0.f;
     float *grow = p.grad + pt * (int64_t)n;
 #pragma unroll
