@@ -382,7 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         advance(dpt, q, tq);
         begin(q, tq, M_START_LD);
       } else {
-        if (lane == 0) mbar_wait_hint(bar_red + 8 * (q & 1), (r - 1) & 1);
+        mbar_wait_hint(bar_red + 8 * (q & 1), (r - 1) & 1);   // the whole warp waits (no divergent wait + reconvergence)
         __syncwarp();
         float s4[4] = {0.f, 0.f, 0.f, 0.f};
         const float4 *rp = red + (size_t)((r - 1) & 1) * 8 * PTS + pl;
@@ -445,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const float tcur = st ? 0.f : tt * ilam, told = (st || fst) ? 0.f : tt * ilam;
       // ---- wait for MMA r (v^k in D[r % 3]) or termination -----------------------------------
       if (r > 0) {
-        if (lane == 0) mbar_wait_hint(bar_mma, (r - 1) & 1);
+        mbar_wait_hint(bar_mma, (r - 1) & 1);
         __syncwarp();
         if (mbar_test(bar_term, 0)) break;
         asm volatile("tcgen05.fence::after_thread_sync;");
