@@ -116,7 +116,13 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   const int64_t ngroups = ((int64_t)gridDim.x * blockDim.x) / G;
   const int n = p.n;
   const float lam = p.lambda, tol = p.tol;
-  const int jmax = (n - gl + G - 1) / G;   // slots j < jmax are real coordinates
+  // slot j of lane gl is coordinate 128 (j / 4) + 4 gl + j % 4: four contiguous coordinates per
+  // lane and block of 128, so x rows load and grad rows store as float4 (vrow) when rows are
+  // 16-byte aligned; the valid slots are a prefix j < jmax of every lane's 32
+  const int jmax = 4 * (n >> 7) + min(4, max(0, (n & 127) - 4 * gl));
+  auto cidx = [&](int j) { return 128 * (j >> 2) + 4 * gl + (j & 3); };
+  const bool vrow = (n & 3) == 0 && ((reinterpret_cast<uintptr_t>(p.X) | reinterpret_cast<uintptr_t>(p.grad) |
+                                      reinterpret_cast<uintptr_t>(p.c)) & 15) == 0;
   float *const D_s = reinterpret_cast<float *>(dyn_smem);
   float *const w_s = reinterpret_cast<float *>(dyn_smem + 4096);
   float *const di_s = reinterpret_cast<float *>(dyn_smem + 8192);   // 1 / (D_i + lambda)
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     float kv[8];
 #pragma unroll
     for (int e = 0; e < 8; e++) {
-      const int j = 8 * c + e, i = gl + G * j;
+      const int j = 8 * c + e, i = cidx(j);
       kv[e] = (j < jmax) ? ksign * __fdividef(lam, D_s[i] + lam) : 0.f;
     }
     st8(T_K + 8 * c, kv);
@@ -182,20 +188,33 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       if (lane == 0 && p.claim) wclaim = atomicAdd(p.claim, 1ull);
     }
     const float *xrow = p.X + (active ? pt : 0) * (int64_t)n;
+    if (vrow) {   // rows on the 16-byte grid: one float4 per block of 128 (n % 4 == 0: all or none)
 #pragma unroll
-    for (int q = 0; q < NP; q++) {
-      const int j0 = 2 * q, j1 = 2 * q + 1;
-      const bool ok0 = active && j0 < jmax, ok1 = active && j1 < jmax;
-      d[q] = make_float2(ok0 ? __ldg(xrow + gl + G * j0) : 0.f, ok1 ? __ldg(xrow + gl + G * j1) : 0.f);
-      b[q] = make_float2(di_s[gl + G * j0], di_s[gl + G * j1]);   // padded slots: x = 0 anyway
+      for (int m = 0; m < 8; m++) {
+        const bool ok = active && 4 * m < jmax;
+        const float4 x4 = ok ? __ldg(reinterpret_cast<const float4 *>(xrow + 128 * m + 4 * gl))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        d[2 * m] = make_float2(x4.x, x4.y);
+        d[2 * m + 1] = make_float2(x4.z, x4.w);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NP; q++) {
+        const int j0 = 2 * q, j1 = 2 * q + 1;
+        const bool ok0 = active && j0 < jmax, ok1 = active && j1 < jmax;
+        d[q] = make_float2(ok0 ? __ldg(xrow + cidx(j0)) : 0.f, ok1 ? __ldg(xrow + cidx(j1)) : 0.f);
+      }
     }
+#pragma unroll
+    for (int q = 0; q < NP; q++)   // padded slots: x = 0 anyway
+      b[q] = *reinterpret_cast<const float2 *>(di_s + cidx(2 * q));
     if (p.c) {
 #pragma unroll
       for (int q = 0; q < NP; q++) {
         const int j0 = 2 * q, j1 = 2 * q + 1;
         const bool ok0 = active && j0 < jmax, ok1 = active && j1 < jmax;
-        d[q].x -= ok0 ? __ldg(p.c + gl + G * j0) : 0.f;
-        d[q].y -= ok1 ? __ldg(p.c + gl + G * j1) : 0.f;
+        d[q].x -= ok0 ? __ldg(p.c + cidx(j0)) : 0.f;
+        d[q].y -= ok1 ? __ldg(p.c + cidx(j1)) : 0.f;
       }
     }
     const float tl = tt / lam;
@@ -214,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         const float di = (e & 1) ? Dq.y : Dq.x;
         xh8[e] = xt * di;
         v8[e] = xt;                                     // v^0 = x - c
-        if (HK == HK_WL1) tau8[e] = (active && j < jmax) ? tl * w_s[gl + G * j] : 0.f;
+        if (HK == HK_WL1) tau8[e] = (active && j < jmax) ? tl * w_s[cidx(j)] : 0.f;
       }
       st8(T_XH + 8 * c, xh8);
       st8(T_V + 8 * c, v8);
@@ -376,7 +395,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
 #pragma unroll
     for (int q = 0; q < NP; q++) {   // D of this lane's slots into b (dead), loads in flight together
       const int j0 = 2 * q, j1 = 2 * q + 1;
-      b[q] = make_float2(j0 < jmax ? D_s[gl + G * j0] : 1.f, j1 < jmax ? D_s[gl + G * j1] : 1.f);
+      b[q] = make_float2(j0 < jmax ? D_s[cidx(j0)] : 1.f, j1 < jmax ? D_s[cidx(j1)] : 1.f);
     }
     // spec is warp-uniform (one point per warp): one branch outside the slot loops, and no
     // per-slot validity test in the sums (padded slots hold x_hat = 0 and d = 0, so they add 0;
@@ -403,7 +422,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
         qs = fmaf(xt, dq, qs);
         qs = fmaf(-0.5f * Dv * dq, dq, qs);
         if (HK == HK_L2) hsum = fmaf(dq, dq, hsum);
-        else if (HK == HK_WL1) hsum = fmaf(w_s[gl + G * (8 * c + e)], fabsf(dq), hsum);
+        else if (HK == HK_WL1) hsum = fmaf(w_s[cidx(8 * c + e)], fabsf(dq), hsum);
         else hsum += fabsf(dq);
         g8[e] = dq;
       }
@@ -411,9 +430,17 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
 #pragma unroll
         for (int e = 0; e < 8; e++) g8[e] = gnan;
       }
+      if (vrow) {
 #pragma unroll
-      for (int e = 0; e < 8; e++)
-        if (8 * c + e < jmax) grow[gl + G * (8 * c + e)] = g8[e];
+        for (int h = 0; h < 2; h++)
+          if (8 * c + 4 * h < jmax)
+            *reinterpret_cast<float4 *>(grow + 128 * (2 * c + h) + 4 * gl) =
+                make_float4(g8[4 * h], g8[4 * h + 1], g8[4 * h + 2], g8[4 * h + 3]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; e++)
+          if (8 * c + e < jmax) grow[cidx(8 * c + e)] = g8[e];
+      }
     }
     qs = group_sum<G>(qs);
     hsum = group_sum<G>(hsum);
