@@ -50,6 +50,15 @@
 namespace hopf {
 namespace tc3 {
 
+#ifdef HOPF_TC3_TRACE
+// timing-only build (tools/tc3_trace.py): clock64 stamps of rounds [TR0, TR0 + TRN) in CTA 0
+constexpr int TR0 = 200, TRN = 16, TRW = 40;
+__device__ long long g_trace[TRN][TRW];
+#define TC3_STAMP(r, k) do { if (blockIdx.x == 0 && (r) >= TR0 && (r) < TR0 + TRN) g_trace[(r) - TR0][(k)] = clock64(); } while (0)
+#else
+#define TC3_STAMP(r, k) do { } while (0)
+#endif
+
 constexpr int N_DIM = 256;
 constexpr int PTS = 64;                  // point slots per CTA (128 per pair)
 constexpr int EPI_WARPS = 16;
@@ -291,6 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // remote arrives are default .release.cta; the tensor core reads the peer's shared
           // memory through the async proxy after the writers' fence.proxy.async)
           mbar_wait_hint(bar_stage0 + 8 * s, r & 1);
+          TC3_STAMP(r + 1, s);   // MMA thread: stage s of round r+1's operand ready
           // the busy word is complete once stage 0 has arrived; its value is only needed
           // after the last stage, so the shared load stays off the MMA issue path
           if (s == 0) any_busy = busy[r & 1];
@@ -317,6 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           mbar_arrive_remote(mapa(bar_mma, 1));
           break;
         }
+        TC3_STAMP(r + 1, 4);     // last MMA of round r+1 issued
         asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                      :: "r"(bar_mma), "h"((uint16_t)3));
       }
@@ -383,6 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         begin(q, tq, M_START_LD);
       } else {
         mbar_wait_hint(bar_red + 8 * (q & 1), (r - 1) & 1);   // the whole warp waits (no divergent wait + reconvergence)
+        if (lane == 0 && (warp == 0 || warp == 15)) TC3_STAMP(r, 8 + (warp == 15) * 16);
         __syncwarp();
         float s4[4] = {0.f, 0.f, 0.f, 0.f};
         const float4 *rp = red + (size_t)((r - 1) & 1) * 8 * PTS + pl;
@@ -446,6 +458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // ---- wait for MMA r (v^k in D[r % 3]) or termination -----------------------------------
       if (r > 0) {
         mbar_wait_hint(bar_mma, (r - 1) & 1);
+        if (lane == 0 && (warp == 0 || warp == 15)) TC3_STAMP(r, 9 + (warp == 15) * 16);
         __syncwarp();
         if (mbar_test(bar_term, 0)) break;
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -544,6 +557,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) {
           if (rank == 0) mbar_arrive_local(bar_stage0 + 8 * s);
           else mbar_arrive_remote(stage_remote + 8 * s);
+          if (warp == 0 || warp == 15) TC3_STAMP(r, 10 + s + (warp == 15) * 16);
         }
         // the paper's three stopping sums of this stage, off the MMA chain
 #pragma unroll
@@ -571,6 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_local(bar_red + 8 * (q & 1));
+      if (lane == 0 && (warp == 0 || warp == 15)) TC3_STAMP(r, 14 + (warp == 15) * 16);
       if (fin && nxt < (int)p.M) {   // the next point of a finished slot: x into us now (START next round)
         const float4 *xr = reinterpret_cast<const float4 *>(p.X + nxt * (int64_t)N_DIM + cb);
 #pragma unroll
@@ -623,6 +638,12 @@ int dense_tc3_prepare(int n, const double *Ml, void **rows_dev, float *mscale_in
   *mscale_inv = (float)ldexp(1.0, -s);
   return HOPF_OK;
 }
+
+#ifdef HOPF_TC3_TRACE
+extern "C" int hopf_tc3_trace_dump(long long *out) {
+  return cudaMemcpyFromSymbol(out, tc3::g_trace, sizeof(tc3::g_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int dense_tc3_launch(const DenseParams &p, int hk, const void *rows, float mscale_inv,
                      int *fix_count, int *fix_list, cudaStream_t stream) {
