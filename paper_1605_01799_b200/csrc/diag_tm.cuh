@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
   int it = 0;
   float tt = 0.f, tauS = 0.f;
   int spec = 0;
+  int lim = 0;   // the solve stops at iteration lim at the latest: 0 for t == 0 / invalid input
   float s_cur = 1.f;
   bool sv_ok = false;
   bool dfull = true;    // l2: d holds -d_k (else u_k is parked in T_U and s_prev = s_k)
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     bad = __any_sync(0xffffffffu, bad);
     if (active) {
       spec = bad ? 2 : (tt == 0.f ? 1 : 0);
+      lim = spec ? 0 : max(p.max_iter, 1);
       tauS = tt / lam;
     }
     it = 0;
@@ -263,7 +265,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
     float2 a0 = splat2(0.f), b0 = a0, c0 = a0, r0 = a0;   // one packed accumulator per sum
     const float2 sP = splat2(s_cur), tP = splat2(tauS);
     const float2 omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
-    const bool full_test = (HK != HK_L2) || sv_ok;   // see hopf_diag_kernel: exact
+    // (warp votes make the per-trip predicates provably uniform: plain branches, no reconvergence)
+    const bool full_test = (HK != HK_L2) || __any_sync(0xffffffffu, sv_ok);   // see hopf_diag_kernel: exact
     // l2: -d_k = -s_k u_k from the u_k a non-final trip parked in T_U (when a final trip or the
     // finalize needs it; a non-final trip does not form d: 7 -> 6 packed ops per pair)
     auto fix_d = [&]() {
@@ -383,7 +386,8 @@ __global__ void __launch_bounds__(THREADS, 4) hopf_diag_tm_kernel(const DiagPara
       }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;");
-    if (!(spec != 0 || (kdone >= 1 && (conv || kdone >= p.max_iter)))) continue;
+    // spec != 0 stops at once; otherwise conv (which needs k >= 1) or the iteration limit
+    if (!__any_sync(0xffffffffu, conv || kdone >= lim)) continue;
     const int wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -p.max_iter));
     if (spec == 0) my_iters += (unsigned)kdone;
 
