@@ -36,7 +36,7 @@ using dtg::THREADS;
 // so up to 8 blocks fit the SM's 512 columns; registers and shared memory then set residency
 template <int CPL> struct Cols {
   static constexpr int R = CPL <= 16 ? 16 : 32;          // region width
-  static constexpr int XH = 0, V = R, K = 2 * R;
+  static constexpr int XH = 0, V = R, K = 2 * R, U = 3 * R;   // U: u_k parked by non-final trips
   static constexpr int ALLOC = 3 * R <= 64 ? 64 : 128;   // power of two >= 32
 };
 #ifndef HOPF_TMU_BLOCKS
@@ -61,7 +61,9 @@ __host__ __device__ constexpr size_t smem_bytes(int K) {
 // aligned case's code as it was: the unaligned bookkeeping cost C5 ~4 % when shared)
 template <int G, int CPL, bool UNAL>
 __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(const DiagParams p) {
-  constexpr int C_XH = Cols<CPL>::XH, C_V = Cols<CPL>::V, C_K = Cols<CPL>::K, TMEM_COLS = Cols<CPL>::ALLOC;
+  constexpr int C_XH = Cols<CPL>::XH, C_V = Cols<CPL>::V, C_K = Cols<CPL>::K, C_U = Cols<CPL>::U,
+                TMEM_COLS = Cols<CPL>::ALLOC;
+  static_assert(Cols<CPL>::U + Cols<CPL>::R <= Cols<CPL>::ALLOC, "u region inside the allocation");
   static_assert(G >= 2 && G <= 16 && (G & (G - 1)) == 0, "G in {2, 4, 8, 16}");
   static_assert(CPL % 2 == 0 && CPL <= 32 && (CPL % 8 == 0 || CPL % 8 == 2 || CPL % 8 == 4),
                 "CPL = 8 a + {0, 2, 4}, at most 32");
@@ -126,6 +128,12 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   int wstatus = 0, it = 0, lim = 0, spec = 0, kset = 0;
   float tt = 0.f, tauS = 0.f, s_cur = 1.f;
   bool sv_ok = false;
+  // A non-final trip does not form -d_k = -s_k u_k: it parks u_k in the TMEM region C_U and the
+  // warp-uniform dfull goes false; fix_d forms -d from there (per lane s_prev = s_k) when a final
+  // trip or a stopping set needs it.  A set start writes u := x - c_k with s_prev = 1, so the
+  // rule -d = -s_prev u holds for every group whenever dfull is false.
+  bool dfull = true;
+  float s_prev = 1.f;
   // distance mode (NEXT-1): non-null p.dist; the point is the query y, evaluated at
   // s_0 = 0 and then at the Newton iterates s_l (p.t is not read)
   const bool DIST = p.dist != nullptr;
@@ -172,13 +180,14 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
     const bool keep_any = __any_sync(0xffffffffu, have && !fresh);
     for_chunks<CPL>([&](auto ci, auto szc) {
       constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
-      float ch[3][8];
+      float ch[4][8];
 #pragma unroll
-      for (int e = 0; e < 8; e++) ch[0][e] = ch[1][e] = ch[2][e] = 0.f;
+      for (int e = 0; e < 8; e++) ch[0][e] = ch[1][e] = ch[2][e] = ch[3][e] = 0.f;
       if (keep_any) {
         ldn<SZ, C_XH + 8 * c>(tl0, ch[0]);
         ldn<SZ, C_V + 8 * c>(tl0, ch[1]);
         ldn<SZ, C_K + 8 * c>(tl0, ch[2]);
+        ldn<SZ, C_U + 8 * c>(tl0, ch[3]);
         wait_ld(ch);
       }
       if (fresh) {
@@ -191,6 +200,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
           ch[0][e] = xt * di;
           ch[1][e] = xt;
           ch[2][e] = -__fdividef(lam, Dc.x + lam);
+          ch[3][e] = xt;                          // u with s_prev = 1: -d^0 = -(x - c_k)
           float2 &dq = d[4 * c + (e >> 1)];
           float2 &bq = b[4 * c + (e >> 1)];
           if (e & 1) { dq.y = -xt; bq.y = xt; } else { dq.x = -xt; bq.x = xt; }
@@ -199,9 +209,11 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
       stn<SZ, C_XH + 8 * c>(tl0, ch[0]);
       stn<SZ, C_V + 8 * c>(tl0, ch[1]);
       stn<SZ, C_K + 8 * c>(tl0, ch[2]);
+      stn<SZ, C_U + 8 * c>(tl0, ch[3]);
     });
     asm volatile("tcgen05.wait::st.sync.aligned;");
     if (fresh) {
+      s_prev = 1.f;
       lim = spec ? 0 : p.max_iter;
       it = 0;
       s_cur = 1.f;
@@ -250,6 +262,20 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
   point_start(have);
   set_setup(have);
 
+  // -d = -s_prev u from the parked u_k (collective; every group, see dfull)
+  auto fix_d = [&]() {
+    const float2 ns = splat2(-s_prev);
+    for_chunks<CPL>([&](auto ci, auto szc) {
+      constexpr int c = decltype(ci)::value, SZ = decltype(szc)::value;
+      float uk[1][8];
+      ldn<SZ, C_U + 8 * c>(tl0, uk[0]);
+      wait_ld(uk);
+#pragma unroll
+      for (int e2 = 0; e2 < SZ / 2; e2++)
+        d[4 * c + e2] = __fmul2_rn(ns, make_float2(uk[0][2 * e2], uk[0][2 * e2 + 1]));
+    });
+    dfull = true;
+  };
   // a stopped set parks its d^k (grad := d, R1) in the candidate row; collective
   auto park = [&](bool stop) {
     if (stop) {
@@ -268,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
     const bool live = have && !waiting;
     float2 a0 = splat2(0.f), b0 = a0, c0 = a0, r0 = a0;
     const float2 sP = splat2(s_cur);
-    const float2 nsP = splat2(-s_cur), omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
+    const float2 omsP = splat2(1.f - s_cur), na_sP = splat2(1.f - 2.f * s_cur);
     const bool full_test = __any_sync(0xffffffffu, live && sv_ok);
     auto trip = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
@@ -278,6 +304,15 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
         ldn<SZ, C_K + 8 * c>(tl0, ch[0]);
         ldn<SZ, C_XH + 8 * c>(tl0, ch[1]);
         ldn<SZ, C_V + 8 * c>(tl0, ch[2]);
+        if constexpr (!FULL) {   // u_k of the chunk -> C_U (-d_k is formed only if needed)
+          float uk[8];
+#pragma unroll
+          for (int e2 = 0; e2 < 4; e2++) {
+            uk[2 * e2] = e2 < SZ / 2 ? b[4 * c + e2].x : 0.f;
+            uk[2 * e2 + 1] = e2 < SZ / 2 ? b[4 * c + e2].y : 0.f;
+          }
+          stn<SZ, C_U + 8 * c>(tl0, uk);
+        }
         wait_ld(ch);
 #pragma unroll
         for (int e2 = 0; e2 < SZ / 2; e2++) {
@@ -292,14 +327,11 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
             d[q] = sub2(d[q], dd);                                // -d_k
             const float2 dmv = add2(d[q], v);                     // v^k - d^k
             a0 = fma2(dd, dd, a0); b0 = fma2(dmv, dmv, b0);
-          } else {
-            d[q] = __fmul2_rn(nsP, u);                            // -d_k
           }
-          const float2 bk = __fmul2_rn(omsP, u);                  // b_k
           const float2 na = __fmul2_rn(na_sP, u);                 // -(d_k - b_k)
           const float2 vn = fma2(kq, na, xh);                     // (3.4a): v_{k+1}
           const float2 dv = sub2(vn, v);
-          b[q] = add2(vn, bk);                                    // u_{k+1} = v_{k+1} + b_k
+          b[q] = fma2(omsP, u, vn);                               // u_{k+1} = v_{k+1} + b_k, b_k = (1 - s_k) u_k
           c0 = fma2(dv, dv, c0);
           r0 = fma2(b[q], b[q], r0);
           ch[2][2 * e2] = vn.x;
@@ -308,8 +340,14 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
         stn<SZ, C_V + 8 * c>(tl0, ch[2]);
       });
     };
-    if (full_test) trip(std::true_type{});
-    else trip(std::false_type{});
+    if (full_test) {
+      if (!dfull) fix_d();
+      trip(std::true_type{});
+    } else {
+      trip(std::false_type{});
+      dfull = false;
+      s_prev = s_cur;
+    }
     {
       // group totals by a plain xor butterfly (every lane ends with every total: no broadcast, the
       // dependent chain is log2(G) shuffles deep); the stores of v drain meanwhile
@@ -348,6 +386,7 @@ __global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM) hopf_union_tmg_kernel(
         wstatus = spec == 2 ? INT32_MIN : (spec == 1 ? 0 : (conv ? kdone : -lim));
         if (spec == 0) my_iters += (unsigned)kdone;
       }
+      if (!dfull) fix_d();   // a set that stops at its limit after a non-final trip
       park(stop);
     }
     {
